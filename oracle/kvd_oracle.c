@@ -1,0 +1,368 @@
+/*
+ * kvd_oracle.c — CPU ORACLE for the KVDrive decode-step hot path.
+ *
+ *   *** TEST INFRASTRUCTURE ONLY. ***
+ *   Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ *   --impl reference legs may load this library.  The product path
+ *   (paper_2605_18071_b200/, libkvd.so) never links, imports or calls it,
+ *   and this file shares no code, header, table or constant with it.
+ *
+ * A plain, slow, obviously-correct restatement of what one decode step
+ * computes for one segment = one (request, layer, KV head), written from
+ * the paper (/root/reference/PAPER.md, cited as PAPER.md:<line>) and the
+ * binding readings of SURVEY.md §8.4.1 (listed again in DESIGN.md §3).
+ * No blocking, no fusion, no reordering beyond what the definitions say.
+ *
+ *   O1  or_block_summaries  mean key per block ("the mean key of each page
+ *                           is used as its representative")
+ *   O2  or_group_query      GQA query of a KV head (paper silent; reading R3)
+ *   O3  or_block_scores     query x summary dot product ("multiplying the
+ *                           query vector with ...")
+ *   O4  or_pinned_blocks    sink 4 + local 64 tokens always resident
+ *
+ *   O5  or_topk             top-k blocks ("retrieving only the Top-K
+ *                           important chunks")
+ *   O6  or_resolve          hit/miss against the GPU cache + eviction
+ *                           (LRU/LFU baselines PAPER.md:223,254,840-859;
+ *                           lookahead "entries with the lowest current-step
+ *                           attention scores are discarded")
+ *   O7  or_fetch            copy missed blocks host -> cache slot
+ *                           (sparse block-level fetch)
+ *   O8  or_attention        softmax attention over the selected tokens, in
+ *                           fp64 ("computing attention
+ *                           over the union of fetched and resident entries")
+ *
+ * Precision: the paper states none (its only dtype is "FP16" in future work,
+ * PAPER.md:1056).  Readings R2/R5 fix O1/O3 to fp32 with a stated order so
+ * that selected ids are reproducible bit for bit; O8 is fp64.
+ *
+ * Pins (tests/test_oracle_*.py) — every function here is pinned:
+ *   O1: P=1 => summary == key bit-exactly; dyadic keys => exact mean vs int64;
+ *       bf16 RNE vs torch.Tensor.bfloat16 (library routine).
+ *   O2/O3: SPEC worked examples; integer inputs vs int64 dot; fp64 error bound.
+ *   O4: hand-enumerated pinned sets.
+ *   O5: brute-force total-order check, sort-all, permutation equivariance,
+ *       P=1 => exact token top-k.
+ *   O6: independent Python LRU (OrderedDict two-phase) / LFU / LA simulators.
+ *   O7: memcmp invariant.
+ *   O8: k = all => dense softmax (torch SDPA fp64); closed-form special cases.
+ * Build: gcc -O2 -ffp-contract=off -fno-fast-math -shared -fPIC (no OpenMP).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------ bf16 */
+/* bf16 is the top 16 bits of an IEEE binary32. */
+static float bf16_to_f32(uint16_t h) {
+    uint32_t u = ((uint32_t)h) << 16;
+    float f;
+    memcpy(&f, &u, 4);
+    return f;
+}
+
+/* Round-to-nearest-even binary32 -> bf16 (reading R2).  NaN -> quiet NaN. */
+uint16_t or_f32_to_bf16_rne(float f) {
+    uint32_t u;
+    memcpy(&u, &f, 4);
+    if ((u & 0x7F800000u) == 0x7F800000u && (u & 0x007FFFFFu) != 0)
+        return (uint16_t)((u >> 16) | 0x0040u);          /* quiet NaN */
+    uint32_t lsb = (u >> 16) & 1u;
+    u += 0x7FFFu + lsb;                                   /* ties to even */
+    return (uint16_t)(u >> 16);
+}
+
+/* -------------------------------------------------------------- O1 summary */
+/* For block b with cnt_b = min(P, n - P*b) valid tokens and every dim j:
+ *   acc = +0f; for t = 0..cnt_b-1: acc = acc + f32(K[P*b+t][j])
+ *   S[b][j] = bf16_rne(acc / (float)cnt_b)
+ * K is token-major [n][d] bf16; S is block-major [nb][d] bf16. */
+void or_block_summaries(const uint16_t* K, int64_t n, int32_t d, int32_t P,
+                        uint16_t* S) {
+    int64_t nb = (n + P - 1) / P;
+    for (int64_t b = 0; b < nb; ++b) {
+        int64_t cnt = n - (int64_t)P * b;
+        if (cnt > P) cnt = P;
+        for (int32_t j = 0; j < d; ++j) {
+            float acc = 0.0f;
+            for (int64_t t = 0; t < cnt; ++t)
+                acc = acc + bf16_to_f32(K[((int64_t)P * b + t) * d + j]);
+            S[b * d + j] = or_f32_to_bf16_rne(acc / (float)cnt);
+        }
+    }
+}
+
+/* ---------------------------------------------------------- O2 group query */
+/* qbar[j] = ((+0 + q[0][j]) + q[1][j]) + ... + q[G-1][j]   (fp32, g ascending)
+ * q holds the G query heads of one KV head, [G][d] bf16. */
+void or_group_query(const uint16_t* q, int32_t G, int32_t d, float* qbar) {
+    for (int32_t j = 0; j < d; ++j) {
+        float acc = 0.0f;
+        for (int32_t g = 0; g < G; ++g) acc = acc + bf16_to_f32(q[(int64_t)g * d + j]);
+        qbar[j] = acc;
+    }
+}
+
+/* -------------------------------------------------------------- O3 scores */
+/* score_b = fma chain over j = 0..d-1 from +0:  acc = fmaf(qbar[j], S[b][j], acc).
+ * No 1/sqrt(d): ranking is invariant to a positive scale (reading R4). */
+void or_block_scores(const float* qbar, const uint16_t* S, int64_t nb, int32_t d,
+                     float* scores) {
+    for (int64_t b = 0; b < nb; ++b) {
+        float acc = 0.0f;
+        for (int32_t j = 0; j < d; ++j) acc = fmaf(qbar[j], bf16_to_f32(S[b * d + j]), acc);
+        scores[b] = acc;
+    }
+}
+
+/* ------------------------------------------------------------- O4 pinned */
+/* Sink: every block overlapping the first `sink` tokens, i.e. blocks
+ * 0 .. ceil(sink/P)-1.  Local: every block overlapping the last
+ * `local` tokens, i.e. blocks floor(max(0, n-local)/P) .. nb-1 when local > 0
+ * (reading R9: block-granular pinning of PAPER.md:685's 4 sink + 64 local).
+ * Writes is_pinned[nb] (0/1), returns the pinned count. */
+int64_t or_pinned_blocks(int64_t n, int32_t P, int32_t sink, int32_t local,
+                         uint8_t* is_pinned) {
+    int64_t nb = (n + P - 1) / P;
+    int64_t count = 0;
+    for (int64_t b = 0; b < nb; ++b) is_pinned[b] = 0;
+    for (int64_t b = 0; b < nb && (int64_t)P * b < sink; ++b) is_pinned[b] = 1;
+    if (local > 0) {
+        int64_t first_tok = n - local;
+        if (first_tok < 0) first_tok = 0;
+        for (int64_t b = first_tok / P; b < nb; ++b) is_pinned[b] = 1;
+    }
+    for (int64_t b = 0; b < nb; ++b) count += is_pinned[b];
+    return count;
+}
+
+/* --------------------------------------------------------------- O5 top-k */
+/* Total order (reading R10): score descending, NaN below everything, -0 == +0
+ * (IEEE equality), then block id ascending.  Candidates are the non-pinned
+ * blocks.  Output: the first k in that order, emitted ascending by id. */
+typedef struct { float s; int64_t id; } or_cand;
+
+static int or_score_better(float a, float b) {        /* a ranks strictly above b */
+    if (isnan(a)) return 0;
+    if (isnan(b)) return 1;
+    return a > b;
+}
+static int or_cand_cmp(const void* x, const void* y) {
+    const or_cand* a = (const or_cand*)x;
+    const or_cand* b = (const or_cand*)y;
+    if (or_score_better(a->s, b->s)) return -1;
+    if (or_score_better(b->s, a->s)) return 1;
+    return (a->id < b->id) ? -1 : (a->id > b->id);
+}
+static int or_i32_cmp(const void* x, const void* y) {
+    int32_t a = *(const int32_t*)x, b = *(const int32_t*)y;
+    return (a > b) - (a < b);
+}
+
+/* returns 0, or 2 (ERANGE) when k exceeds the candidate count */
+int32_t or_topk(const float* scores, int64_t nb, const uint8_t* is_pinned, int32_t k,
+                int32_t* ids) {
+    or_cand* c = (or_cand*)malloc(sizeof(or_cand) * (size_t)(nb > 0 ? nb : 1));
+    int64_t m = 0;
+    for (int64_t b = 0; b < nb; ++b)
+        if (!is_pinned[b]) { c[m].s = scores[b]; c[m].id = b; ++m; }
+    if (k < 0 || k > m) { free(c); return 2; }
+    qsort(c, (size_t)m, sizeof(or_cand), or_cand_cmp);
+    for (int32_t i = 0; i < k; ++i) ids[i] = (int32_t)c[i].id;
+    qsort(ids, (size_t)k, sizeof(int32_t), or_i32_cmp);
+    free(c);
+    return 0;
+}
+
+/* ------------------------------------------------------------- O6 resolve */
+/* One segment's GPU cache: C slots, a block table, per-slot metadata.
+ *   table[b]      slot holding block b, or -1
+ *   slot_block[s] block held by slot s, or -1 (free)
+ *   last_use[s], phase[s], use_count[s]  policy metadata of slot s's block
+ * Initial state (reading R14): fully resident if C >= nb (block b in slot b);
+ * otherwise cold: only the pinned blocks, in slots 0..p-1, ascending id. */
+enum { OR_LRU = 0, OR_LFU = 1, OR_LA = 2 };
+
+int32_t or_cache_init(int64_t nb, int64_t C, const uint8_t* is_pinned,
+                      int32_t* table, int32_t* slot_block, uint32_t* last_use,
+                      uint8_t* phase, uint32_t* use_count) {
+    for (int64_t b = 0; b < nb; ++b) table[b] = -1;
+    for (int64_t s = 0; s < C; ++s) { slot_block[s] = -1; last_use[s] = 0; phase[s] = 0; use_count[s] = 0; }
+    if (C >= nb) {
+        for (int64_t b = 0; b < nb; ++b) { table[b] = (int32_t)b; slot_block[b] = (int32_t)b; }
+        return 0;
+    }
+    int64_t s = 0;
+    for (int64_t b = 0; b < nb; ++b) {
+        if (!is_pinned[b]) continue;
+        if (s >= C) return 3;                                  /* ECAPACITY */
+        table[b] = (int32_t)s; slot_block[s] = (int32_t)b; ++s;
+    }
+    return 0;
+}
+
+typedef struct {
+    int64_t slot;
+    int64_t block;
+    uint32_t last, count;
+    uint8_t phase;
+    float score;
+    int policy;
+} or_victim;
+
+/* Policy keys, smallest evicted first (reading R12 / SURVEY §8.4 O6):
+ *   LRU: (last_use, phase, block)          LFU: (use_count, last_use, phase, block)
+ *   LA : (this step's score ascending with NaN lowest and -0 == +0, block descending) */
+static int or_victim_cmp(const void* x, const void* y) {
+    const or_victim* a = (const or_victim*)x;
+    const or_victim* b = (const or_victim*)y;
+    if (a->policy == OR_LA) {
+        if (or_score_better(b->score, a->score)) return -1;   /* a lower -> evict first */
+        if (or_score_better(a->score, b->score)) return 1;
+        return (a->block > b->block) ? -1 : (a->block < b->block);
+    }
+    if (a->policy == OR_LFU && a->count != b->count) return (a->count < b->count) ? -1 : 1;
+    if (a->last != b->last) return (a->last < b->last) ? -1 : 1;
+    if (a->phase != b->phase) return (a->phase < b->phase) ? -1 : 1;
+    return (a->block < b->block) ? -1 : (a->block > b->block);
+}
+
+/* Resolve step `step` for the selected set S (k ids, ascending, non-pinned):
+ *  (1) hits = {b in S : table[b] >= 0};  M = S \ hits, ascending
+ *  (2) F = free slots, ascending
+ *  (3) V = the first max(0, |M|-|F|) resident blocks not in S and not pinned,
+ *      by the policy key
+ *  (4) M[i] -> (F ++ V)[i]; each victim's table entry -> -1
+ *  (5) hits: last=step, phase=0, count+=1; admitted: last=step, phase=1, count=1
+ * Outputs:
+ *  attn[W][2]  (block, slot) for S u pinned, ascending by block, (-1,-1) padded
+ *  miss[k][2]  (block, slot) for M in order, (-1,-1) padded;  *n_miss
+ *  *n_hit      |hits| (selected, non-pinned)
+ * Returns 0, 3 (ECAPACITY: |M| > |F| + |evictable|), or 1 (EINVAL: S pinned/out of range). */
+int32_t or_resolve(int64_t nb, int64_t C, const uint8_t* is_pinned,
+                   int32_t* table, int32_t* slot_block, uint32_t* last_use,
+                   uint8_t* phase, uint32_t* use_count,
+                   const int32_t* S, int32_t k, uint32_t step, int32_t policy,
+                   const float* scores, int32_t W,
+                   int32_t* attn, int32_t* miss, int32_t* n_miss, int32_t* n_hit) {
+    uint8_t* in_S = (uint8_t*)calloc((size_t)(nb > 0 ? nb : 1), 1);
+    for (int32_t i = 0; i < k; ++i) {
+        if (S[i] < 0 || S[i] >= nb || is_pinned[S[i]]) { free(in_S); return 1; }
+        in_S[S[i]] = 1;
+    }
+    /* (1) */
+    int32_t* M = (int32_t*)malloc(sizeof(int32_t) * (size_t)(k > 0 ? k : 1));
+    int32_t nm = 0, nh = 0;
+    for (int32_t i = 0; i < k; ++i) {
+        if (table[S[i]] >= 0) ++nh; else M[nm++] = S[i];
+    }
+    /* (2) */
+    int64_t* dest = (int64_t*)malloc(sizeof(int64_t) * (size_t)(nm > 0 ? nm : 1));
+    int32_t nd = 0;
+    for (int64_t s = 0; s < C && nd < nm; ++s)
+        if (slot_block[s] < 0) dest[nd++] = s;
+    /* (3) */
+    if (nd < nm) {
+        or_victim* v = (or_victim*)malloc(sizeof(or_victim) * (size_t)C);
+        int64_t nv = 0;
+        for (int64_t s = 0; s < C; ++s) {
+            int32_t b = slot_block[s];
+            if (b < 0 || in_S[b] || is_pinned[b]) continue;
+            v[nv].slot = s; v[nv].block = b; v[nv].last = last_use[s];
+            v[nv].count = use_count[s]; v[nv].phase = phase[s];
+            v[nv].score = scores ? scores[b] : 0.0f; v[nv].policy = policy;
+            ++nv;
+        }
+        if (nv < nm - nd) { free(v); free(dest); free(M); free(in_S); return 3; }
+        qsort(v, (size_t)nv, sizeof(or_victim), or_victim_cmp);
+        for (int64_t i = 0; nd < nm; ++i) {
+            table[v[i].block] = -1;
+            dest[nd++] = v[i].slot;
+        }
+        free(v);
+    }
+    /* (4)+(5) */
+    for (int32_t i = 0; i < k; ++i) {
+        int32_t b = S[i];
+        if (table[b] >= 0) {                       /* hit (tables of victims already cleared;
+                                                      victims are never in S) */
+            int32_t s = table[b];
+            last_use[s] = step; phase[s] = 0; use_count[s] += 1;
+        }
+    }
+    for (int32_t i = 0; i < nm; ++i) {
+        int64_t s = dest[i];
+        table[M[i]] = (int32_t)s; slot_block[s] = M[i];
+        last_use[s] = step; phase[s] = 1; use_count[s] = 1;
+        miss[2 * i] = M[i]; miss[2 * i + 1] = (int32_t)s;
+    }
+    for (int32_t i = nm; i < k; ++i) { miss[2 * i] = -1; miss[2 * i + 1] = -1; }
+    /* attention list: S u pinned, ascending by block */
+    int32_t w = 0;
+    for (int64_t b = 0; b < nb; ++b) {
+        if (!(in_S[b] || is_pinned[b])) continue;
+        if (w >= W) { free(dest); free(M); free(in_S); return 3; }
+        attn[2 * w] = (int32_t)b; attn[2 * w + 1] = table[b];
+        ++w;
+    }
+    for (; w < W; ++w) { attn[2 * w] = -1; attn[2 * w + 1] = -1; }
+    *n_miss = nm; *n_hit = nh;
+    free(dest); free(M); free(in_S);
+    return 0;
+}
+
+/* --------------------------------------------------------------- O7 fetch */
+/* For each (block, slot) in miss: slot_pool[slot] := host_records[block]
+ * (record_bytes each; byte copy). */
+void or_fetch(const uint8_t* host_records, uint8_t* slot_pool, int64_t record_bytes,
+              const int32_t* miss, int32_t n_miss) {
+    for (int32_t i = 0; i < n_miss; ++i)
+        memcpy(slot_pool + (int64_t)miss[2 * i + 1] * record_bytes,
+               host_records + (int64_t)miss[2 * i] * record_bytes, (size_t)record_bytes);
+}
+
+/* ----------------------------------------------------------- O8 attention */
+/* For each query head g (of the G heads sharing this KV head): over the token
+ * set T = U_{b in blocks} {P*b + t : t < cnt_b}, in fp64 from the bf16 inputs:
+ *   z_i = (q_g . K_i) / sqrt(d);  m = max z;  p_i = exp(z_i - m);  l = sum p_i
+ *   o_g = sum p_i V_i / l  (stored fp32);  lse_g = m + ln l  (stored fp32)
+ * K, V token-major [n][d] bf16; q [G][d] bf16; blocks: nblk block ids (-1 skipped). */
+void or_attention(const uint16_t* q, int32_t G, int32_t d, const uint16_t* K,
+                  const uint16_t* V, int64_t n, int32_t P, const int32_t* blocks,
+                  int32_t nblk, float* o, float* lse) {
+    int64_t ntok = 0;
+    for (int32_t i = 0; i < nblk; ++i) if (blocks[i] >= 0) ntok += P;
+    int64_t* tok = (int64_t*)malloc(sizeof(int64_t) * (size_t)(ntok > 0 ? ntok : 1));
+    double* z = (double*)malloc(sizeof(double) * (size_t)(ntok > 0 ? ntok : 1));
+    double* acc = (double*)malloc(sizeof(double) * (size_t)d);
+    int64_t nt = 0;
+    for (int32_t i = 0; i < nblk; ++i) {
+        int64_t b = blocks[i];
+        if (b < 0) continue;
+        for (int64_t t = 0; t < P; ++t)
+            if ((int64_t)P * b + t < n) tok[nt++] = (int64_t)P * b + t;
+    }
+    const double scale = 1.0 / sqrt((double)d);
+    for (int32_t g = 0; g < G; ++g) {
+        double m = -INFINITY;
+        for (int64_t i = 0; i < nt; ++i) {
+            double s = 0.0;
+            for (int32_t j = 0; j < d; ++j)
+                s += (double)bf16_to_f32(q[(int64_t)g * d + j]) *
+                     (double)bf16_to_f32(K[tok[i] * d + j]);
+            z[i] = s * scale;
+            if (z[i] > m) m = z[i];
+        }
+        double l = 0.0;
+        for (int32_t j = 0; j < d; ++j) acc[j] = 0.0;
+        for (int64_t i = 0; i < nt; ++i) {
+            double p = exp(z[i] - m);
+            l += p;
+            for (int32_t j = 0; j < d; ++j) acc[j] += p * (double)bf16_to_f32(V[tok[i] * d + j]);
+        }
+        for (int32_t j = 0; j < d; ++j) o[(int64_t)g * d + j] = (float)(acc[j] / l);
+        if (lse) lse[g] = (float)(m + log(l));
+    }
+    free(tok); free(z); free(acc);
+}
