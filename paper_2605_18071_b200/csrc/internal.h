@@ -1,0 +1,106 @@
+// internal.h — libkvd's cache object and the launch interface of its kernels.
+// Layouts:
+//   slots      [L][R][Hkv][C] records; record = K[P][128] || V[P][128] bf16,
+//              each 256-B token row stored as 16 chunks of 16 B, chunk c of row
+//              t at position c ^ (t & 7)  (bank-conflict-free ldmatrix)
+//   host store [A][R][Hkv][nb_max] records (same layout), pinned + mapped
+//   summ       [L][R][Hkv][128][nb_pad] bf16, dim-major (row = one dim j)
+//   scores     [L][R][Hkv][nb_pad] fp32 (last select of that layer)
+//   table      [L][R][Hkv][nb_pad] int32 block -> slot | -1
+//   slot_block/last_use/phase/use_count [L][R][Hkv][C]
+//   miss       [R][Hkv][kmax] int2 (block, slot) + miss_count [R][Hkv]
+//   partials   [R][Hkv][max_splits][8][128] fp32 + (m, l) [R][Hkv][max_splits][8][2]
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <vector>
+
+#include "../../include/kvd.h"
+
+namespace kvd {
+
+constexpr int kScoreCols = 128;       // blocks per score-kernel tile (nb_pad multiple)
+constexpr int kAttnWarps = 4;         // warps per attention CTA
+constexpr int kAttnStages = 3;        // smem stages per warp
+constexpr int kTileBytes = 8192;      // one 16-token K||V tile
+constexpr int kSplitTiles = 16;       // 16-token tiles per split (one CTA)
+constexpr int64_t kSlotOfBytes = 64ll << 20;   // setup scratch for per-block slot targets
+
+struct SegGeom {                      // per-request pinned geometry (device copy in params)
+    int32_t n, nb, sink_end, local_begin;   // pinned = [0, sink_end) U [local_begin, nb)
+};
+
+struct StepParams {
+    int32_t B, layer, k, W;
+    int32_t R, Hkv, Hq, G, P, E;      // E = 16 / P list entries per 16-token tile
+    int64_t nb_pad, C, nb_max;
+    int32_t sink_tokens, local_tokens;
+    int32_t policy;
+    uint32_t step;
+    int32_t host_layer;
+    int32_t rec_bytes;
+    int32_t nsplit;
+    float scale_log2;
+    int32_t req[KVD_MAX_BATCH];
+};
+
+}  // namespace kvd
+
+struct kvd_cache {
+    kvd_config cfg;
+    int L, Hq, Hkv, G, P, R, kmax, pmax, A, E;
+    int64_t nmax, nb_max, nb_pad, C;
+    bool resident;
+    int64_t rec_bytes;
+    int max_splits;
+    // device
+    uint8_t* slots = nullptr;
+    uint16_t* summ = nullptr;
+    float* scores = nullptr;
+    int32_t* table = nullptr;
+    int32_t* slot_block = nullptr;
+    uint32_t* last_use = nullptr;
+    uint8_t* phase = nullptr;
+    uint32_t* use_count = nullptr;
+    int32_t* miss = nullptr;
+    int32_t* miss_count = nullptr;
+    float* part_o = nullptr;
+    float* part_ml = nullptr;
+    uint32_t* split_ctr = nullptr;
+    unsigned long long* stats = nullptr;   // [5] kvd_stats fields
+    int32_t* err = nullptr;
+    int32_t* ntok_dev = nullptr;
+    uint8_t* zero_rec = nullptr;           // one zero record (padding entries)
+    // setup staging (lazily allocated)
+    uint16_t* stage_kv = nullptr;
+    uint8_t* stage_rec = nullptr;
+    // host
+    uint8_t* host_store = nullptr;          // pinned, mapped (UVA: same pointer on device)
+    std::vector<int64_t> ntok;              // host copy of per-request token counts
+};
+
+namespace kvd {
+// launchers (return cudaGetLastError())
+cudaError_t launch_prefix(kvd_cache* c, int layer, int req, const uint16_t* dk, const uint16_t* dv, int64_t n,
+                          cudaStream_t s);
+cudaError_t launch_select(kvd_cache* c, const StepParams& p, const uint16_t* q, int32_t* out_ids, float* out_scores,
+                          cudaStream_t s);
+cudaError_t launch_resolve(kvd_cache* c, const StepParams& p, const int32_t* ids, int32_t* out_attn, cudaStream_t s);
+cudaError_t launch_attention(kvd_cache* c, const StepParams& p, const uint16_t* q, const int32_t* attn, float* out,
+                             float* out_lse, cudaStream_t s);
+
+__host__ __device__ inline SegGeom seg_geom(int64_t n, int P, int sink, int local) {
+    SegGeom g;
+    g.n = (int32_t)n;
+    g.nb = (int32_t)((n + P - 1) / P);
+    int32_t se = (int32_t)((sink + P - 1) / P);
+    int64_t ft = n - local;
+    if (ft < 0) ft = 0;
+    int32_t lb = local > 0 ? (int32_t)(ft / P) : g.nb;
+    if (lb > g.nb) lb = g.nb;
+    if (se > lb) se = lb;                  // overlapping sink/local: all blocks pinned
+    g.sink_end = se;
+    g.local_begin = lb;
+    return g;
+}
+}  // namespace kvd

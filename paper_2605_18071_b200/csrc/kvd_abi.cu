@@ -1,0 +1,445 @@
+// kvd_abi.cu — the C ABI of libkvd.so (include/kvd.h): configuration and
+// allocation, synchronous argument validation, step-call dispatch to the
+// kernels, introspection.  No exception crosses this boundary.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "internal.h"
+
+using namespace kvd;
+
+namespace {
+
+thread_local std::string g_err;
+
+kvd_status fail(kvd_status st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return st;
+}
+
+#define KVD_CUDA(call)                                                                            \
+    do {                                                                                          \
+        cudaError_t e_ = (call);                                                                  \
+        if (e_ != cudaSuccess)                                                                    \
+            return fail(e_ == cudaErrorMemoryAllocation ? KVD_ENOMEM : KVD_ECUDA, "%s: %s (%s:%d)", \
+                        #call, cudaGetErrorString(e_), __FILE__, __LINE__);                       \
+    } while (0)
+
+struct Geometry {
+    int L, Hq, Hkv, G, P, R, kmax, pmax, A, E, max_splits;
+    int64_t nmax, nb_max, nb_pad, C, rec_bytes;
+    bool resident;
+};
+
+kvd_status check_config(const kvd_config* cfg, Geometry* g) {
+    if (!cfg) return fail(KVD_EINVAL, "config is NULL");
+    if (cfg->head_dim != KVD_HEAD_DIM) return fail(KVD_EINVAL, "head_dim must be %d", KVD_HEAD_DIM);
+    if (cfg->num_layers < 1 || cfg->num_kv_heads < 1 || cfg->num_q_heads < 1 || cfg->max_requests < 1)
+        return fail(KVD_EINVAL, "layers, heads and max_requests must be >= 1");
+    if (cfg->num_q_heads % cfg->num_kv_heads) return fail(KVD_EINVAL, "num_q_heads %% num_kv_heads != 0");
+    if (cfg->num_q_heads / cfg->num_kv_heads > KVD_MAX_GROUP)
+        return fail(KVD_EINVAL, "group size > %d unsupported", KVD_MAX_GROUP);
+    const int P = cfg->block_tokens;
+    if (P != 1 && P != 2 && P != 4 && P != 8 && P != 16) return fail(KVD_EINVAL, "block_tokens must be 1,2,4,8,16");
+    if (cfg->max_context < 1) return fail(KVD_EINVAL, "max_context must be >= 1");
+    if (cfg->slots_per_segment < 1) return fail(KVD_EINVAL, "slots_per_segment must be >= 1");
+    if (cfg->max_select < 0) return fail(KVD_EINVAL, "max_select must be >= 0");
+    if (cfg->sink_tokens < 0 || cfg->local_tokens < 0) return fail(KVD_EINVAL, "sink/local tokens must be >= 0");
+    if (cfg->policy < 0 || cfg->policy > 2) return fail(KVD_EINVAL, "unknown policy %d", cfg->policy);
+    g->L = cfg->num_layers;
+    g->Hq = cfg->num_q_heads;
+    g->Hkv = cfg->num_kv_heads;
+    g->G = g->Hq / g->Hkv;
+    g->P = P;
+    g->E = 16 / P;
+    g->R = cfg->max_requests;
+    g->nmax = cfg->max_context;
+    g->nb_max = (g->nmax + P - 1) / P;
+    if (g->nb_max >= (1ll << 23)) return fail(KVD_EINVAL, "too many blocks per request");
+    g->nb_pad = (g->nb_max + kScoreCols - 1) / kScoreCols * kScoreCols;
+    g->C = cfg->slots_per_segment;
+    g->resident = g->C >= g->nb_max;
+    g->kmax = cfg->max_select;
+    if (g->kmax > g->nb_max) return fail(KVD_EINVAL, "max_select > blocks per request");
+    g->pmax = (cfg->sink_tokens + P - 1) / P + (cfg->local_tokens > 0 ? (cfg->local_tokens + P - 1) / P + 1 : 0);
+    g->A = (cfg->host_layer_alias <= 0 || cfg->host_layer_alias > g->L) ? g->L : cfg->host_layer_alias;
+    g->rec_bytes = 2ll * P * kRowBytes;
+    const int64_t wmax = g->kmax + g->pmax;
+    g->max_splits = (int)(((wmax + g->E - 1) / g->E + kSplitTiles - 1) / kSplitTiles);
+    if (g->max_splits < 1) g->max_splits = 1;
+    if ((int64_t)g->Hkv * g->nb_max * 4 > kSlotOfBytes) return fail(KVD_EINVAL, "context too long for setup scratch");
+    return KVD_OK;
+}
+
+struct Sizes {
+    size_t slots, summ, scores, table, meta4, meta1, miss, part_o, part_ml, small, host;
+    size_t dev_total() const { return slots + summ + scores + table + 3 * meta4 + meta1 + miss + part_o + part_ml + small; }
+};
+
+Sizes sizes_of(const Geometry& g) {
+    Sizes s;
+    const size_t segs = (size_t)g.L * g.R * g.Hkv;
+    const size_t rsegs = (size_t)g.R * g.Hkv;
+    s.slots = segs * g.C * g.rec_bytes;
+    s.summ = segs * kHeadDim * g.nb_pad * 2;
+    s.scores = segs * g.nb_pad * 4;
+    s.table = segs * g.nb_pad * 4;
+    s.meta4 = segs * g.C * 4;
+    s.meta1 = segs * g.C;
+    s.miss = rsegs * (size_t)(g.kmax > 0 ? g.kmax : 1) * 2 * 4 + rsegs * 4;
+    s.part_o = rsegs * g.max_splits * 8 * kHeadDim * 4;
+    s.part_ml = rsegs * g.max_splits * 8 * 2 * 4;
+    s.small = rsegs * 4 + 64 + 4 + (size_t)g.R * 4 + g.rec_bytes;
+    s.host = g.resident ? 0 : (size_t)g.A * g.R * g.Hkv * g.nb_max * g.rec_bytes;
+    return s;
+}
+
+template <class T>
+cudaError_t dalloc(T** p, size_t bytes) {
+    void* v = nullptr;
+    cudaError_t e = cudaMalloc(&v, bytes ? bytes : 16);
+    *p = static_cast<T*>(v);
+    return e;
+}
+
+kvd_status check_step(kvd_cache* c, int32_t layer, const int32_t* req_ids, int32_t B, int32_t k, StepParams* p) {
+    if (!c) return fail(KVD_EINVAL, "cache is NULL");
+    if (!req_ids) return fail(KVD_EINVAL, "req_ids is NULL");
+    if (B < 1 || B > KVD_MAX_BATCH) return fail(KVD_EINVAL, "B=%d outside [1, %d]", B, KVD_MAX_BATCH);
+    if (layer < 0 || layer >= c->L) return fail(KVD_EINVAL, "layer %d out of range", layer);
+    if (k < 0 || k > c->kmax) return fail(KVD_EINVAL, "k_blocks=%d outside [0, max_select=%d]", k, c->kmax);
+    std::vector<char> seen((size_t)c->R, 0);
+    for (int b = 0; b < B; ++b) {
+        const int r = req_ids[b];
+        if (r < 0 || r >= c->R) return fail(KVD_EINVAL, "req_ids[%d]=%d out of range", b, r);
+        if (seen[(size_t)r]) return fail(KVD_EINVAL, "req_ids[%d]=%d repeated", b, r);
+        seen[(size_t)r] = 1;
+        if (c->ntok[(size_t)r] <= 0) return fail(KVD_ESTATE, "request %d has no prefix loaded", r);
+        const SegGeom sg = seg_geom(c->ntok[(size_t)r], c->P, c->cfg.sink_tokens, c->cfg.local_tokens);
+        const int pr = sg.sink_end + (sg.nb - sg.local_begin);
+        if (k > sg.nb - pr)
+            return fail(KVD_ERANGE, "request %d: k_blocks=%d > %d candidate blocks", r, k, sg.nb - pr);
+        if ((int64_t)k + pr > c->C)
+            return fail(KVD_ECAPACITY, "request %d: k_blocks + pinned = %d > slots_per_segment=%lld", r, k + pr,
+                        (long long)c->C);
+        p->req[b] = r;
+    }
+    p->B = B;
+    p->layer = layer;
+    p->k = k;
+    p->W = k + c->pmax;
+    p->R = c->R;
+    p->Hkv = c->Hkv;
+    p->Hq = c->Hq;
+    p->G = c->G;
+    p->P = c->P;
+    p->E = c->E;
+    p->nb_pad = c->nb_pad;
+    p->C = c->C;
+    p->nb_max = c->nb_max;
+    p->sink_tokens = c->cfg.sink_tokens;
+    p->local_tokens = c->cfg.local_tokens;
+    p->policy = c->cfg.policy;
+    p->step = 0;
+    p->host_layer = layer % c->A;
+    p->rec_bytes = (int32_t)c->rec_bytes;
+    p->nsplit = (int)(((p->W + c->E - 1) / c->E + kSplitTiles - 1) / kSplitTiles);
+    p->scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)KVD_HEAD_DIM));
+    return KVD_OK;
+}
+
+kvd_status launched(cudaError_t e) {
+    if (e != cudaSuccess) return fail(KVD_ECUDA, "kernel launch: %s", cudaGetErrorString(e));
+    return KVD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* kvd_last_error(void) { return g_err.c_str(); }
+
+const char* kvd_version(void) { return "kvd 0.1 sm_100a"; }
+
+kvd_status kvd_required_bytes(const kvd_config* cfg, size_t* dev_bytes, size_t* host_pinned_bytes) {
+    Geometry g;
+    kvd_status st = check_config(cfg, &g);
+    if (st) return st;
+    Sizes s = sizes_of(g);
+    if (dev_bytes) *dev_bytes = s.dev_total();
+    if (host_pinned_bytes) *host_pinned_bytes = s.host;
+    return KVD_OK;
+}
+
+kvd_status kvd_create_cache(const kvd_config* cfg, kvd_cache** out) {
+    if (!out) return fail(KVD_EINVAL, "out is NULL");
+    *out = nullptr;
+    Geometry g;
+    kvd_status st = check_config(cfg, &g);
+    if (st) return st;
+    KVD_CUDA(cudaSetDevice(cfg->device));
+    kvd_cache* c = new (std::nothrow) kvd_cache();
+    if (!c) return fail(KVD_ENOMEM, "host allocation failed");
+    c->cfg = *cfg;
+    c->L = g.L; c->Hq = g.Hq; c->Hkv = g.Hkv; c->G = g.G; c->P = g.P; c->R = g.R; c->kmax = g.kmax;
+    c->pmax = g.pmax; c->A = g.A; c->E = g.E; c->nmax = g.nmax; c->nb_max = g.nb_max; c->nb_pad = g.nb_pad;
+    c->C = g.C; c->resident = g.resident; c->rec_bytes = g.rec_bytes; c->max_splits = g.max_splits;
+    c->ntok.assign((size_t)g.R, 0);
+    const Sizes s = sizes_of(g);
+    const size_t rsegs = (size_t)g.R * g.Hkv;
+    cudaError_t e = cudaSuccess;
+#define ALLOC(ptr, bytes)                                       \
+    if (e == cudaSuccess) e = dalloc(&c->ptr, (bytes));
+    ALLOC(slots, s.slots);
+    ALLOC(summ, s.summ);
+    ALLOC(scores, s.scores);
+    ALLOC(table, s.table);
+    ALLOC(slot_block, s.meta4);
+    ALLOC(last_use, s.meta4);
+    ALLOC(use_count, s.meta4);
+    ALLOC(phase, s.meta1);
+    ALLOC(miss, rsegs * (size_t)(g.kmax > 0 ? g.kmax : 1) * 2 * 4);
+    ALLOC(miss_count, rsegs * 4);
+    ALLOC(part_o, s.part_o);
+    ALLOC(part_ml, s.part_ml);
+    ALLOC(split_ctr, rsegs * 4);
+    ALLOC(stats, 64);
+    ALLOC(err, 4);
+    ALLOC(ntok_dev, (size_t)g.R * 4);
+    ALLOC(zero_rec, (size_t)g.rec_bytes);
+#undef ALLOC
+    if (e == cudaSuccess) e = cudaMemset(c->scores, 0, s.scores);
+    if (e == cudaSuccess) e = cudaMemset(c->table, 0xFF, s.table);
+    if (e == cudaSuccess) e = cudaMemset(c->slot_block, 0xFF, s.meta4);
+    if (e == cudaSuccess) e = cudaMemset(c->miss_count, 0, rsegs * 4);
+    if (e == cudaSuccess) e = cudaMemset(c->split_ctr, 0, rsegs * 4);
+    if (e == cudaSuccess) e = cudaMemset(c->stats, 0, 64);
+    if (e == cudaSuccess) e = cudaMemset(c->err, 0, 4);
+    if (e == cudaSuccess) e = cudaMemset(c->ntok_dev, 0, (size_t)g.R * 4);
+    if (e == cudaSuccess) e = cudaMemset(c->zero_rec, 0, (size_t)g.rec_bytes);
+    if (e == cudaSuccess && !g.resident) {
+        void* h = nullptr;
+        e = cudaHostAlloc(&h, s.host, cudaHostAllocMapped | cudaHostAllocPortable);
+        c->host_store = static_cast<uint8_t*>(h);
+    }
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+        kvd_destroy_cache(c);
+        return fail(e == cudaErrorMemoryAllocation ? KVD_ENOMEM : KVD_ECUDA, "create: %s", cudaGetErrorString(e));
+    }
+    *out = c;
+    return KVD_OK;
+}
+
+void kvd_destroy_cache(kvd_cache* c) {
+    if (!c) return;
+    cudaSetDevice(c->cfg.device);
+    cudaDeviceSynchronize();
+    void* dev[] = {c->slots, c->summ, c->scores, c->table, c->slot_block, c->last_use, c->phase,
+                   c->use_count, c->miss, c->miss_count, c->part_o, c->part_ml, c->split_ctr, c->stats,
+                   c->err, c->ntok_dev, c->zero_rec, c->stage_kv, c->stage_rec};
+    for (void* p : dev)
+        if (p) cudaFree(p);
+    if (c->host_store) cudaFreeHost(c->host_store);
+    delete c;
+}
+
+kvd_status kvd_get_info(const kvd_cache* c, kvd_cache_info* out) {
+    if (!c || !out) return fail(KVD_EINVAL, "NULL argument");
+    out->nb_max = c->nb_max;
+    out->nb_pad = c->nb_pad;
+    out->slots_per_segment = c->C;
+    out->max_pinned = c->pmax;
+    out->record_bytes = (int32_t)c->rec_bytes;
+    out->resident = c->resident ? 1 : 0;
+    out->host_layers = c->A;
+    return KVD_OK;
+}
+
+int32_t kvd_attn_width(const kvd_cache* c, int32_t k_blocks) { return c ? k_blocks + c->pmax : -1; }
+
+kvd_status kvd_load_prefix(kvd_cache* c, int32_t layer, int32_t req, const uint16_t* k, const uint16_t* v,
+                           int64_t n_tokens, kvd_stream stream) {
+    if (!c || !k || !v) return fail(KVD_EINVAL, "NULL argument");
+    if (layer < 0 || layer >= c->L) return fail(KVD_EINVAL, "layer %d out of range", layer);
+    if (req < 0 || req >= c->R) return fail(KVD_EINVAL, "req %d out of range", req);
+    if (n_tokens < 1 || n_tokens > c->nmax)
+        return fail(KVD_EINVAL, "n_tokens=%lld outside [1, %lld]", (long long)n_tokens, (long long)c->nmax);
+    if (c->ntok[(size_t)req] > 0 && c->ntok[(size_t)req] != n_tokens)
+        return fail(KVD_ESTATE, "request %d already has %lld tokens in another layer", req,
+                    (long long)c->ntok[(size_t)req]);
+    KVD_CUDA(cudaSetDevice(c->cfg.device));
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const size_t kv_elems = (size_t)c->Hkv * n_tokens * kHeadDim;
+    if (!c->stage_kv) KVD_CUDA(dalloc(&c->stage_kv, 2 * (size_t)c->Hkv * c->nmax * kHeadDim * 2));
+    if (!c->stage_rec)
+        KVD_CUDA(dalloc(&c->stage_rec, (size_t)kSlotOfBytes +
+                                           (c->resident ? 0 : (size_t)c->Hkv * c->nb_max * c->rec_bytes)));
+    const uint16_t* dk = k;
+    const uint16_t* dv = v;
+    cudaPointerAttributes ak{}, av{};
+    KVD_CUDA(cudaPointerGetAttributes(&ak, k));
+    KVD_CUDA(cudaPointerGetAttributes(&av, v));
+    if (ak.type != cudaMemoryTypeDevice && ak.type != cudaMemoryTypeManaged) {
+        KVD_CUDA(cudaMemcpyAsync(c->stage_kv, k, kv_elems * 2, cudaMemcpyHostToDevice, s));
+        dk = c->stage_kv;
+    }
+    if (av.type != cudaMemoryTypeDevice && av.type != cudaMemoryTypeManaged) {
+        KVD_CUDA(cudaMemcpyAsync(c->stage_kv + kv_elems, v, kv_elems * 2, cudaMemcpyHostToDevice, s));
+        dv = c->stage_kv + kv_elems;
+    }
+    KVD_CUDA(launch_prefix(c, layer, req, dk, dv, n_tokens, s));
+    KVD_CUDA(cudaStreamSynchronize(s));
+    c->ntok[(size_t)req] = n_tokens;
+    return KVD_OK;
+}
+
+kvd_status kvd_select_topk(kvd_cache* c, int32_t layer, const uint16_t* q, const int32_t* req_ids, int32_t B,
+                           int32_t k_blocks, int32_t* out_ids, float* out_scores, kvd_stream stream) {
+    StepParams p;
+    kvd_status st = check_step(c, layer, req_ids, B, k_blocks, &p);
+    if (st) return st;
+    if (!q || (!out_ids && k_blocks > 0)) return fail(KVD_EINVAL, "q / out_ids is NULL");
+    return launched(launch_select(c, p, q, out_ids, out_scores, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+kvd_status kvd_resolve_and_fetch(kvd_cache* c, int32_t layer, const int32_t* req_ids, int32_t B, const int32_t* ids,
+                                 int32_t k_blocks, uint32_t step, int32_t* out_attn, kvd_stream stream) {
+    StepParams p;
+    kvd_status st = check_step(c, layer, req_ids, B, k_blocks, &p);
+    if (st) return st;
+    if ((!ids && k_blocks > 0) || !out_attn) return fail(KVD_EINVAL, "ids / out_attn is NULL");
+    p.step = step;
+    return launched(launch_resolve(c, p, ids, out_attn, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+kvd_status kvd_sparse_decode(kvd_cache* c, int32_t layer, const uint16_t* q, const int32_t* req_ids, int32_t B,
+                             const int32_t* attn, int32_t W, float* out, float* out_lse, kvd_stream stream) {
+    if (!c) return fail(KVD_EINVAL, "cache is NULL");
+    const int32_t k = W - c->pmax;
+    if (k < 0) return fail(KVD_EINVAL, "W=%d smaller than max pinned %d", W, c->pmax);
+    StepParams p;
+    kvd_status st = check_step(c, layer, req_ids, B, k, &p);
+    if (st) return st;
+    if (!q || !attn || !out) return fail(KVD_EINVAL, "q / attn / out is NULL");
+    return launched(launch_attention(c, p, q, attn, out, out_lse, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+static kvd_status check_seg(kvd_cache* c, int32_t layer, int32_t req, int32_t head) {
+    if (!c) return fail(KVD_EINVAL, "cache is NULL");
+    if (layer < 0 || layer >= c->L || req < 0 || req >= c->R || head < 0 || head >= c->Hkv)
+        return fail(KVD_EINVAL, "segment (%d,%d,%d) out of range", layer, req, head);
+    return KVD_OK;
+}
+
+kvd_status kvd_read_segment(kvd_cache* c, int32_t layer, int32_t req, int32_t head, int32_t* table,
+                            int32_t* slot_block, uint32_t* last_use, uint8_t* phase, uint32_t* use_count) {
+    kvd_status st = check_seg(c, layer, req, head);
+    if (st) return st;
+    KVD_CUDA(cudaDeviceSynchronize());
+    const int64_t seg = ((int64_t)layer * c->R + req) * c->Hkv + head;
+    if (table) KVD_CUDA(cudaMemcpy(table, c->table + seg * c->nb_pad, c->nb_pad * 4, cudaMemcpyDeviceToHost));
+    if (slot_block) KVD_CUDA(cudaMemcpy(slot_block, c->slot_block + seg * c->C, c->C * 4, cudaMemcpyDeviceToHost));
+    if (last_use) KVD_CUDA(cudaMemcpy(last_use, c->last_use + seg * c->C, c->C * 4, cudaMemcpyDeviceToHost));
+    if (phase) KVD_CUDA(cudaMemcpy(phase, c->phase + seg * c->C, c->C, cudaMemcpyDeviceToHost));
+    if (use_count) KVD_CUDA(cudaMemcpy(use_count, c->use_count + seg * c->C, c->C * 4, cudaMemcpyDeviceToHost));
+    return KVD_OK;
+}
+
+kvd_status kvd_read_slot(kvd_cache* c, int32_t layer, int32_t req, int32_t head, int64_t slot, void* out_record) {
+    kvd_status st = check_seg(c, layer, req, head);
+    if (st) return st;
+    if (slot < 0 || slot >= c->C || !out_record) return fail(KVD_EINVAL, "bad slot / NULL");
+    KVD_CUDA(cudaDeviceSynchronize());
+    const int64_t seg = ((int64_t)layer * c->R + req) * c->Hkv + head;
+    KVD_CUDA(cudaMemcpy(out_record, c->slots + (seg * c->C + slot) * c->rec_bytes, (size_t)c->rec_bytes,
+                        cudaMemcpyDeviceToHost));
+    return KVD_OK;
+}
+
+kvd_status kvd_read_host_record(kvd_cache* c, int32_t layer, int32_t req, int32_t head, int64_t block,
+                                void* out_record) {
+    kvd_status st = check_seg(c, layer, req, head);
+    if (st) return st;
+    if (c->resident || !c->host_store) return fail(KVD_ESTATE, "fully resident cache has no host store");
+    if (block < 0 || block >= c->nb_max || !out_record) return fail(KVD_EINVAL, "bad block / NULL");
+    KVD_CUDA(cudaDeviceSynchronize());
+    const int64_t hl = layer % c->A;
+    memcpy(out_record, c->host_store + (((hl * c->R + req) * c->Hkv + head) * c->nb_max + block) * c->rec_bytes,
+           (size_t)c->rec_bytes);
+    return KVD_OK;
+}
+
+kvd_status kvd_read_summaries(kvd_cache* c, int32_t layer, int32_t req, int32_t head, uint16_t* out) {
+    kvd_status st = check_seg(c, layer, req, head);
+    if (st) return st;
+    if (!out) return fail(KVD_EINVAL, "out is NULL");
+    if (c->ntok[(size_t)req] <= 0) return fail(KVD_ESTATE, "request %d not loaded", req);
+    KVD_CUDA(cudaDeviceSynchronize());
+    const int64_t seg = ((int64_t)layer * c->R + req) * c->Hkv + head;
+    const int64_t nb = (c->ntok[(size_t)req] + c->P - 1) / c->P;
+    std::vector<uint16_t> tmp((size_t)(kHeadDim * c->nb_pad));
+    KVD_CUDA(cudaMemcpy(tmp.data(), c->summ + seg * kHeadDim * c->nb_pad, tmp.size() * 2, cudaMemcpyDeviceToHost));
+    for (int64_t b = 0; b < nb; ++b)
+        for (int j = 0; j < kHeadDim; ++j) out[b * kHeadDim + j] = tmp[(size_t)(j * c->nb_pad + b)];
+    return KVD_OK;
+}
+
+kvd_status kvd_read_scores(kvd_cache* c, int32_t layer, int32_t req, int32_t head, float* out) {
+    kvd_status st = check_seg(c, layer, req, head);
+    if (st) return st;
+    if (!out) return fail(KVD_EINVAL, "out is NULL");
+    if (c->ntok[(size_t)req] <= 0) return fail(KVD_ESTATE, "request %d not loaded", req);
+    KVD_CUDA(cudaDeviceSynchronize());
+    const int64_t seg = ((int64_t)layer * c->R + req) * c->Hkv + head;
+    const int64_t nb = (c->ntok[(size_t)req] + c->P - 1) / c->P;
+    KVD_CUDA(cudaMemcpy(out, c->scores + seg * c->nb_pad, (size_t)nb * 4, cudaMemcpyDeviceToHost));
+    return KVD_OK;
+}
+
+kvd_status kvd_get_stats(kvd_cache* c, kvd_stats* out) {
+    if (!c || !out) return fail(KVD_EINVAL, "NULL argument");
+    KVD_CUDA(cudaDeviceSynchronize());
+    unsigned long long v[5];
+    KVD_CUDA(cudaMemcpy(v, c->stats, sizeof v, cudaMemcpyDeviceToHost));
+    out->selected = v[0];
+    out->hits = v[1];
+    out->misses = v[2];
+    out->pinned = v[3];
+    out->fetched_bytes = v[4];
+    return KVD_OK;
+}
+
+kvd_status kvd_reset_stats(kvd_cache* c) {
+    if (!c) return fail(KVD_EINVAL, "cache is NULL");
+    KVD_CUDA(cudaDeviceSynchronize());
+    KVD_CUDA(cudaMemset(c->stats, 0, 64));
+    KVD_CUDA(cudaDeviceSynchronize());
+    return KVD_OK;
+}
+
+kvd_status kvd_check(kvd_cache* c) {
+    if (!c) return fail(KVD_EINVAL, "cache is NULL");
+    KVD_CUDA(cudaDeviceSynchronize());
+    int32_t e = 0;
+    KVD_CUDA(cudaMemcpy(&e, c->err, 4, cudaMemcpyDeviceToHost));
+    if (e) {
+        KVD_CUDA(cudaMemset(c->err, 0, 4));
+        return fail(KVD_EDEVICE, "device flagged bad input (code %d: %s)", e,
+                    (e & 1) ? "selection not ascending / out of range / pinned" : "LFU key bounds exceeded");
+    }
+    return KVD_OK;
+}
+
+}  // extern "C"

@@ -48,9 +48,14 @@ static inline uint64_t ctr_u64(uint64_t key, uint64_t ctr) {
 static inline double ctr_unif(uint64_t key, uint64_t ctr) {       /* (0,1) */
     return ((double)(ctr_u64(key, ctr) >> 11) + 0.5) * (1.0 / 9007199254740992.0);
 }
-static inline double ctr_normal(uint64_t key, uint64_t ctr) {      /* N(0,1), Box-Muller */
-    double u1 = ctr_unif(key, 2 * ctr), u2 = ctr_unif(key, 2 * ctr + 1);
-    return sqrt(-2.0 * log(u1)) * cos(6.283185307179586 * u2);
+/* Approximately N(0,1): Irwin-Hall sum of four 16-bit uniforms from one hash,
+ * centred and scaled to unit variance (tails bounded at +-3.46).  Integer and
+ * exact float arithmetic only: identical on every host. */
+static inline float ctr_normal(uint64_t key, uint64_t ctr) {
+    uint64_t x = ctr_u64(key, ctr);
+    uint32_t s = (uint32_t)(x & 0xFFFF) + (uint32_t)((x >> 16) & 0xFFFF) +
+                 (uint32_t)((x >> 32) & 0xFFFF) + (uint32_t)(x >> 48);      /* 0 .. 4*65535 */
+    return ((float)s - 131070.0f) * (1.7320508f / 65536.0f);
 }
 static inline uint16_t to_bf16(float f) {
     uint32_t u; memcpy(&u, &f, 4);
