@@ -170,6 +170,13 @@ kvd_status kvd_resolve_and_fetch(kvd_cache* c, int32_t layer, const int32_t* req
                                  int32_t B, const int32_t* ids, int32_t k_blocks,
                                  uint32_t step, int32_t* out_attn, kvd_stream stream);
 
+/* CUDA-graph support for (2): when dev_step != NULL, every later resolve reads
+ * the decode-step index from *dev_step (device uint32) when the kernel runs and
+ * ignores its host `step` argument, so one captured step can be replayed for
+ * step t, t+1, ... by advancing *dev_step on the stream.  NULL restores the
+ * host argument.  dev_step must stay valid while the cache uses it. */
+kvd_status kvd_set_device_step(kvd_cache* c, const uint32_t* dev_step);
+
 kvd_status kvd_get_info(const kvd_cache* c, kvd_cache_info* out);
 
 /* Width W of the attention list for k_blocks (k_blocks + max pinned blocks). */

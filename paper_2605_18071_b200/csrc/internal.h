@@ -37,6 +37,7 @@ struct StepParams {
     int32_t sink_tokens, local_tokens;
     int32_t policy;
     uint32_t step;
+    const uint32_t* step_dev;         // non-null: read the step on the device (graph replay)
     int32_t host_layer;
     int32_t rec_bytes;
     int32_t nsplit;
@@ -71,6 +72,7 @@ struct kvd_cache {
     int32_t* err = nullptr;
     int32_t* ntok_dev = nullptr;
     uint8_t* zero_rec = nullptr;           // one zero record (padding entries)
+    const uint32_t* step_dev = nullptr;    // kvd_set_device_step
     // setup staging (lazily allocated)
     uint16_t* stage_kv = nullptr;
     uint8_t* stage_rec = nullptr;

@@ -208,12 +208,13 @@ __global__ void __launch_bounds__(kResolveThreads) resolve_kernel(StepParams p, 
     }
     __syncthreads();
     // ---- 5. admit misses, update metadata
+    const uint32_t step = p.step_dev ? *p.step_dev : p.step;
     int32_t* miss_out = rb.miss + rs * (int64_t)rb.kmax * 2;
     for (int i = tid; i < nm; i += blockDim.x) {
         const int32_t b = M[i], s = dest[i];
         table[b] = s;
         sb[s] = b;
-        lu[s] = p.step;
+        lu[s] = step;
         ph[s] = 1;
         uc[s] = 1;
         miss_out[2 * i] = b;
@@ -222,7 +223,7 @@ __global__ void __launch_bounds__(kResolveThreads) resolve_kernel(StepParams p, 
     for (int i = tid; i < k; i += blockDim.x) {
         const int32_t s = hitslot[i];
         if (s >= 0) {
-            lu[s] = p.step;
+            lu[s] = step;
             ph[s] = 0;
             uc[s] = uc[s] + 1;
         }
@@ -295,6 +296,12 @@ cudaError_t launch_resolve(kvd_cache* c, const StepParams& p, const int32_t* ids
                    c->ntok_dev, c->miss,       c->miss_count, c->kmax, c->stats,    c->err};
     const size_t smem = sizeof(uint64_t) * (size_t)c->C + sizeof(int32_t) * (size_t)c->kmax * 5 +
                         sizeof(uint32_t) * (size_t)((c->nb_pad + 31) / 32);
+    static size_t smem_set = 48 << 10;
+    if (smem > smem_set) {
+        cudaError_t e = cudaFuncSetAttribute(resolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        smem_set = smem;
+    }
     resolve_kernel<<<dim3(p.Hkv, p.B), kResolveThreads, smem, s>>>(p, rb, ids, out_attn);
     if (!c->resident) {
         gather_kernel<<<148 * 4, kGatherThreads, 0, s>>>(p, c->miss, c->miss_count, c->kmax, c->host_store,

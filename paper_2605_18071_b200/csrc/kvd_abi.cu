@@ -152,6 +152,7 @@ kvd_status check_step(kvd_cache* c, int32_t layer, const int32_t* req_ids, int32
     p->local_tokens = c->cfg.local_tokens;
     p->policy = c->cfg.policy;
     p->step = 0;
+    p->step_dev = c->step_dev;
     p->host_layer = layer % c->A;
     p->rec_bytes = (int32_t)c->rec_bytes;
     p->nsplit = (int)(((p->W + c->E - 1) / c->E + kSplitTiles - 1) / kSplitTiles);
@@ -253,6 +254,12 @@ void kvd_destroy_cache(kvd_cache* c) {
         if (p) cudaFree(p);
     if (c->host_store) cudaFreeHost(c->host_store);
     delete c;
+}
+
+kvd_status kvd_set_device_step(kvd_cache* c, const uint32_t* dev_step) {
+    if (!c) return fail(KVD_EINVAL, "cache is NULL");
+    c->step_dev = dev_step;
+    return KVD_OK;
 }
 
 kvd_status kvd_get_info(const kvd_cache* c, kvd_cache_info* out) {

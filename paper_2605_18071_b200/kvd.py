@@ -55,7 +55,7 @@ EXPORTS = ["kvd_required_bytes", "kvd_create_cache", "kvd_destroy_cache", "kvd_g
            "kvd_load_prefix", "kvd_select_topk", "kvd_resolve_and_fetch", "kvd_sparse_decode",
            "kvd_read_segment", "kvd_read_slot", "kvd_read_host_record", "kvd_read_summaries",
            "kvd_read_scores", "kvd_get_stats", "kvd_reset_stats", "kvd_check", "kvd_last_error",
-           "kvd_version"]
+           "kvd_version", "kvd_set_device_step"]
 
 
 def lib():
@@ -71,6 +71,7 @@ def lib():
             "kvd_create_cache": ([p, p], i32),
             "kvd_destroy_cache": ([p], None),
             "kvd_get_info": ([p, p], i32),
+            "kvd_set_device_step": ([p, p], i32),
             "kvd_attn_width": ([p, i32], i32),
             "kvd_load_prefix": ([p, i32, i32, p, p, i64, p], i32),
             "kvd_select_topk": ([p, i32, p, p, i32, i32, p, p, p], i32),
@@ -167,6 +168,10 @@ class KVCache:
 
     def attn_width(self, k_blocks):
         return lib().kvd_attn_width(self.h, k_blocks)
+
+    def set_device_step(self, dev_step):
+        """Resolve reads the step index from this device uint32 (graph replay); None = host arg."""
+        _check(lib().kvd_set_device_step(self.h, ptr(dev_step)))
 
     # ------------------------------------------------------------ setup
     def load_prefix(self, layer, req, k, v, n_tokens, stream=None):

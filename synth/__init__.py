@@ -11,7 +11,9 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "libsynth.so")
+_GPU_SO = os.path.join(_HERE, "libsynth_gpu.so")
 _lib = None
+_glib = None
 
 
 def build(force: bool = False) -> str:
@@ -20,6 +22,29 @@ def build(force: bool = False) -> str:
         subprocess.check_call(["gcc", "-O2", "-fopenmp", "-ffp-contract=off", "-shared", "-fPIC",
                                "-o", _SO, src, "-lm"])
     return _SO
+
+
+def build_gpu(force: bool = False) -> str:
+    """Device copy of the K/V generator (synth_gpu.cu), sm_100a."""
+    src = os.path.join(_HERE, "synth_gpu.cu")
+    if force or not os.path.exists(_GPU_SO) or os.path.getmtime(_GPU_SO) < os.path.getmtime(src):
+        subprocess.check_call(["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3",
+                               "-Xcompiler", "-fPIC", "-shared", "-o", _GPU_SO + ".tmp", src])
+        os.replace(_GPU_SO + ".tmp", _GPU_SO)
+    return _GPU_SO
+
+
+def glib():
+    global _glib
+    if _glib is None:
+        build_gpu()
+        L = ctypes.CDLL(_GPU_SO)
+        L.synth_gpu_segment_kv.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p,
+                                           ctypes.c_uint64, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p,
+                                           ctypes.c_void_p]
+        L.synth_gpu_segment_kv.restype = ctypes.c_int
+        _glib = L
+    return _glib
 
 
 def lib():
@@ -32,7 +57,9 @@ def lib():
         L.synth_request_kv.argtypes = [u64, i64, i64, i32, i64, i32, p, p]
         L.synth_queries.argtypes = [u64, i64, i64, i64, i32, i32, i64, i64, ctypes.c_double, p]
         L.synth_batch_queries.argtypes = [u64, i64, p, i32, i32, i32, i32, i64, i64, ctypes.c_double, p]
-        for f in (L.synth_segment_kv, L.synth_request_kv, L.synth_queries, L.synth_batch_queries):
+        L.synth_segment_plan.argtypes = [u64, i64, i64, i64, i64, i32, p, p, p]
+        for f in (L.synth_segment_kv, L.synth_request_kv, L.synth_queries, L.synth_batch_queries,
+                  L.synth_segment_plan):
             f.restype = None
         _lib = L
     return _lib
@@ -59,6 +86,27 @@ def request_kv(seed, layer, req, Hkv, n, d=128, out_k=None, out_v=None):
     V = out_v if out_v is not None else np.empty((Hkv, n, d), np.uint16)
     lib().synth_request_kv(seed, layer, req, Hkv, n, d, _ptr(K), _ptr(V))
     return K, V
+
+
+def request_kv_device(seed, layer, req, Hkv, n, K, V, d=128, stream=None):
+    """Same bytes as request_kv, generated on the GPU into device torch tensors
+    K, V [Hkv][n][d] (int16 / uint16 views of bf16).  Host computes the per-token
+    topic runs and topic centres; the device expands them."""
+    import torch
+    topic = np.empty(n, np.uint8)
+    mu = np.empty((32, d), np.float32)
+    keys = np.empty(2, np.uint64)
+    dev = K.device
+    s = stream.cuda_stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
+    for h in range(Hkv):
+        lib().synth_segment_plan(seed, layer, req, h, n, d, _ptr(topic), _ptr(mu), _ptr(keys))
+        t_d = torch.from_numpy(topic).to(dev)
+        m_d = torch.from_numpy(mu).to(dev)
+        rc = glib().synth_gpu_segment_kv(n, d, t_d.data_ptr(), m_d.data_ptr(), int(keys[0]), int(keys[1]),
+                                         K[h].data_ptr(), V[h].data_ptr(), s)
+        if rc:
+            raise RuntimeError(f"synth_gpu_segment_kv: cuda error {rc}")
+        torch.cuda.current_stream(dev).synchronize()
 
 
 def queries(seed, layer, req, head, G, d=128, t0=0, nsteps=1, alpha=0.9):

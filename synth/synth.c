@@ -83,6 +83,18 @@ static void topic_centres(uint64_t seed, int64_t l, int64_t r, int64_t h, int32_
     for (int64_t i = 0; i < (int64_t)SYN_TOPICS * d; ++i) mu[i] = (float)ctr_normal(km, (uint64_t)i);
 }
 
+/* Exported pieces for the device generator (synth_gpu.cu): topic of every
+ * token [n] and topic centres [SYN_TOPICS][d] of one segment, plus the two
+ * stream keys.  The device side turns these into exactly the bytes
+ * synth_segment_kv writes. */
+void synth_segment_plan(uint64_t seed, int64_t l, int64_t r, int64_t h, int64_t n, int32_t d,
+                        uint8_t* topic, float* mu, uint64_t* keys2) {
+    topic_centres(seed, l, r, h, d, mu);
+    token_topics(seed, l, r, h, n, topic);
+    keys2[0] = seg_key(seed, l, r, h, ST_KEYNOISE);
+    keys2[1] = seg_key(seed, l, r, h, ST_VAL);
+}
+
 /* Keys and values of one segment, token-major [n][d] bf16 (caller-owned). */
 void synth_segment_kv(uint64_t seed, int64_t l, int64_t r, int64_t h, int64_t n, int32_t d,
                       uint16_t* K, uint16_t* V) {
