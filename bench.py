@@ -67,6 +67,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch layer by layer instead of graph replay")
+    ap.add_argument("--layers", type=int, default=None, help="override L (profiling only; not a bench number)")
     ap.add_argument("--cpu-sample-s", type=float, default=12.0, help="target seconds of oracle work")
     return ap.parse_args()
 
@@ -238,6 +239,8 @@ def run_gpu(args):
     import synth
     synth.build_gpu()
     cfg = dict(CONFIGS[args.config])
+    if args.layers:
+        cfg["L"] = args.layers
 
     def barrier():
         if world > 1:
@@ -272,13 +275,13 @@ def run_gpu(args):
     if not args.no_graph:
         R.capture(s)
     run = (lambda: R.eager_step(s)) if args.no_graph else (lambda: R.graph_step(s))
+    clk = ClockSampler(local)          # sampled from warm-up through the e2e pass (GPU busy throughout)
+    clk.start()
     for _ in range(args.warmup):
         run()
     s.synchronize()
     R.cache.reset_stats()
     # ---- timed region: K steps, device-timed on the launching stream
-    clk = ClockSampler(local)
-    clk.start()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     ev0.record(s)
@@ -287,7 +290,6 @@ def run_gpu(args):
     ev1.record(s)
     ev1.synchronize()
     barrier()
-    clocks = clk.stop()
     ms = ev0.elapsed_time(ev1) / args.steps
     st = R.cache.stats()
     ms_max = max_over_ranks(ms)
@@ -372,6 +374,7 @@ def run_gpu(args):
         e2e = {"value": tokens / (ems * args.steps * 1e-3), "unit": "tokens/s", "ms_per_step": ems,
                "h2d_bytes_per_step": int(R.q_cur.numel() * 2), "d2h_bytes_per_step": int(R.out.numel() * 4)}
     R.cache.check()
+    clocks = clk.stop()
 
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,

@@ -131,6 +131,41 @@ __device__ __forceinline__ int4 ld_stream16(const void* p) {
     return r;
 }
 
+// ------------------------------------------- programmatic dependent launch
+// Every step kernel is launched with programmatic stream serialization
+// (launch_pdl) so its prologue overlaps the previous kernel's tail; it calls
+// griddep_wait() before touching anything an earlier kernel of the step wrote,
+// and griddep_launch() once its main loop is done.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
+// Shared-memory histogram increment aggregated over the lanes of a warp that
+// hit the same bin (the leading key bits are nearly constant, so plain atomics
+// would serialise on one bin).  All 32 lanes must call it; `active` = this
+// lane contributes.
+__device__ __forceinline__ void warp_hist_add(int* hist, uint32_t bin, bool active) {
+    const uint32_t act = __ballot_sync(0xffffffffu, active);
+    if (!active) return;
+    const uint32_t peers = __match_any_sync(act, bin);
+    if ((threadIdx.x & 31) == (uint32_t)(__ffs(peers) - 1)) atomicAdd(&hist[bin], __popc(peers));
+}
+
 // ------------------------------------------------------------ block scans
 // Exclusive prefix sum of one int per thread over the whole CTA (blockDim.x a
 // multiple of 32, <= 1024).  `scratch` >= 33 ints of shared memory.  Returns the

@@ -43,6 +43,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(StepParams p, AttnBu
     __shared__ __align__(8) uint64_t bar[kAttnWarps][kAttnStages];
     __shared__ float red_m[kAttnWarps][8], red_l[kAttnWarps][8];
     __shared__ int s_last;
+    __shared__ int2 s_list[kSplitTiles * 16];          // (block, slot) of the split's entries
     const int split = blockIdx.x, h = blockIdx.y, bi = blockIdx.z;
     const int r = p.req[bi];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -66,8 +67,14 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(StepParams p, AttnBu
         for (int s = 0; s < kAttnStages; ++s) mbar_init(&my_bar[s], 1);
         fence_mbar_init();
     }
-    __syncwarp();
     const uint64_t pol = l2_evict_first_policy();
+    // everything below reads what resolve / gather (the previous kernels) wrote
+    griddep_wait();
+    // the split's (block, slot) entries -> shared memory, so issuing a tile's copy
+    // never waits on a dependent global load
+    const int e0 = t0 * p.E, ne = max(0, min(nvalid, t1 * p.E) - e0);
+    for (int i = tid; i < ne; i += kAttnThreads) s_list[i] = reinterpret_cast<const int2*>(lst)[e0 + i];
+    __syncthreads();
     auto issue = [&](int i) {
         if (lane == 0) {
             const int t = t0 + warp + kAttnWarps * i;
@@ -78,7 +85,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(StepParams p, AttnBu
                 const int idx = t * p.E + e;
                 const uint8_t* src = ab.zero_rec;
                 if (idx < nvalid) {
-                    const int32_t slot = lst[2 * idx + 1];
+                    const int32_t slot = s_list[idx - e0].y;
                     if (slot >= 0) src = seg_slots + (int64_t)slot * rec;
                 }
                 bulk_g2s_hint(dst + e * rec, src, (uint32_t)rec, b, pol);
@@ -122,8 +129,8 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(StepParams p, AttnBu
         {
             const int e_lo = row_lo / p.P, e_hi = row_hi / p.P;
             const int idx_lo = t * p.E + e_lo, idx_hi = t * p.E + e_hi;
-            vlo = idx_lo < nvalid && (int64_t)p.P * lst[2 * idx_lo] + (row_lo % p.P) < g.n;
-            vhi = idx_hi < nvalid && (int64_t)p.P * lst[2 * idx_hi] + (row_hi % p.P) < g.n;
+            vlo = idx_lo < nvalid && (int64_t)p.P * s_list[idx_lo - e0].x + (row_lo % p.P) < g.n;
+            vhi = idx_hi < nvalid && (int64_t)p.P * s_list[idx_hi - e0].x + (row_hi % p.P) < g.n;
         }
         mbar_wait(&my_bar[i % kAttnStages], (uint32_t)((i / kAttnStages) & 1));
         const uint32_t sbase = smem_u32(my_stage + (size_t)(i % kAttnStages) * kTileBytes);
@@ -183,6 +190,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(StepParams p, AttnBu
             issue(i + kAttnStages);
         }
     }
+    griddep_launch();
     // full row sums per head
 #pragma unroll
     for (int o = 4; o < 32; o <<= 1) {
@@ -249,13 +257,17 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(StepParams p, AttnBu
             pml[hh * 2 + 1] = l;
         }
     }
-    // ---- (a6) split merge in the last-arriving CTA of this segment
-    __threadfence();
+    // ---- (a6) split merge in the last-arriving CTA of this segment.  The barrier
+    // orders the CTA's partial writes before thread 0's gpu-scope fence (fence
+    // cumulativity), so one fence per CTA suffices.
     __syncthreads();
-    if (tid == 0) s_last = (atomicAdd(&ab.ctr[rs], 1u) == (uint32_t)(p.nsplit - 1));
+    if (tid == 0) {
+        __threadfence();
+        s_last = (atomicAdd(&ab.ctr[rs], 1u) == (uint32_t)(p.nsplit - 1));
+        if (s_last) __threadfence();
+    }
     __syncthreads();
     if (!s_last) return;
-    __threadfence();
     const float* po0 = ab.part_o + (rs * ab.max_splits * 8) * (int64_t)kHeadDim;
     const float* pml0 = ab.part_ml + (rs * ab.max_splits * 8) * 2;
     for (int hh = 0; hh < p.G; ++hh) {
@@ -285,7 +297,9 @@ cudaError_t launch_attention(kvd_cache* c, const StepParams& p, const uint16_t* 
         attr_set = true;
     }
     AttnBufs ab{c->slots, c->ntok_dev, c->zero_rec, c->part_o, c->part_ml, c->split_ctr, c->max_splits};
-    attn_kernel<<<dim3(p.nsplit, p.Hkv, p.B), kAttnThreads, kAttnSmem, s>>>(p, ab, q, attn, out, out_lse);
+    cudaError_t e = launch_pdl(attn_kernel, dim3(p.nsplit, p.Hkv, p.B), dim3(kAttnThreads), kAttnSmem, s, p, ab, q,
+                               attn, out, out_lse);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 

@@ -84,6 +84,7 @@ __global__ void __launch_bounds__(kResolveThreads) resolve_kernel(StepParams p, 
 
     // ---- 1. load + validate the selection (ascending, in range, not pinned)
     if (tid == 0) s_bad = 0;
+    griddep_wait();                               // ids / scores come from select
     __syncthreads();
     for (int i = tid; i < k; i += blockDim.x) {
         const int32_t b = S_in[i];
@@ -238,6 +239,7 @@ __global__ void __launch_bounds__(kResolveThreads) resolve_kernel(StepParams p, 
         atomicAdd(&rb.stats[4], (unsigned long long)nm * (unsigned long long)p.rec_bytes);
     }
     __syncthreads();
+    griddep_launch();
     // ---- 6. attention list: sink blocks ++ S ++ local blocks, ascending, with slots
     const int ns = g.sink_end, nl = g.nb - g.local_begin;
     for (int i = tid; i < p.W; i += blockDim.x) {
@@ -262,6 +264,7 @@ __global__ void __launch_bounds__(kGatherThreads) gather_kernel(StepParams p, co
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int64_t total = (int64_t)p.B * p.Hkv * p.k;
     const int chunks = p.rec_bytes / 16;
+    griddep_wait();                               // miss list comes from resolve
     for (int64_t w = warp; w < total; w += nwarps) {
         const int i = (int)(w % p.k);
         const int64_t bh = w / p.k;
@@ -302,10 +305,12 @@ cudaError_t launch_resolve(kvd_cache* c, const StepParams& p, const int32_t* ids
         if (e != cudaSuccess) return e;
         smem_set = smem;
     }
-    resolve_kernel<<<dim3(p.Hkv, p.B), kResolveThreads, smem, s>>>(p, rb, ids, out_attn);
+    cudaError_t e = launch_pdl(resolve_kernel, dim3(p.Hkv, p.B), dim3(kResolveThreads), smem, s, p, rb, ids, out_attn);
+    if (e != cudaSuccess) return e;
     if (!c->resident) {
-        gather_kernel<<<148 * 4, kGatherThreads, 0, s>>>(p, c->miss, c->miss_count, c->kmax, c->host_store,
-                                                          c->slots);
+        e = launch_pdl(gather_kernel, dim3(148 * 4), dim3(kGatherThreads), 0, s, p, (const int32_t*)c->miss,
+                       (const int32_t*)c->miss_count, (int)c->kmax, (const uint8_t*)c->host_store, c->slots);
+        if (e != cudaSuccess) return e;
     }
     return cudaGetLastError();
 }
