@@ -298,28 +298,34 @@ def run_gpu(args):
     hit_rate = st["hits"] / max(1, st["selected"])
     misses_per_seg = st["misses"] / max(1, args.steps * L * segs_per_layer)
 
-    # ---- per-kernel pass: the same steps launched eagerly with events around each ABI call
+    # ---- per-kernel pass: the same steps, each ABI call bracketed by CUDA events on the
+    # launching stream.  A GPU spin (torch.cuda._sleep) gates each step so the host has
+    # queued every launch before the device starts: the events then see device time only.
     kt = {"select": 0.0, "resolve_fetch": 0.0, "attn": 0.0}
-    evs = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(L)]
     npk = args.steps
     R.cache.set_device_step(None)
     for _ in range(npk):
         with torch.cuda.stream(s):
+            torch.cuda._sleep(20_000_000)            # ~10 ms at 1.965 GHz: covers the host enqueue
             R.q_cur.copy_(R.q_dev[R.t], non_blocking=True)
         R.t += 1
+        c = R.cache
         for l in range(L):
-            c = R.cache
-            evs[0].record(s)
+            e = evs[l]
+            e[0].record(s)
             c.select_topk(l, R.q_cur[l], R.reqs, cfg["k"], R.ids[l], None, stream=s)
-            evs[1].record(s)
+            e[1].record(s)
             c.resolve_and_fetch(l, R.reqs, R.ids[l], cfg["k"], R.t, R.attn[l], stream=s)
-            evs[2].record(s)
+            e[2].record(s)
             c.sparse_decode(l, R.q_cur[l], R.reqs, R.attn[l], R.W, R.out[l], R.lse[l], stream=s)
-            evs[3].record(s)
-            evs[3].synchronize()
-            kt["select"] += evs[0].elapsed_time(evs[1])
-            kt["resolve_fetch"] += evs[1].elapsed_time(evs[2])
-            kt["attn"] += evs[2].elapsed_time(evs[3])
+            e[3].record(s)
+        s.synchronize()
+        for l in range(L):
+            e = evs[l]
+            kt["select"] += e[0].elapsed_time(e[1])
+            kt["resolve_fetch"] += e[1].elapsed_time(e[2])
+            kt["attn"] += e[2].elapsed_time(e[3])
     nl = npk * L
     per_launch_ms = {key: v / nl for key, v in kt.items()}
     b = per_segment_bytes(cfg, misses_per_seg)

@@ -9,7 +9,7 @@
 //   table      [L][R][Hkv][nb_pad] int32 block -> slot | -1
 //   slot_block/last_use/phase/use_count [L][R][Hkv][C]
 //   miss       [R][Hkv][kmax] int2 (block, slot) + miss_count [R][Hkv]
-//   partials   [R][Hkv][max_splits][8][128] fp32 + (m, l) [R][Hkv][max_splits][8][2]
+//   partials   [R][Hkv][kMaxPieces][8][128] fp32 + (m, l) [R][Hkv][kMaxPieces][8][2]
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -23,7 +23,8 @@ constexpr int kScoreCols = 128;       // blocks per score-kernel tile (nb_pad mu
 constexpr int kAttnWarps = 4;         // warps per attention CTA
 constexpr int kAttnStages = 3;        // smem stages per warp
 constexpr int kTileBytes = 8192;      // one 16-token K||V tile
-constexpr int kSplitTiles = 16;       // 16-token tiles per split (one CTA)
+constexpr int kSplitTiles = 16;       // (legacy split size; StepParams.nsplit)
+constexpr int kMaxPieces = 32;        // attention partials per (request, KV head) (k_attn.cu)
 constexpr int64_t kSlotOfBytes = 64ll << 20;   // setup scratch for per-block slot targets
 
 struct SegGeom {                      // per-request pinned geometry (device copy in params)
@@ -68,6 +69,7 @@ struct kvd_cache {
     float* part_o = nullptr;
     float* part_ml = nullptr;
     uint32_t* split_ctr = nullptr;
+    uint32_t* sel_ctr = nullptr;           // [R][Hkv] select arrival counters
     unsigned long long* stats = nullptr;   // [5] kvd_stats fields
     int32_t* err = nullptr;
     int32_t* ntok_dev = nullptr;

@@ -1,23 +1,37 @@
 // k_attn.cu — rows (a5) split-K sparse decode attention and (a6) LSE merge.
 //
 // "executing attention ... over the union of the newly fetched and resident KV
-// entries".  Per (request, KV head, split) one CTA of 4 warps.
-// The attention list (selected + pinned blocks, from resolve) is cut into
-// 16-token tiles (E = 16/P list entries, 8 KiB); each warp streams its tiles
-// from the slot pool into a private 3-stage shared-memory ring with bulk async
-// copies (TMA engine) completing on mbarriers, then runs the two contractions
-// on tensor cores (mma.sync m16n8k16 bf16 -> fp32, swap-AB so the 16 tokens
-// fill M and the G <= 8 query heads of the KV head fill N):
-//     S^T[16 tok][8 h] = K[16][128] . Q^T            (8 MMAs)
-//     O^T[128][8 h]   += V^T[128][16] . (P_hi + P_lo)^T  (16 MMAs)
-// P is split into bf16 hi + lo parts so P.V keeps ~16 mantissa bits (a single
-// bf16 P misses the 2e-3 bar, SURVEY §7 hard part 4).  The S^T accumulator is
-// turned into the P^T B-fragment with movmatrix.trans.  Online softmax in the
-// log2 domain (exp2), warp-shuffle max/sum.  Warps merge through shared
-// memory; splits merge (a6) in the last-arriving CTA of the segment:
-//     m = max_s m_s;  l = sum_s l_s 2^(m_s-m);  o = sum_s 2^(m_s-m) o~_s / l;
+// entries".  The attention lists from resolve (selected +
+// pinned blocks, ascending) are cut into 16-token tiles (E = 16/P list
+// entries, 8 KiB).  The call's S = B*Hkv segments give T = S*TS tiles (TS =
+// ceil(W/E) per segment, uniform; entries past a segment's valid length read a
+// zero record and are masked).  The tile sequence is split evenly over NW warp
+// workers (stream-K: worker w owns tiles [w*T/NW, (w+1)*T/NW)), so every SM
+// streams the same number of tiles whatever B, Hkv and k are; a worker whose
+// range crosses a segment boundary produces one partial per segment piece.
+//
+// Per worker (one warp): a private STAGES-deep ring of 8 KiB tiles in shared
+// memory fed by bulk async copies (TMA engine) completing on mbarriers; the
+// (block, slot) entries are staged through shared memory 128 at a time so a
+// copy is never issued behind a dependent global load.  Per tile, on tensor
+// cores (mma.sync m16n8k16 bf16 -> fp32, swap-AB: 16 tokens fill M, heads N):
+//     S^T[16 tok][8] = K[16][128] . Q^T                   (8 MMAs)
+//     O^T[128][8]   += V^T[128][16] . P^T                  (8 or 16 MMAs)
+// P^T holds P = P_hi + P_lo (two bf16 parts; a single bf16 P misses the 2e-3
+// bar, R26).  For G <= 4 both parts share one MMA: columns 0-3 carry
+// P_hi of heads 0-3 and columns 4-7 P_lo of the same heads (Q^T columns 4-7
+// duplicate heads 0-3, so those lanes see identical softmax statistics); the
+// two output columns are summed in the epilogue.  For 4 < G <= 8 the hi and lo
+// parts take two MMAs.  The S^T accumulator becomes the P^T B-fragment with
+// movmatrix.trans.  Online softmax in the log2 domain (exp2).
+//
+// (a6) Pieces of a segment merge in the last-arriving worker:
+//     m = max_j m_j;  l = sum_j l_j 2^(m_j-m);  o = sum_j 2^(m_j-m) o~_j / l;
 //     lse = (m + log2 l) ln 2.
 // HBM-bound: 8 KiB per 16-token tile; 4*G flop per 4 B of K/V.
+#include <algorithm>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -27,127 +41,292 @@ struct AttnBufs {
     const uint8_t* slots;
     const int32_t* ntok;
     const uint8_t* zero_rec;
-    float* part_o;      // [R][Hkv][max_splits][8][128]
-    float* part_ml;     // [R][Hkv][max_splits][8][2]
-    uint32_t* ctr;      // [R][Hkv]
-    int32_t max_splits;
+    float* part_o;      // [R][Hkv][kMaxPieces][8][128]
+    float* part_ml;     // [R][Hkv][kMaxPieces][8][2]
+    uint32_t* ctr;      // [R][Hkv] pieces arrived
 };
 
 constexpr int kAttnThreads = kAttnWarps * 32;
-constexpr size_t kAttnSmem = (size_t)kAttnWarps * kAttnStages * kTileBytes;
+constexpr int kEntChunk = 128;                      // list entries staged per chunk (>= STAGES * 16)
 
-__global__ void __launch_bounds__(kAttnThreads) attn_kernel(StepParams p, AttnBufs ab, const uint16_t* __restrict__ q,
-                                                            const int32_t* __restrict__ attn,
-                                                            float* __restrict__ out, float* __restrict__ out_lse) {
+struct Work {
+    int32_t T;          // total tiles of the call (< 2^31: B <= 256, Hkv * TS small)
+    int32_t TS;         // tiles per segment
+    int32_t NW;         // workers
+};
+
+__device__ __forceinline__ int tile_begin(int w, const Work& wk) { return (int)((int64_t)w * wk.T / wk.NW); }
+__device__ __forceinline__ int worker_of(int t, const Work& wk) {
+    return (int)(((int64_t)(t + 1) * wk.NW - 1) / wk.T);
+}
+
+template <int STAGES>
+__global__ void __launch_bounds__(kAttnThreads, 1) attn_kernel(StepParams p, AttnBufs ab, Work wk,
+                                                               const uint16_t* __restrict__ q,
+                                                               const int32_t* __restrict__ attn,
+                                                               float* __restrict__ out, float* __restrict__ out_lse) {
     extern __shared__ __align__(1024) uint8_t stage[];
-    __shared__ __align__(8) uint64_t bar[kAttnWarps][kAttnStages];
-    __shared__ float red_m[kAttnWarps][8], red_l[kAttnWarps][8];
-    __shared__ int s_last;
-    __shared__ int2 s_list[kSplitTiles * 16];          // (block, slot) of the split's entries
-    const int split = blockIdx.x, h = blockIdx.y, bi = blockIdx.z;
-    const int r = p.req[bi];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const SegGeom g = seg_geom(ab.ntok[r], p.P, p.sink_tokens, p.local_tokens);
-    const int pr = g.sink_end + (g.nb - g.local_begin);
-    const int nvalid = min(p.W, p.k + pr);
-    const int ntiles = (nvalid + p.E - 1) / p.E;
-    const int t0 = split * kSplitTiles;
-    const int t1 = min(ntiles, t0 + kSplitTiles);
-    const int64_t seg = ((int64_t)p.layer * p.R + r) * p.Hkv + h;
-    const int64_t rs = (int64_t)r * p.Hkv + h;
-    const int32_t* lst = attn + ((int64_t)bi * p.Hkv + h) * (int64_t)p.W * 2;
-    const uint8_t* seg_slots = ab.slots + seg * p.C * (int64_t)p.rec_bytes;
-    const int rec = p.rec_bytes;
-
-    // this warp's tiles: t0 + warp + 4 i
-    const int nt_w = (t1 - t0 - warp + kAttnWarps - 1) / kAttnWarps > 0 ? (t1 - t0 - warp + kAttnWarps - 1) / kAttnWarps : 0;
-    uint8_t* my_stage = stage + (size_t)warp * kAttnStages * kTileBytes;
+    __shared__ __align__(8) uint64_t bar[kAttnWarps][STAGES];
+    __shared__ int2 s_ent[kAttnWarps][2][kEntChunk];
+    __shared__ float s_scale[kAttnWarps][kMaxPieces][8];    // merge weights of the pieces
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int w = blockIdx.x * kAttnWarps + warp;
+    uint8_t* my_stage = stage + (size_t)warp * STAGES * kTileBytes;
     uint64_t* my_bar = bar[warp];
     if (lane == 0) {
-        for (int s = 0; s < kAttnStages; ++s) mbar_init(&my_bar[s], 1);
+        for (int s = 0; s < STAGES; ++s) mbar_init(&my_bar[s], 1);
         fence_mbar_init();
     }
+    __syncwarp();
+    const int ta = w < wk.NW ? tile_begin(w, wk) : 0, tb = w < wk.NW ? tile_begin(w + 1, wk) : 0;
+    const int nt = tb - ta;
+    const int s_first = ta / wk.TS, i_first = ta - s_first * wk.TS;   // segment / tile-in-segment of tile ta
+    // P, E = 16/P and CT = kEntChunk/E >= STAGES (tiles per entry chunk) are powers of two: shifts, no divisions
+    const int logP = __ffs(p.P) - 1, logE = 4 - logP, logCT = 7 - logE;
+    const int E = 1 << logE, rec = p.rec_bytes, CT = 1 << logCT;
     const uint64_t pol = l2_evict_first_policy();
-    // everything below reads what resolve / gather (the previous kernels) wrote
-    griddep_wait();
-    // the split's (block, slot) entries -> shared memory, so issuing a tile's copy
-    // never waits on a dependent global load
-    const int e0 = t0 * p.E, ne = max(0, min(nvalid, t1 * p.E) - e0);
-    for (int i = tid; i < ne; i += kAttnThreads) s_list[i] = reinterpret_cast<const int2*>(lst)[e0 + i];
-    __syncthreads();
-    auto issue = [&](int i) {
+    const bool packed = p.G <= 4;
+    griddep_wait();                                // lists / slots / q come from earlier kernels
+    if (nt <= 0) return;
+
+    // stage entry chunk c (tiles ta + c*CT ..) into buffer c & 1: (block, slot), or (-1, -1).
+    // resolve pads each list past its valid length with (-1, -1); entries j >= W are tile padding.
+    auto load_chunk = [&](int c) {
+        for (int i = lane; i < kEntChunk; i += 32) {
+            const int k = (c << logCT) + (i >> logE);   // worker-relative tile
+            int2 v = make_int2(-1, -1);
+            if (k < nt) {
+                const int x = i_first + k;              // tile-in-segment relative to s_first
+                const int ds = x / wk.TS;
+                const int j = ((x - ds * wk.TS) << logE) + (i & (E - 1));
+                if (j < p.W) v = reinterpret_cast<const int2*>(attn)[(int64_t)(s_first + ds) * p.W + j];
+            }
+            s_ent[warp][c & 1][i] = v;
+        }
+        __syncwarp();
+    };
+    // issue side: tile ik goes to stage ist; its segment's slot base is tracked incrementally
+    int ik = 0, ist = 0, is_seg = s_first - 1, is_left = 0;
+    const uint8_t* is_slots = nullptr;
+    auto issue = [&]() {
+        if (is_left == 0) {
+            ++is_seg;
+            is_left = is_seg == s_first ? wk.TS - i_first : wk.TS;
+            const int bi = is_seg / p.Hkv, h = is_seg - bi * p.Hkv;
+            is_slots = ab.slots + (((int64_t)p.layer * p.R + p.req[bi]) * p.Hkv + h) * p.C * (int64_t)rec;
+        }
         if (lane == 0) {
-            const int t = t0 + warp + kAttnWarps * i;
-            uint64_t* b = &my_bar[i % kAttnStages];
-            uint8_t* dst = my_stage + (size_t)(i % kAttnStages) * kTileBytes;
-            mbar_arrive_expect_tx(b, (uint32_t)(p.E * rec));
-            for (int e = 0; e < p.E; ++e) {
-                const int idx = t * p.E + e;
-                const uint8_t* src = ab.zero_rec;
-                if (idx < nvalid) {
-                    const int32_t slot = s_list[idx - e0].y;
-                    if (slot >= 0) src = seg_slots + (int64_t)slot * rec;
-                }
+            uint64_t* b = &my_bar[ist];
+            uint8_t* dst = my_stage + (size_t)ist * kTileBytes;
+            mbar_arrive_expect_tx(b, (uint32_t)(E * rec));
+            const int2* ent = &s_ent[warp][(ik >> logCT) & 1][(ik & (CT - 1)) << logE];
+            for (int e = 0; e < E; ++e) {
+                const int32_t slot = ent[e].y;
+                const uint8_t* src = slot >= 0 ? is_slots + (int64_t)slot * rec : ab.zero_rec;
                 bulk_g2s_hint(dst + e * rec, src, (uint32_t)rec, b, pol);
             }
         }
+        --is_left;
+        ++ik;
+        ist = ist + 1 == STAGES ? 0 : ist + 1;
     };
-    for (int i = 0; i < kAttnStages && i < nt_w; ++i) issue(i);
+    load_chunk(0);
+    while (ik < STAGES && ik < nt) issue();
 
-    // Q^T B-fragments: head = lane/4 (< G), dims 16 kk + 2 (lane%4) + {0,1} and +8
-    uint32_t qf[8][2];
-    {
-        const int hd = lane >> 2;
-        const uint16_t* qh = q + ((int64_t)bi * p.Hq + (int64_t)h * p.G + hd) * kHeadDim + 2 * (lane & 3);
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-            qf[kk][0] = hd < p.G ? *reinterpret_cast<const uint32_t*>(qh + 16 * kk) : 0u;
-            qf[kk][1] = hd < p.G ? *reinterpret_cast<const uint32_t*>(qh + 16 * kk + 8) : 0u;
-        }
-    }
     // per-lane ldmatrix row offsets.  K (non-trans): matrix i = lane/8 -> row (lane&7) + 8 (i&1),
     // chunk 2kk + (i>>1).  V (trans): row (lane&7) + 8 (i>>1), chunk 2mt + (i&1).
     const int mi = lane >> 3;
     const int rk = (lane & 7) + 8 * (mi & 1), rv = (lane & 7) + 8 * (mi >> 1);
-    const uint32_t koff = (uint32_t)((rk / p.P) * rec + (rk % p.P) * kRowBytes);
-    const uint32_t kswz = (uint32_t)((rk % p.P) & 7);
-    const uint32_t voff = (uint32_t)((rv / p.P) * rec + p.P * kRowBytes + (rv % p.P) * kRowBytes);
-    const uint32_t vswz = (uint32_t)((rv % p.P) & 7);
+    const int pm = p.P - 1;
+    const uint32_t koff = (uint32_t)((rk >> logP) * rec + (rk & pm) * kRowBytes);
+    const uint32_t kswz = (uint32_t)((rk & pm) & 7);
+    const uint32_t voff = (uint32_t)((rv >> logP) * rec + p.P * kRowBytes + (rv & pm) * kRowBytes);
+    const uint32_t vswz = (uint32_t)((rv & pm) & 7);
     const int kchunk_hi = mi >> 1, vchunk_hi = mi & 1;
-    // the two token rows this thread's accumulators hold
-    const int row_lo = lane >> 2, row_hi = row_lo + 8;
+    const int row_lo = lane >> 2, row_hi = row_lo + 8;     // token rows of this lane's accumulators
+    const int quad = lane & 3;                              // accumulator columns 2 quad, 2 quad + 1
+    const bool lo_lane = packed && quad >= 2;               // packed: this lane's columns carry P_lo
+    const float kLn2 = 0.69314718055994531f;
 
+    uint32_t qf[8][2];
     float oacc[8][4];
-#pragma unroll
-    for (int mt = 0; mt < 8; ++mt) oacc[mt][0] = oacc[mt][1] = oacc[mt][2] = oacc[mt][3] = 0.f;
-    float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;   // heads h0 = 2 (lane%4), h1 = h0 + 1
+    float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+    int cs = -1;                                            // current segment
+    int n_cur = 0;
 
-    for (int i = 0; i < nt_w; ++i) {
-        const int t = t0 + warp + kAttnWarps * i;
-        // token validity of this thread's two rows
-        bool vlo, vhi;
-        {
-            const int e_lo = row_lo / p.P, e_hi = row_hi / p.P;
-            const int idx_lo = t * p.E + e_lo, idx_hi = t * p.E + e_hi;
-            vlo = idx_lo < nvalid && (int64_t)p.P * s_list[idx_lo - e0].x + (row_lo % p.P) < g.n;
-            vhi = idx_hi < nvalid && (int64_t)p.P * s_list[idx_hi - e0].x + (row_hi % p.P) < g.n;
+    // flush the running piece of segment cs: partial or (single piece) final output
+    auto flush = [&]() {
+#pragma unroll
+        for (int o = 4; o < 32; o <<= 1) {
+            l0 += __shfl_xor_sync(0xffffffffu, l0, o);
+            l1 += __shfl_xor_sync(0xffffffffu, l1, o);
         }
-        mbar_wait(&my_bar[i % kAttnStages], (uint32_t)((i / kAttnStages) & 1));
-        const uint32_t sbase = smem_u32(my_stage + (size_t)(i % kAttnStages) * kTileBytes);
-
-        float sacc[4] = {0.f, 0.f, 0.f, 0.f};
+        if (packed) {
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-            uint32_t a0, a1, a2, a3;
-            const uint32_t c = (uint32_t)(2 * kk + kchunk_hi);
+            for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) oacc[mt][c] += __shfl_xor_sync(0xffffffffu, oacc[mt][c], 2);
+        }
+        const int bi = cs / p.Hkv, h = cs - bi * p.Hkv;
+        const int64_t rs = (int64_t)p.req[bi] * p.Hkv + h;
+        const int s0 = cs * wk.TS;
+        const int fw = worker_of(s0, wk), lw = worker_of(s0 + wk.TS - 1, wk);
+        const int np = lw - fw + 1;
+        const int h0 = 2 * quad, h1 = h0 + 1, d = lane >> 2;
+        const bool own = !packed || quad < 2;               // lanes holding real head columns
+        if (np == 1) {
+            if (own) {
+                const float i0 = l0 > 0.f ? 1.f / l0 : 0.f, i1 = l1 > 0.f ? 1.f / l1 : 0.f;
+#pragma unroll
+                for (int mt = 0; mt < 8; ++mt) {
+                    if (h0 < p.G) {
+                        float* o = out + ((int64_t)bi * p.Hq + (int64_t)h * p.G + h0) * kHeadDim + 16 * mt + d;
+                        o[0] = oacc[mt][0] * i0;
+                        o[8] = oacc[mt][2] * i0;
+                    }
+                    if (h1 < p.G) {
+                        float* o = out + ((int64_t)bi * p.Hq + (int64_t)h * p.G + h1) * kHeadDim + 16 * mt + d;
+                        o[0] = oacc[mt][1] * i1;
+                        o[8] = oacc[mt][3] * i1;
+                    }
+                }
+                if (out_lse && d == 0) {
+                    const int64_t ob = (int64_t)bi * p.Hq + (int64_t)h * p.G;
+                    if (h0 < p.G) out_lse[ob + h0] = l0 > 0.f ? (m0 + log2f(l0)) * kLn2 : -INFINITY;
+                    if (h1 < p.G) out_lse[ob + h1] = l1 > 0.f ? (m1 + log2f(l1)) * kLn2 : -INFINITY;
+                }
+            }
+            return;
+        }
+        const int j = w - fw;
+        float* po = ab.part_o + ((rs * kMaxPieces + j) * 8) * (int64_t)kHeadDim;
+        float* pml = ab.part_ml + ((rs * kMaxPieces + j) * 8) * 2;
+        if (own) {
+#pragma unroll
+            for (int mt = 0; mt < 8; ++mt) {
+                po[h0 * kHeadDim + 16 * mt + d] = oacc[mt][0];
+                po[h1 * kHeadDim + 16 * mt + d] = oacc[mt][1];
+                po[h0 * kHeadDim + 16 * mt + 8 + d] = oacc[mt][2];
+                po[h1 * kHeadDim + 16 * mt + 8 + d] = oacc[mt][3];
+            }
+            if (d == 0) {
+                pml[h0 * 2] = m0;
+                pml[h0 * 2 + 1] = l0;
+                pml[h1 * 2] = m1;
+                pml[h1 * 2 + 1] = l1;
+            }
+        }
+        __threadfence();
+        __syncwarp();
+        uint32_t last = 0;
+        if (lane == 0) last = atomicAdd(&ab.ctr[rs], 1u) == (uint32_t)(np - 1);
+        last = __shfl_sync(0xffffffffu, last, 0);
+        if (!last) return;
+        __threadfence();
+        // (a6) merge the np <= 32 pieces, all heads at once.  Phase 1: lane jj holds piece jj's
+        // (m, l) of every head; per-head max / weighted sum by warp reductions; the weights
+        // 2^(m_jj - M) go to shared memory.  Phase 2: lane owns dims 4 lane .. +3 of every head
+        // and sums the np partials with independent loads.
+        const float* po0 = ab.part_o + (rs * kMaxPieces * 8) * (int64_t)kHeadDim;
+        const float* pml0 = ab.part_ml + (rs * kMaxPieces * 8) * 2;
+        float Mh[8], lh[8];
+        float mj[8], lj[8];
+#pragma unroll
+        for (int hh = 0; hh < 8; ++hh) {
+            mj[hh] = (lane < np && hh < p.G) ? __ldcg(&pml0[(lane * 8 + hh) * 2]) : -INFINITY;
+            lj[hh] = (lane < np && hh < p.G) ? __ldcg(&pml0[(lane * 8 + hh) * 2 + 1]) : 0.f;
+        }
+#pragma unroll
+        for (int hh = 0; hh < 8; ++hh) {
+            float M = mj[hh];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+            const float scj = (lane < np && M != -INFINITY) ? fast_exp2(mj[hh] - M) : 0.f;
+            float l = scj * lj[hh];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+            s_scale[warp][lane][hh] = scj;
+            Mh[hh] = M;
+            lh[hh] = l;
+        }
+        __syncwarp();
+        float4 acc[8];
+#pragma unroll
+        for (int hh = 0; hh < 8; ++hh) acc[hh] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 2
+        for (int jj = 0; jj < np; ++jj) {
+#pragma unroll
+            for (int hh = 0; hh < 8; ++hh) {
+                if (hh < p.G) {
+                    const float sc = s_scale[warp][jj][hh];
+                    const float4 x = __ldcg(reinterpret_cast<const float4*>(po0 + (jj * 8 + hh) * kHeadDim) + lane);
+                    acc[hh].x += sc * x.x; acc[hh].y += sc * x.y; acc[hh].z += sc * x.z; acc[hh].w += sc * x.w;
+                }
+            }
+        }
+#pragma unroll
+        for (int hh = 0; hh < 8; ++hh) {
+            if (hh < p.G) {
+                const float il = lh[hh] > 0.f ? 1.f / lh[hh] : 0.f;
+                const int64_t oh = (int64_t)bi * p.Hq + (int64_t)h * p.G + hh;
+                reinterpret_cast<float4*>(out + oh * kHeadDim)[lane] =
+                    make_float4(acc[hh].x * il, acc[hh].y * il, acc[hh].z * il, acc[hh].w * il);
+                if (out_lse && lane == 0) out_lse[oh] = lh[hh] > 0.f ? (Mh[hh] + log2f(lh[hh])) * kLn2 : -INFINITY;
+            }
+        }
+        if (lane == 0) ab.ctr[rs] = 0u;
+    };
+
+    int seg_left = 0;                                       // tiles left in the current segment
+    int st = 0;                                             // consumer stage
+    uint32_t ph = 0;                                        // its mbarrier phase
+    for (int k = 0; k < nt; ++k) {
+        if (seg_left == 0) {                                // new segment piece
+            if (cs >= 0) flush();
+            cs = cs < 0 ? s_first : cs + 1;
+            seg_left = cs == s_first ? wk.TS - i_first : wk.TS;
+            const int bi = cs / p.Hkv, h = cs - bi * p.Hkv;
+            n_cur = ab.ntok[p.req[bi]];
+            // Q^T B-fragments: column n = lane/4 -> head n (packed: n & 3), dims 16 kk + 2 quad + {0,1} (+8)
+            const int hd = packed ? (lane >> 2) & 3 : lane >> 2;
+            const uint16_t* qh = q + ((int64_t)bi * p.Hq + (int64_t)h * p.G + hd) * kHeadDim + 2 * quad;
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+                qf[kk][0] = hd < p.G ? *reinterpret_cast<const uint32_t*>(qh + 16 * kk) : 0u;
+                qf[kk][1] = hd < p.G ? *reinterpret_cast<const uint32_t*>(qh + 16 * kk + 8) : 0u;
+            }
+#pragma unroll
+            for (int mt = 0; mt < 8; ++mt) oacc[mt][0] = oacc[mt][1] = oacc[mt][2] = oacc[mt][3] = 0.f;
+            m0 = m1 = -INFINITY;
+            l0 = l1 = 0.f;
+        }
+        --seg_left;
+        // token validity of this lane's two rows
+        const int2* ent = &s_ent[warp][(k >> logCT) & 1][(k & (CT - 1)) << logE];
+        const int2 elo = ent[row_lo >> logP], ehi = ent[row_hi >> logP];
+        const bool vlo = elo.x >= 0 && (elo.x << logP) + (row_lo & pm) < n_cur;
+        const bool vhi = ehi.x >= 0 && (ehi.x << logP) + (row_hi & pm) < n_cur;
+        mbar_wait(&my_bar[st], ph);
+        const uint32_t sbase = smem_u32(my_stage + (size_t)st * kTileBytes);
+
+        // S^T = K . Q^T as two independent accumulation chains (even / odd 16-dim slices)
+        float sacc[4] = {0.f, 0.f, 0.f, 0.f}, sacc2[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int kk = 0; kk < 8; kk += 2) {
+            uint32_t a0, a1, a2, a3, b0, b1, b2, b3;
+            const uint32_t c = (uint32_t)(2 * kk + kchunk_hi), c2 = c + 2;
             ldsm_x4(sbase + koff + ((c ^ kswz) << 4), a0, a1, a2, a3);
+            ldsm_x4(sbase + koff + ((c2 ^ kswz) << 4), b0, b1, b2, b3);
             mma_bf16_16816(sacc, a0, a1, a2, a3, qf[kk][0], qf[kk][1]);
+            mma_bf16_16816(sacc2, b0, b1, b2, b3, qf[kk + 1][0], qf[kk + 1][1]);
         }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) sacc[i] += sacc2[i];
         // online softmax (log2 domain)
-        const float x0 = vlo ? sacc[0] * p.scale_log2 : -INFINITY;   // row_lo, h0
-        const float x1 = vlo ? sacc[1] * p.scale_log2 : -INFINITY;   // row_lo, h1
-        const float x2 = vhi ? sacc[2] * p.scale_log2 : -INFINITY;   // row_hi, h0
-        const float x3 = vhi ? sacc[3] * p.scale_log2 : -INFINITY;   // row_hi, h1
+        const float x0 = vlo ? sacc[0] * p.scale_log2 : -INFINITY;   // row_lo, col 2 quad
+        const float x1 = vlo ? sacc[1] * p.scale_log2 : -INFINITY;   // row_lo, col 2 quad + 1
+        const float x2 = vhi ? sacc[2] * p.scale_log2 : -INFINITY;   // row_hi, col 2 quad
+        const float x3 = vhi ? sacc[3] * p.scale_log2 : -INFINITY;   // row_hi, col 2 quad + 1
         float mx0 = fmaxf(x0, x2), mx1 = fmaxf(x1, x3);
 #pragma unroll
         for (int o = 4; o < 32; o <<= 1) {
@@ -163,144 +342,97 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(StepParams p, AttnBu
         m1 = mn1;
         l0 = l0 * al0 + (p0 + p2);
         l1 = l1 * al1 + (p1 + p3);
+        if (__any_sync(0xffffffffu, al0 != 1.f || al1 != 1.f)) {   // running max moved somewhere
 #pragma unroll
-        for (int mt = 0; mt < 8; ++mt) {
-            oacc[mt][0] *= al0;
-            oacc[mt][1] *= al1;
-            oacc[mt][2] *= al0;
-            oacc[mt][3] *= al1;
+            for (int mt = 0; mt < 8; ++mt) {
+                oacc[mt][0] *= al0;
+                oacc[mt][1] *= al1;
+                oacc[mt][2] *= al0;
+                oacc[mt][3] *= al1;
+            }
         }
-        // P^T B-fragments (hi and lo bf16 parts) via movmatrix.trans
-        const uint32_t hlo = pack_bf16x2(p0, p1), hhi = pack_bf16x2(p2, p3);
-        const uint32_t llo = pack_bf16x2(p0 - bf16_lo(hlo), p1 - bf16_hi(hlo));
-        const uint32_t lhi = pack_bf16x2(p2 - bf16_lo(hhi), p3 - bf16_hi(hhi));
-        const uint32_t bh0 = movmatrix_t(hlo), bh1 = movmatrix_t(hhi);
-        const uint32_t bl0 = movmatrix_t(llo), bl1 = movmatrix_t(lhi);
+        // P^T B-fragments via movmatrix.trans (hardware RNE packs)
+        const uint32_t hlo = cvt_bf16x2(p0, p1), hhi = cvt_bf16x2(p2, p3);
+        const uint32_t llo = cvt_bf16x2(p0 - bf16_lo(hlo), p1 - bf16_hi(hlo));
+        const uint32_t lhi = cvt_bf16x2(p2 - bf16_lo(hhi), p3 - bf16_hi(hhi));
+        if (packed) {
+            const uint32_t b0 = movmatrix_t(lo_lane ? llo : hlo), b1 = movmatrix_t(lo_lane ? lhi : hhi);
 #pragma unroll
-        for (int mt = 0; mt < 8; ++mt) {
-            uint32_t a0, a1, a2, a3;
-            const uint32_t c = (uint32_t)(2 * mt + vchunk_hi);
-            ldsm_x4_t(sbase + voff + ((c ^ vswz) << 4), a0, a1, a2, a3);
-            mma_bf16_16816(oacc[mt], a0, a1, a2, a3, bh0, bh1);
-            mma_bf16_16816(oacc[mt], a0, a1, a2, a3, bl0, bl1);
+            for (int mt = 0; mt < 8; ++mt) {
+                uint32_t a0, a1, a2, a3;
+                const uint32_t c = (uint32_t)(2 * mt + vchunk_hi);
+                ldsm_x4_t(sbase + voff + ((c ^ vswz) << 4), a0, a1, a2, a3);
+                mma_bf16_16816(oacc[mt], a0, a1, a2, a3, b0, b1);
+            }
+        } else {
+            const uint32_t bh0 = movmatrix_t(hlo), bh1 = movmatrix_t(hhi);
+            const uint32_t bl0 = movmatrix_t(llo), bl1 = movmatrix_t(lhi);
+#pragma unroll
+            for (int mt = 0; mt < 8; ++mt) {
+                uint32_t a0, a1, a2, a3;
+                const uint32_t c = (uint32_t)(2 * mt + vchunk_hi);
+                ldsm_x4_t(sbase + voff + ((c ^ vswz) << 4), a0, a1, a2, a3);
+                mma_bf16_16816(oacc[mt], a0, a1, a2, a3, bh0, bh1);
+                mma_bf16_16816(oacc[mt], a0, a1, a2, a3, bl0, bl1);
+            }
         }
         __syncwarp();
-        if (i + kAttnStages < nt_w) {
+        if (ik < nt) {                                      // refill the stage just consumed
+            if ((ik & (CT - 1)) == 0) load_chunk(ik >> logCT);
             fence_proxy_async();
-            issue(i + kAttnStages);
+            issue();
         }
+        st = st + 1 == STAGES ? 0 : st + 1;
+        ph ^= st == 0 ? 1u : 0u;
     }
     griddep_launch();
-    // full row sums per head
-#pragma unroll
-    for (int o = 4; o < 32; o <<= 1) {
-        l0 += __shfl_xor_sync(0xffffffffu, l0, o);
-        l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+    flush();
+}
+
+template <int STAGES>
+static cudaError_t launch_attn_s(kvd_cache* c, const StepParams& p, const uint16_t* q, const int32_t* attn, float* out,
+                                 float* out_lse, cudaStream_t s) {
+    constexpr size_t smem = (size_t)kAttnWarps * STAGES * kTileBytes;
+    static int max_ctas = 0;
+    if (!max_ctas) {
+        cudaError_t e = cudaFuncSetAttribute(attn_kernel<STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        int per_sm = 0, sms = 0, dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, attn_kernel<STAGES>, kAttnThreads, smem);
+        if (e != cudaSuccess) return e;
+        max_ctas = sms * (per_sm > 0 ? per_sm : 1);
     }
-    // ---- merge the 4 warps through shared memory (reuse the stage ring)
-    __syncthreads();
-    float* red_o = reinterpret_cast<float*>(stage);   // [warp][8 heads][128 dims]
-    {
-        const int h0 = 2 * (lane & 3), h1 = h0 + 1, d = lane >> 2;
-        float* ro = red_o + (size_t)warp * 8 * kHeadDim;
-#pragma unroll
-        for (int mt = 0; mt < 8; ++mt) {
-            ro[h0 * kHeadDim + 16 * mt + d] = oacc[mt][0];
-            ro[h1 * kHeadDim + 16 * mt + d] = oacc[mt][1];
-            ro[h0 * kHeadDim + 16 * mt + 8 + d] = oacc[mt][2];
-            ro[h1 * kHeadDim + 16 * mt + 8 + d] = oacc[mt][3];
-        }
-        if (lane < 4) {
-            red_m[warp][h0] = m0;
-            red_m[warp][h1] = m1;
-            red_l[warp][h0] = l0;
-            red_l[warp][h1] = l1;
-        }
-    }
-    __syncthreads();
-    const int dim = tid;   // kAttnThreads == 128 == head_dim
-    const float kLn2 = 0.69314718055994531f;
-    if (p.nsplit == 1) {
-        for (int hh = 0; hh < p.G; ++hh) {
-            float M = -INFINITY;
-            for (int w = 0; w < kAttnWarps; ++w) M = fmaxf(M, red_m[w][hh]);
-            float o = 0.f, l = 0.f;
-            if (M != -INFINITY) {
-                for (int w = 0; w < kAttnWarps; ++w) {
-                    const float sc = fast_exp2(red_m[w][hh] - M);
-                    o += sc * red_o[((size_t)w * 8 + hh) * kHeadDim + dim];
-                    l += sc * red_l[w][hh];
-                }
-            }
-            const int64_t oh = (int64_t)bi * p.Hq + (int64_t)h * p.G + hh;
-            out[oh * kHeadDim + dim] = l > 0.f ? o / l : 0.f;
-            if (out_lse && dim == 0) out_lse[oh] = l > 0.f ? (M + log2f(l)) * kLn2 : -INFINITY;
-        }
-        return;
-    }
-    float* po = ab.part_o + ((rs * ab.max_splits + split) * 8) * (int64_t)kHeadDim;
-    float* pml = ab.part_ml + ((rs * ab.max_splits + split) * 8) * 2;
-    for (int hh = 0; hh < p.G; ++hh) {
-        float M = -INFINITY;
-        for (int w = 0; w < kAttnWarps; ++w) M = fmaxf(M, red_m[w][hh]);
-        float o = 0.f, l = 0.f;
-        if (M != -INFINITY) {
-            for (int w = 0; w < kAttnWarps; ++w) {
-                const float sc = fast_exp2(red_m[w][hh] - M);
-                o += sc * red_o[((size_t)w * 8 + hh) * kHeadDim + dim];
-                l += sc * red_l[w][hh];
-            }
-        }
-        po[hh * kHeadDim + dim] = o;
-        if (dim == 0) {
-            pml[hh * 2] = M;
-            pml[hh * 2 + 1] = l;
-        }
-    }
-    // ---- (a6) split merge in the last-arriving CTA of this segment.  The barrier
-    // orders the CTA's partial writes before thread 0's gpu-scope fence (fence
-    // cumulativity), so one fence per CTA suffices.
-    __syncthreads();
-    if (tid == 0) {
-        __threadfence();
-        s_last = (atomicAdd(&ab.ctr[rs], 1u) == (uint32_t)(p.nsplit - 1));
-        if (s_last) __threadfence();
-    }
-    __syncthreads();
-    if (!s_last) return;
-    const float* po0 = ab.part_o + (rs * ab.max_splits * 8) * (int64_t)kHeadDim;
-    const float* pml0 = ab.part_ml + (rs * ab.max_splits * 8) * 2;
-    for (int hh = 0; hh < p.G; ++hh) {
-        float M = -INFINITY;
-        for (int s = 0; s < p.nsplit; ++s) M = fmaxf(M, __ldcg(&pml0[(s * 8 + hh) * 2]));
-        float o = 0.f, l = 0.f;
-        if (M != -INFINITY) {
-            for (int s = 0; s < p.nsplit; ++s) {
-                const float ms = __ldcg(&pml0[(s * 8 + hh) * 2]);
-                const float sc = fast_exp2(ms - M);
-                o += sc * __ldcg(&po0[(s * 8 + hh) * kHeadDim + dim]);
-                l += sc * __ldcg(&pml0[(s * 8 + hh) * 2 + 1]);
-            }
-        }
-        const int64_t oh = (int64_t)bi * p.Hq + (int64_t)h * p.G + hh;
-        out[oh * kHeadDim + dim] = l > 0.f ? o / l : 0.f;
-        if (out_lse && dim == 0) out_lse[oh] = l > 0.f ? (M + log2f(l)) * kLn2 : -INFINITY;
-    }
-    if (tid == 0) ab.ctr[rs] = 0u;
+    const int S = p.B * p.Hkv;
+    Work wk;
+    wk.TS = (p.W + p.E - 1) / p.E;
+    wk.T = S * wk.TS;
+    // workers: enough to fill every SM, but at most kMaxPieces - 1 per segment so a
+    // segment never has more than kMaxPieces pieces (<= ceil(NW/S) + 1), and at most T
+    int nw = max_ctas * kAttnWarps;
+    nw = std::min(nw, S * (kMaxPieces - 1));
+    nw = std::min(nw, wk.T);
+    wk.NW = std::max(nw, 1);
+    AttnBufs ab{c->slots, c->ntok_dev, c->zero_rec, c->part_o, c->part_ml, c->split_ctr};
+    const unsigned grid = (unsigned)((wk.NW + kAttnWarps - 1) / kAttnWarps);
+    cudaError_t e = launch_pdl(attn_kernel<STAGES>, dim3(grid), dim3(kAttnThreads), smem, s, p, ab, wk, q, attn, out,
+                               out_lse);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
 }
 
 cudaError_t launch_attention(kvd_cache* c, const StepParams& p, const uint16_t* q, const int32_t* attn, float* out,
                              float* out_lse, cudaStream_t s) {
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAttnSmem);
-        attr_set = true;
+    // ring depth per warp worker; KVD_ATTN_STAGES (3 or 6) overrides for experiments
+    static int stages = 0;
+    if (!stages) {
+        const char* env = getenv("KVD_ATTN_STAGES");
+        stages = env ? atoi(env) : 6;
+        if (stages != 3 && stages != 6) stages = 6;
     }
-    AttnBufs ab{c->slots, c->ntok_dev, c->zero_rec, c->part_o, c->part_ml, c->split_ctr, c->max_splits};
-    cudaError_t e = launch_pdl(attn_kernel, dim3(p.nsplit, p.Hkv, p.B), dim3(kAttnThreads), kAttnSmem, s, p, ab, q,
-                               attn, out, out_lse);
-    if (e != cudaSuccess) return e;
-    return cudaGetLastError();
+    if (stages == 3) return launch_attn_s<3>(c, p, q, attn, out, out_lse, s);
+    return launch_attn_s<6>(c, p, q, attn, out, out_lse, s);
 }
 
 }  // namespace kvd

@@ -7,26 +7,27 @@
 // HBM-bound: 256 B of summary per block.  The summaries are dim-major, so a
 // thread owning V consecutive blocks reads one V*2-byte vector per dim row and
 // a warp reads 64*V contiguous bytes per row (coalesced).  No shared-memory
-// staging: each thread keeps 8 rows of its blocks in flight (double-buffered
-// registers) and runs V independent chains.  V in {2, 4, 8} is picked so the
+// staging: each thread keeps 16-32 rows of its blocks in flight (two ping-pong
+// register batches) and runs V independent chains.  V in {2, 4, 8} is picked so the
 // grid has >= 2 CTAs per SM.  Rows for the first batch are requested before
 // griddepcontrol.wait (summaries are immutable during a step), overlapping
 // the previous kernel's tail.
 //
-// (a2) "retrieving only the Top-K important chunks": one
-// 1024-thread CTA per segment.  Thread t owns the contiguous blocks
-// [t*KPT, (t+1)*KPT) (keys in registers when nb <= 16384).  A 3-pass radix
-// select (11 + 11 + 10 bits, warp-aggregated shared histograms) finds the
-// k-th largest monotone key T among the candidates; keys > T are taken and the
-// kk lowest-id keys == T (R10).  Two block scans give tie ranks and output
-// positions, so ids come out ascending with no sort.
+// (a2) "retrieving only the Top-K important chunks", fused:
+// the last scoring CTA of a segment to finish (arrival counter per segment)
+// selects that segment's top-k while other CTAs keep streaming summaries.
+// Thread t owns the contiguous blocks [t*KPT*reps, (t+1)*KPT*reps) (keys in
+// registers when reps == 1).  A 3-pass radix select (11 + 11 + 10 bits,
+// warp-aggregated shared histograms) finds the k-th largest monotone key T
+// among the candidates; keys > T are taken and the kk lowest-id keys == T
+// (R10).  Two block scans give tie ranks and output positions, so ids come out
+// ascending with no sort.
 #include "common.cuh"
 #include "internal.h"
 
 namespace kvd {
 
 constexpr int kScoreThreads = 256;
-constexpr int kScoreRows = 8;                 // dim rows in flight per thread
 
 template <int V>
 struct VecOf;
@@ -49,29 +50,25 @@ struct VecOf<8> {
 };
 
 template <int V>
-__global__ void __launch_bounds__(kScoreThreads) score_kernel(StepParams p, const uint16_t* __restrict__ q,
-                                                              const uint16_t* __restrict__ summ,
-                                                              float* __restrict__ scores,
-                                                              const int32_t* __restrict__ ntok) {
+__device__ __forceinline__ void score_tile(const StepParams& p, int bi, int h, int64_t nb, int64_t seg,
+                                           const uint16_t* __restrict__ q, const uint16_t* __restrict__ summ,
+                                           float* __restrict__ scores, float* qbar) {
     using Vec = typename VecOf<V>::T;
-    __shared__ float qbar[kHeadDim];
-    const int bi = blockIdx.z, h = blockIdx.y;
-    const int r = p.req[bi];
-    const int64_t cta0 = (int64_t)blockIdx.x * kScoreThreads * V;
-    const int n = ntok[r];                        // written only by kvd_load_prefix (setup)
-    const int64_t nb = (n + p.P - 1) / p.P;
-    if (cta0 >= nb) return;                       // whole CTA past this request's end
-    const int64_t b0 = cta0 + (int64_t)threadIdx.x * V;
+    const int64_t b0 = (int64_t)blockIdx.x * kScoreThreads * V + (int64_t)threadIdx.x * V;
     const bool ld = b0 < nb;                      // V-groups never straddle nb_pad (V | 128)
-    const int64_t seg = ((int64_t)p.layer * p.R + r) * p.Hkv + h;
     const Vec* base = reinterpret_cast<const Vec*>(summ + seg * kHeadDim * p.nb_pad + (ld ? b0 : 0));
     const int64_t rstride = p.nb_pad / V;         // Vec elements per dim row
-
-    Vec buf[kScoreRows], cur[kScoreRows];
+    // two register batches of R rows (ping-pong): while one batch is consumed the
+    // other is in flight, so 2R rows of this thread's blocks are always requested
+    constexpr int R = V == 8 ? 8 : 16;
+    Vec bufA[R], bufB[R];
 #pragma unroll
-    for (int u = 0; u < kScoreRows; ++u)
-        if (ld) buf[u] = __ldcs(base + u * rstride);
-    griddep_wait();
+    for (int u = 0; u < R; ++u)
+        if (ld) bufA[u] = __ldcs(base + u * rstride);
+#pragma unroll
+    for (int u = 0; u < R; ++u)
+        if (ld) bufB[u] = __ldcs(base + (R + u) * rstride);
+    griddep_wait();                               // summaries are immutable; q may come from an earlier kernel
     if (threadIdx.x < kHeadDim) {
         // group query: qbar[j] = ((+0 + q_0[j]) + q_1[j]) + ... (fp32, g ascending; R3)
         const uint16_t* qh = q + ((int64_t)bi * p.Hq + (int64_t)h * p.G) * kHeadDim;
@@ -83,22 +80,28 @@ __global__ void __launch_bounds__(kScoreThreads) score_kernel(StepParams p, cons
     float acc[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) acc[v] = 0.0f;
-#pragma unroll 1
-    for (int j0 = 0; j0 < kHeadDim; j0 += kScoreRows) {
+    auto consume = [&](const Vec (&buf)[R], int j0) {
 #pragma unroll
-        for (int u = 0; u < kScoreRows; ++u) cur[u] = buf[u];
-        if (ld && j0 + kScoreRows < kHeadDim) {
-#pragma unroll
-            for (int u = 0; u < kScoreRows; ++u) buf[u] = __ldcs(base + (j0 + kScoreRows + u) * rstride);
-        }
-#pragma unroll
-        for (int u = 0; u < kScoreRows; ++u) {
+        for (int u = 0; u < R; ++u) {
             const float qj = qbar[j0 + u];
 #pragma unroll
             for (int v = 0; v < V; ++v) {
-                const uint32_t w = VecOf<V>::word(cur[u], v >> 1);
+                const uint32_t w = VecOf<V>::word(buf[u], v >> 1);
                 acc[v] = __fmaf_rn(qj, (v & 1) ? bf16_hi(w) : bf16_lo(w), acc[v]);   // sequential in j (R5)
             }
+        }
+    };
+#pragma unroll 1
+    for (int j0 = 0; j0 < kHeadDim; j0 += 2 * R) {
+        consume(bufA, j0);
+        if (ld && j0 + 2 * R < kHeadDim) {
+#pragma unroll
+            for (int u = 0; u < R; ++u) bufA[u] = __ldcs(base + (j0 + 2 * R + u) * rstride);
+        }
+        consume(bufB, j0 + R);
+        if (ld && j0 + 3 * R < kHeadDim) {
+#pragma unroll
+            for (int u = 0; u < R; ++u) bufB[u] = __ldcs(base + (j0 + 3 * R + u) * rstride);
         }
     }
     griddep_launch();
@@ -114,44 +117,29 @@ __global__ void __launch_bounds__(kScoreThreads) score_kernel(StepParams p, cons
     }
 }
 
-constexpr int kTopkThreads = 1024;
+struct TopkSmem {
+    int hist[2048];
+    int scan[33];
+    uint32_t digit;
+    int above;
+};
 
-// KPT keys per thread per chunk; `reps` chunks per thread (reps > 1 re-reads
-// the scores from L2 in every pass instead of keeping them in registers).
+// Top-k of one segment by the whole CTA (kScoreThreads threads).
 template <int KPT>
-__global__ void __launch_bounds__(kTopkThreads, 1) topk_kernel(StepParams p, const float* __restrict__ scores,
-                                                            const int32_t* __restrict__ ntok, int reps,
-                                                            int32_t* __restrict__ out_ids,
-                                                            float* __restrict__ out_scores) {
-    __shared__ int hist[2048];
-    __shared__ int scan_scratch[33];
-    __shared__ uint32_t s_digit;
-    __shared__ int s_above;
-    const int bi = blockIdx.y, h = blockIdx.x;
-    const int r = p.req[bi];
-    const int tid = threadIdx.x;
-    if (p.k == 0) return;
-    const SegGeom g = seg_geom(ntok[r], p.P, p.sink_tokens, p.local_tokens);
-    const int64_t seg = ((int64_t)p.layer * p.R + r) * p.Hkv + h;
-    const float* sc = scores + seg * p.nb_pad;
-    griddep_wait();
-
+__device__ void topk_segment(const StepParams& p, const SegGeom& g, const float* __restrict__ sc, int reps,
+                             int32_t* __restrict__ ids_out, float* __restrict__ sc_out, TopkSmem& sm) {
+    const int tid = threadIdx.x, nthr = blockDim.x;
     uint32_t key[KPT];
-    uint32_t cm = 0;                         // candidate mask of the chunk in registers
+    uint32_t cm = 0;                              // candidate mask of the chunk in registers
     auto load = [&](int c) {
         const int64_t b0 = ((int64_t)tid * reps + c) * KPT;
         cm = 0;
         if (b0 >= g.nb) return;
         float f[KPT];
-        if constexpr (KPT % 4 == 0) {
 #pragma unroll
-            for (int i = 0; i < KPT; i += 4) {
-                const float4 x = __ldcg(reinterpret_cast<const float4*>(sc + b0 + i));
-                f[i] = x.x; f[i + 1] = x.y; f[i + 2] = x.z; f[i + 3] = x.w;
-            }
-        } else {
-#pragma unroll
-            for (int i = 0; i < KPT; ++i) f[i] = __ldcg(sc + b0 + i);
+        for (int i = 0; i < KPT; i += 4) {
+            const float4 x = __ldcg(reinterpret_cast<const float4*>(sc + b0 + i));
+            f[i] = x.x; f[i + 1] = x.y; f[i + 2] = x.z; f[i + 3] = x.w;
         }
 #pragma unroll
         for (int i = 0; i < KPT; ++i) {
@@ -170,7 +158,7 @@ __global__ void __launch_bounds__(kTopkThreads, 1) topk_kernel(StepParams p, con
     for (int pass = 0; pass < 3; ++pass) {
         const int shift = pass == 0 ? 21 : pass == 1 ? 10 : 0;
         const int nbins = pass == 2 ? 1024 : 2048;
-        for (int i = tid; i < nbins; i += kTopkThreads) hist[i] = 0;
+        for (int i = tid; i < nbins; i += nthr) sm.hist[i] = 0;
         __syncthreads();
 #pragma unroll 1
         for (int c = 0; c < reps; ++c) {
@@ -178,34 +166,35 @@ __global__ void __launch_bounds__(kTopkThreads, 1) topk_kernel(StepParams p, con
 #pragma unroll
             for (int i = 0; i < KPT; ++i) {
                 const bool act = ((cm >> i) & 1u) && (key[i] & mask) == prefix;
-                warp_hist_add(hist, (key[i] >> shift) & (uint32_t)(nbins - 1), act);
+                warp_hist_add(sm.hist, (key[i] >> shift) & (uint32_t)(nbins - 1), act);
             }
         }
         __syncthreads();
-        // bins in descending order: thread t owns bins nbins-1-2t and nbins-2-2t (pass 2: one bin)
-        int c0 = 0, c1 = 0;
-        const int d0 = nbins == 2048 ? 2047 - 2 * tid : 1023 - tid;
-        c0 = hist[d0];
-        if (nbins == 2048) c1 = hist[d0 - 1];
+        // bins in descending order; thread t owns bins [nbins - (t+1) bpt, nbins - t bpt)
+        const int bpt = nbins / nthr;             // 8 or 4 (256 threads)
+        int cnt = 0;
+        for (int i = 0; i < bpt; ++i) cnt += sm.hist[nbins - 1 - (tid * bpt + i)];
         int tot;
-        const int above = block_exclusive_scan(c0 + c1, scan_scratch, &tot);
-        if (above < kk && kk <= above + c0 + c1) {
-            if (above + c0 >= kk) {
-                s_digit = (uint32_t)d0;
-                s_above = above;
-            } else {
-                s_digit = (uint32_t)(d0 - 1);
-                s_above = above + c0;
+        int above = block_exclusive_scan(cnt, sm.scan, &tot);
+        if (above < kk && kk <= above + cnt) {
+            for (int i = 0; i < bpt; ++i) {
+                const int d = nbins - 1 - (tid * bpt + i);
+                const int ci = sm.hist[d];
+                if (above + ci >= kk) {
+                    sm.digit = (uint32_t)d;
+                    sm.above = above;
+                    break;
+                }
+                above += ci;
             }
         }
         __syncthreads();
-        prefix |= s_digit << shift;
+        prefix |= sm.digit << shift;
         mask |= (uint32_t)(nbins - 1) << shift;
-        kk -= s_above;
+        kk -= sm.above;
         __syncthreads();
     }
-    griddep_launch();
-    const uint32_t T = prefix;               // take keys > T, and the kk lowest-id keys == T
+    const uint32_t T = prefix;                    // take keys > T, and the kk lowest-id keys == T
 
     // ---- tie ranks and output positions (thread-contiguous ownership => ascending ids)
     int ngt = 0, neq = 0;
@@ -220,11 +209,9 @@ __global__ void __launch_bounds__(kTopkThreads, 1) topk_kernel(StepParams p, con
         }
     }
     int tot;
-    const int tie0 = block_exclusive_scan(neq, scan_scratch, &tot);
+    const int tie0 = block_exclusive_scan(neq, sm.scan, &tot);
     const int ntake = min(max(kk - tie0, 0), neq);
-    const int pos0 = block_exclusive_scan(ngt + ntake, scan_scratch, &tot);
-    int32_t* ids_out = out_ids + ((int64_t)bi * p.Hkv + h) * p.k;
-    float* sc_out = out_scores ? out_scores + ((int64_t)bi * p.Hkv + h) * p.k : nullptr;
+    const int pos0 = block_exclusive_scan(ngt + ntake, sm.scan, &tot);
     int pos = pos0, tie = tie0;
 #pragma unroll 1
     for (int c = 0; c < reps; ++c) {
@@ -244,18 +231,64 @@ __global__ void __launch_bounds__(kTopkThreads, 1) topk_kernel(StepParams p, con
     }
 }
 
-template <int V>
-static cudaError_t launch_score(kvd_cache* c, const StepParams& p, const uint16_t* q, cudaStream_t s) {
-    const unsigned tiles = (unsigned)((c->nb_pad + kScoreThreads * V - 1) / (kScoreThreads * V));
-    return launch_pdl(score_kernel<V>, dim3(tiles, p.Hkv, p.B), dim3(kScoreThreads), 0, s, p, q,
-                      (const uint16_t*)c->summ, c->scores, (const int32_t*)c->ntok_dev);
+// grid (tiles per segment, Hkv, B); CTA = kScoreThreads threads scoring kScoreThreads*V blocks.
+template <int V, int KPT>
+__global__ void __launch_bounds__(kScoreThreads, 2) select_kernel(StepParams p, const uint16_t* __restrict__ q,
+                                                                  const uint16_t* __restrict__ summ,
+                                                                  float* __restrict__ scores,
+                                                                  const int32_t* __restrict__ ntok,
+                                                                  uint32_t* __restrict__ sel_ctr, int reps,
+                                                                  int32_t* __restrict__ out_ids,
+                                                                  float* __restrict__ out_scores) {
+    __shared__ float qbar[kHeadDim];
+    __shared__ TopkSmem sm;
+    __shared__ int s_last;
+    const int bi = blockIdx.z, h = blockIdx.y;
+    const int r = p.req[bi];
+    const int n = ntok[r];                        // written only by kvd_load_prefix (setup)
+    const int64_t nb = (n + p.P - 1) / p.P;
+    const int64_t bpc = (int64_t)kScoreThreads * V;
+    if ((int64_t)blockIdx.x * bpc >= nb) return;  // whole CTA past this request's end (does not arrive)
+    const int64_t seg = ((int64_t)p.layer * p.R + r) * p.Hkv + h;
+    score_tile<V>(p, bi, h, nb, seg, q, summ, scores, qbar);
+    if (p.k == 0) return;
+    // ---- the last CTA of the segment to finish runs its top-k
+    const int64_t rs = (int64_t)r * p.Hkv + h;
+    const uint32_t ntiles = (uint32_t)((nb + bpc - 1) / bpc);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(&sel_ctr[rs], 1u) == ntiles - 1;
+        if (s_last) {
+            sel_ctr[rs] = 0u;
+            __threadfence();
+        }
+    }
+    __syncthreads();
+    if (!s_last) return;
+    const SegGeom g = seg_geom(n, p.P, p.sink_tokens, p.local_tokens);
+    int32_t* ids_out = out_ids + ((int64_t)bi * p.Hkv + h) * p.k;
+    float* sc_out = out_scores ? out_scores + ((int64_t)bi * p.Hkv + h) * p.k : nullptr;
+    topk_segment<KPT>(p, g, scores + seg * p.nb_pad, reps, ids_out, sc_out, sm);
 }
 
-template <int KPT>
-static cudaError_t launch_topk(kvd_cache* c, const StepParams& p, int reps, int32_t* out_ids, float* out_scores,
-                               cudaStream_t s) {
-    return launch_pdl(topk_kernel<KPT>, dim3(p.Hkv, p.B), dim3(kTopkThreads), 0, s, p, (const float*)c->scores,
-                      (const int32_t*)c->ntok_dev, reps, out_ids, out_scores);
+template <int V, int KPT>
+static cudaError_t launch_sel(kvd_cache* c, const StepParams& p, const uint16_t* q, int reps, int32_t* out_ids,
+                              float* out_scores, cudaStream_t s) {
+    const unsigned tiles = (unsigned)((c->nb_pad + kScoreThreads * V - 1) / (kScoreThreads * V));
+    return launch_pdl(select_kernel<V, KPT>, dim3(tiles, p.Hkv, p.B), dim3(kScoreThreads), 0, s, p, q,
+                      (const uint16_t*)c->summ, c->scores, (const int32_t*)c->ntok_dev, c->sel_ctr, reps, out_ids,
+                      out_scores);
+}
+
+template <int V>
+static cudaError_t launch_sel_v(kvd_cache* c, const StepParams& p, const uint16_t* q, int32_t* out_ids,
+                                float* out_scores, cudaStream_t s) {
+    const int64_t per = (c->nb_pad + kScoreThreads - 1) / kScoreThreads;   // blocks per top-k thread
+    if (per <= 4) return launch_sel<V, 4>(c, p, q, 1, out_ids, out_scores, s);
+    if (per <= 8) return launch_sel<V, 8>(c, p, q, 1, out_ids, out_scores, s);
+    if (per <= 16) return launch_sel<V, 16>(c, p, q, 1, out_ids, out_scores, s);
+    return launch_sel<V, 32>(c, p, q, (int)((per + 31) / 32), out_ids, out_scores, s);
 }
 
 cudaError_t launch_select(kvd_cache* c, const StepParams& p, const uint16_t* q, int32_t* out_ids, float* out_scores,
@@ -264,17 +297,9 @@ cudaError_t launch_select(kvd_cache* c, const StepParams& p, const uint16_t* q, 
     const int64_t segs = (int64_t)p.B * p.Hkv;
     auto ctas = [&](int V) { return segs * ((c->nb_pad + kScoreThreads * V - 1) / (kScoreThreads * V)); };
     cudaError_t e;
-    if (ctas(8) >= 2 * 148) e = launch_score<8>(c, p, q, s);
-    else if (ctas(4) >= 2 * 148) e = launch_score<4>(c, p, q, s);
-    else e = launch_score<2>(c, p, q, s);
-    if (e != cudaSuccess) return e;
-    const int64_t per = (c->nb_pad + kTopkThreads - 1) / kTopkThreads;   // blocks per thread
-    if (per <= 1) e = launch_topk<1>(c, p, 1, out_ids, out_scores, s);
-    else if (per <= 2) e = launch_topk<2>(c, p, 1, out_ids, out_scores, s);
-    else if (per <= 4) e = launch_topk<4>(c, p, 1, out_ids, out_scores, s);
-    else if (per <= 8) e = launch_topk<8>(c, p, 1, out_ids, out_scores, s);
-    else if (per <= 16) e = launch_topk<16>(c, p, 1, out_ids, out_scores, s);
-    else e = launch_topk<16>(c, p, (int)((per + 15) / 16), out_ids, out_scores, s);
+    if (ctas(8) >= 2 * 148) e = launch_sel_v<8>(c, p, q, out_ids, out_scores, s);
+    else if (ctas(4) >= 2 * 148) e = launch_sel_v<4>(c, p, q, out_ids, out_scores, s);
+    else e = launch_sel_v<2>(c, p, q, out_ids, out_scores, s);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }

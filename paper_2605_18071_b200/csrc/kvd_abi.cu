@@ -76,8 +76,8 @@ kvd_status check_config(const kvd_config* cfg, Geometry* g) {
     g->A = (cfg->host_layer_alias <= 0 || cfg->host_layer_alias > g->L) ? g->L : cfg->host_layer_alias;
     g->rec_bytes = 2ll * P * kRowBytes;
     const int64_t wmax = g->kmax + g->pmax;
-    g->max_splits = (int)(((wmax + g->E - 1) / g->E + kSplitTiles - 1) / kSplitTiles);
-    if (g->max_splits < 1) g->max_splits = 1;
+    (void)wmax;
+    g->max_splits = kMaxPieces;
     if ((int64_t)g->Hkv * g->nb_max * 4 > kSlotOfBytes) return fail(KVD_EINVAL, "context too long for setup scratch");
     return KVD_OK;
 }
@@ -100,7 +100,7 @@ Sizes sizes_of(const Geometry& g) {
     s.miss = rsegs * (size_t)(g.kmax > 0 ? g.kmax : 1) * 2 * 4 + rsegs * 4;
     s.part_o = rsegs * g.max_splits * 8 * kHeadDim * 4;
     s.part_ml = rsegs * g.max_splits * 8 * 2 * 4;
-    s.small = rsegs * 4 + 64 + 4 + (size_t)g.R * 4 + g.rec_bytes;
+    s.small = rsegs * 8 + 64 + 4 + (size_t)g.R * 4 + g.rec_bytes;
     s.host = g.resident ? 0 : (size_t)g.A * g.R * g.Hkv * g.nb_max * g.rec_bytes;
     return s;
 }
@@ -215,6 +215,7 @@ kvd_status kvd_create_cache(const kvd_config* cfg, kvd_cache** out) {
     ALLOC(part_o, s.part_o);
     ALLOC(part_ml, s.part_ml);
     ALLOC(split_ctr, rsegs * 4);
+    ALLOC(sel_ctr, rsegs * 4);
     ALLOC(stats, 64);
     ALLOC(err, 4);
     ALLOC(ntok_dev, (size_t)g.R * 4);
@@ -225,6 +226,7 @@ kvd_status kvd_create_cache(const kvd_config* cfg, kvd_cache** out) {
     if (e == cudaSuccess) e = cudaMemset(c->slot_block, 0xFF, s.meta4);
     if (e == cudaSuccess) e = cudaMemset(c->miss_count, 0, rsegs * 4);
     if (e == cudaSuccess) e = cudaMemset(c->split_ctr, 0, rsegs * 4);
+    if (e == cudaSuccess) e = cudaMemset(c->sel_ctr, 0, rsegs * 4);
     if (e == cudaSuccess) e = cudaMemset(c->stats, 0, 64);
     if (e == cudaSuccess) e = cudaMemset(c->err, 0, 4);
     if (e == cudaSuccess) e = cudaMemset(c->ntok_dev, 0, (size_t)g.R * 4);
@@ -248,7 +250,7 @@ void kvd_destroy_cache(kvd_cache* c) {
     cudaSetDevice(c->cfg.device);
     cudaDeviceSynchronize();
     void* dev[] = {c->slots, c->summ, c->scores, c->table, c->slot_block, c->last_use, c->phase,
-                   c->use_count, c->miss, c->miss_count, c->part_o, c->part_ml, c->split_ctr, c->stats,
+                   c->use_count, c->miss, c->miss_count, c->part_o, c->part_ml, c->split_ctr, c->sel_ctr, c->stats,
                    c->err, c->ntok_dev, c->zero_rec, c->stage_kv, c->stage_rec};
     for (void* p : dev)
         if (p) cudaFree(p);
