@@ -35,16 +35,16 @@ sys.path.insert(0, ROOT)
 
 # BASELINE.json configs: per-rank shapes.
 CONFIGS = {
-    "c1": dict(L=1, B=1, Hq=8, Hkv=2, n=4096, P=16, k=32, C=None, alias=0,
+    "c1": dict(chains=1, L=1, B=1, Hq=8, Hkv=2, n=4096, P=16, k=32, C=None, alias=0,
                desc="1 req, 1 layer, 8q/2kv, d128, 4k ctx, block 16, top-k 32, resident"),
-    "c2": dict(L=32, B=8, Hq=32, Hkv=8, n=32768, P=16, k=128, C=None, alias=0,
+    "c2": dict(chains=2, L=32, B=8, Hq=32, Hkv=8, n=32768, P=16, k=128, C=None, alias=0,
                desc="Llama-3.1-8B shapes (32 layers, 32q/8kv, d128) bf16, 32k ctx, batch 8, top-k 2048 tokens, resident"),
-    "c3": dict(L=32, B=16, Hq=32, Hkv=8, n=131072, P=16, k=128, C=2048, alias=4,
+    "c3": dict(chains=4, L=32, B=16, Hq=32, Hkv=8, n=131072, P=16, k=128, C=2048, alias=4,
                desc="Llama-3.1-8B shapes, 128k ctx, batch 16, GPU cache 25% of KV (2048 slots/segment), misses "
                     "gathered from pinned host DRAM, top-k 2048 tokens"),
-    "c4": dict(L=28, B=4, Hq=28, Hkv=4, n=1 << 20, P=16, k=128, C=16384, alias=2,
+    "c4": dict(chains=2, L=28, B=4, Hq=28, Hkv=4, n=1 << 20, P=16, k=128, C=16384, alias=2,
                desc="Qwen2.5-7B-1M shapes (28 layers, 28q/4kv, d128), 1M ctx, batch 4, GPU cache 25%, host-backed"),
-    "c5": dict(L=32, B=64, Hq=32, Hkv=8, n=131072, P=16, k=128, C=768, alias=2,
+    "c5": dict(chains=4, L=32, B=64, Hq=32, Hkv=8, n=131072, P=16, k=128, C=768, alias=2,
                desc="Llama-3.1-8B shapes, 128k ctx, batch 64, GPU cache 768 slots/segment (9.4%), host-backed"),
 }
 METRIC = "decode tokens/s at 128k ctx; sparse-attn HBM GB/s % peak; fetch GB/s, 1-8 GPU"
@@ -67,6 +67,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch layer by layer instead of graph replay")
+    ap.add_argument("--chains", type=int, default=None,
+                    help="micro-batch chains (SFC overlap): the batch is split into this many request groups, "
+                         "each run through all layers on its own stream inside the graph")
     ap.add_argument("--layers", type=int, default=None, help="override L (profiling only; not a bench number)")
     ap.add_argument("--cpu-sample-s", type=float, default=12.0, help="target seconds of oracle work")
     return ap.parse_args()
@@ -183,14 +186,22 @@ class Runner:
         self.out_host = torch.empty_like(self.out, device="cpu").pin_memory()
         self.step_dev = torch.zeros(1, dtype=torch.int32, device=dev)
         self.t = 0                     # next step index to run (query row)
-        self.launches_per_step = L * (4 if self.resident else 5)
+        m = args.chains if args.chains else cfg.get("chains", 1)
+        m = max(1, min(m, B))
+        edges = [round(i * B / m) for i in range(m + 1)]
+        self.chains = [(edges[i], edges[i + 1]) for i in range(m) if edges[i + 1] > edges[i]]
+        self.chain_streams = [torch.cuda.Stream(device=dev) for _ in self.chains]
+        self.launches_per_step = L * (3 if self.resident else 4) * len(self.chains)
 
-    # one layer through the three ABI calls
-    def layer(self, l, s, step=0):
+    # one layer of one chain (requests b0..b1-1) through the three ABI calls
+    def layer(self, l, s, step=0, chain=None):
         c, k = self.cache, self.cfg["k"]
-        c.select_topk(l, self.q_cur[l], self.reqs, k, self.ids[l], None, stream=s)
-        c.resolve_and_fetch(l, self.reqs, self.ids[l], k, step, self.attn[l], stream=s)
-        c.sparse_decode(l, self.q_cur[l], self.reqs, self.attn[l], self.W, self.out[l], self.lse[l], stream=s)
+        b0, b1 = chain if chain else (0, len(self.reqs))
+        reqs = self.reqs[b0:b1]
+        q = self.q_cur[l, b0:b1]
+        c.select_topk(l, q, reqs, k, self.ids[l, b0:b1], None, stream=s)
+        c.resolve_and_fetch(l, reqs, self.ids[l, b0:b1], k, step, self.attn[l, b0:b1], stream=s)
+        c.sparse_decode(l, q, reqs, self.attn[l, b0:b1], self.W, self.out[l, b0:b1], self.lse[l, b0:b1], stream=s)
 
     def eager_step(self, s):
         torch = self.torch
@@ -207,8 +218,15 @@ class Runner:
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=s):
             self.step_dev.add_(1)
-            for l in range(self.cfg["L"]):
-                self.layer(l, torch.cuda.current_stream())
+            # SFC overlap: each request group runs its own chain of layers on its own stream
+            # (fork from / join to the capture stream); groups share no state, so the GPU
+            # overlaps one chain's host-link gathers with the others' HBM-bound kernels
+            for ch, cs in zip(self.chains, self.chain_streams):
+                cs.wait_stream(s)
+                for l in range(self.cfg["L"]):
+                    self.layer(l, cs, chain=ch)
+            for cs in self.chain_streams:
+                s.wait_stream(cs)
         self.graph = g
 
     def graph_step(self, s, source="dev"):
@@ -390,7 +408,7 @@ def run_gpu(args):
                    "layers": L, "q_heads": cfg["Hq"], "kv_heads": Hkv, "block_tokens": cfg["P"],
                    "top_k_blocks": cfg["k"], "slots_per_segment": cfg["C"] or (cfg["n"] // cfg["P"]),
                    "policy": args.policy, "alpha": args.alpha, "host_layer_alias": R.A if not R.resident else None,
-                   "fill_steps": R.fill, "graph": not args.no_graph, "parallelism": f"request-shard x{world}",
+                   "fill_steps": R.fill, "graph": not args.no_graph, "chains": len(R.chains), "parallelism": f"request-shard x{world}",
                    "l2": "inputs larger than L2 (no flush)"},
         "hit_rate": hit_rate, "misses_per_segment": misses_per_seg,
         "roofline": roof, "roofline_attn": roof_attn, "kernels": kernels,

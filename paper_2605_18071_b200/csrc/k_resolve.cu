@@ -308,7 +308,7 @@ cudaError_t launch_resolve(kvd_cache* c, const StepParams& p, const int32_t* ids
     cudaError_t e = launch_pdl(resolve_kernel, dim3(p.Hkv, p.B), dim3(kResolveThreads), smem, s, p, rb, ids, out_attn);
     if (e != cudaSuccess) return e;
     if (!c->resident) {
-        e = launch_pdl(gather_kernel, dim3(148 * 4), dim3(kGatherThreads), 0, s, p, (const int32_t*)c->miss,
+        e = launch_pdl(gather_kernel, dim3(148), dim3(kGatherThreads), 0, s, p, (const int32_t*)c->miss,
                        (const int32_t*)c->miss_count, (int)c->kmax, (const uint8_t*)c->host_store, c->slots);
         if (e != cudaSuccess) return e;
     }
