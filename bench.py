@@ -37,14 +37,14 @@ sys.path.insert(0, ROOT)
 CONFIGS = {
     "c1": dict(chains=1, L=1, B=1, Hq=8, Hkv=2, n=4096, P=16, k=32, C=None, alias=0,
                desc="1 req, 1 layer, 8q/2kv, d128, 4k ctx, block 16, top-k 32, resident"),
-    "c2": dict(chains=2, L=32, B=8, Hq=32, Hkv=8, n=32768, P=16, k=128, C=None, alias=0,
+    "c2": dict(chains=1, L=32, B=8, Hq=32, Hkv=8, n=32768, P=16, k=128, C=None, alias=0,
                desc="Llama-3.1-8B shapes (32 layers, 32q/8kv, d128) bf16, 32k ctx, batch 8, top-k 2048 tokens, resident"),
-    "c3": dict(chains=4, L=32, B=16, Hq=32, Hkv=8, n=131072, P=16, k=128, C=2048, alias=4,
+    "c3": dict(chains=16, L=32, B=16, Hq=32, Hkv=8, n=131072, P=16, k=128, C=2048, alias=4,
                desc="Llama-3.1-8B shapes, 128k ctx, batch 16, GPU cache 25% of KV (2048 slots/segment), misses "
                     "gathered from pinned host DRAM, top-k 2048 tokens"),
-    "c4": dict(chains=2, L=28, B=4, Hq=28, Hkv=4, n=1 << 20, P=16, k=128, C=16384, alias=2,
+    "c4": dict(chains=4, L=28, B=4, Hq=28, Hkv=4, n=1 << 20, P=16, k=128, C=16384, alias=2,
                desc="Qwen2.5-7B-1M shapes (28 layers, 28q/4kv, d128), 1M ctx, batch 4, GPU cache 25%, host-backed"),
-    "c5": dict(chains=4, L=32, B=64, Hq=32, Hkv=8, n=131072, P=16, k=128, C=768, alias=2,
+    "c5": dict(chains=16, L=32, B=64, Hq=32, Hkv=8, n=131072, P=16, k=128, C=768, alias=2,
                desc="Llama-3.1-8B shapes, 128k ctx, batch 64, GPU cache 768 slots/segment (9.4%), host-backed"),
 }
 METRIC = "decode tokens/s at 128k ctx; sparse-attn HBM GB/s % peak; fetch GB/s, 1-8 GPU"

@@ -31,6 +31,9 @@
 // HBM-bound: 8 KiB per 16-token tile; 4*G flop per 4 B of K/V.
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
+#include <vector>
+#include <cstdio>
 
 #include "common.cuh"
 #include "internal.h"
@@ -53,7 +56,19 @@ struct Work {
     int32_t T;          // total tiles of the call (< 2^31: B <= 256, Hkv * TS small)
     int32_t TS;         // tiles per segment
     int32_t NW;         // workers
+    int32_t xflags;     // timing experiments only (KVD_ATTN_X): 1 = skip S MMAs, 2 = skip P.V MMAs
+    unsigned long long* trace;   // KVD_ATTN_TRACE: per-warp globaltimer stamps [NW][8] (experiments only)
 };
+
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define ATTN_STAMP(i)                                                         \
+    do {                                                                      \
+        if (wk.trace && lane == 0 && w < wk.NW) wk.trace[(int64_t)w * 8 + (i)] = gtime(); \
+    } while (0)
 
 __device__ __forceinline__ int tile_begin(int w, const Work& wk) { return (int)((int64_t)w * wk.T / wk.NW); }
 __device__ __forceinline__ int worker_of(int t, const Work& wk) {
@@ -86,7 +101,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_kernel(StepParams p, Att
     const int E = 1 << logE, rec = p.rec_bytes, CT = 1 << logCT;
     const uint64_t pol = l2_evict_first_policy();
     const bool packed = p.G <= 4;
+    ATTN_STAMP(0);
     griddep_wait();                                // lists / slots / q come from earlier kernels
+    ATTN_STAMP(1);
     if (nt <= 0) return;
 
     // stage entry chunk c (tiles ta + c*CT ..) into buffer c & 1: (block, slot), or (-1, -1).
@@ -222,6 +239,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_kernel(StepParams p, Att
         if (lane == 0) last = atomicAdd(&ab.ctr[rs], 1u) == (uint32_t)(np - 1);
         last = __shfl_sync(0xffffffffu, last, 0);
         if (!last) return;
+        ATTN_STAMP(4);
         __threadfence();
         // (a6) merge the np <= 32 pieces, all heads at once.  Phase 1: lane jj holds piece jj's
         // (m, l) of every head; per-head max / weighted sum by warp reductions; the weights
@@ -275,12 +293,144 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_kernel(StepParams p, Att
             }
         }
         if (lane == 0) ab.ctr[rs] = 0u;
+        ATTN_STAMP(5);
     };
 
     int seg_left = 0;                                       // tiles left in the current segment
-    int st = 0;                                             // consumer stage
+    int st = 0;                                             // stage of the next tile to consume
     uint32_t ph = 0;                                        // its mbarrier phase
-    for (int k = 0; k < nt; ++k) {
+
+    // Consume NT (1 or 2) tiles of the current segment: the two tiles' S chains, one softmax
+    // update over their 16 NT tokens and their P.V products are interleaved for ILP.
+    auto step = [&](auto nt_tag, int k) {
+        constexpr int NT = decltype(nt_tag)::value;
+        uint32_t sb[NT];
+        bool vlo[NT], vhi[NT];
+        int st_t = st;
+        uint32_t ph_t = ph;
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+            const int kt = k + t;
+            const int2* ent = &s_ent[warp][(kt >> logCT) & 1][(kt & (CT - 1)) << logE];
+            const int2 elo = ent[row_lo >> logP], ehi = ent[row_hi >> logP];
+            vlo[t] = elo.x >= 0 && (elo.x << logP) + (row_lo & pm) < n_cur;
+            vhi[t] = ehi.x >= 0 && (ehi.x << logP) + (row_hi & pm) < n_cur;
+            mbar_wait(&my_bar[st_t], ph_t);
+            if (kt == 0) ATTN_STAMP(2);
+            sb[t] = smem_u32(my_stage + (size_t)st_t * kTileBytes);
+            st_t = st_t + 1 == STAGES ? 0 : st_t + 1;
+            ph_t ^= st_t == 0 ? 1u : 0u;
+        }
+        st = st_t;
+        ph = ph_t;
+        // S^T = K . Q^T: two accumulation chains (even / odd 16-dim slices) per tile
+        float sacc[NT][4], sacc2[NT][4];
+#pragma unroll
+        for (int t = 0; t < NT; ++t)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) sacc[t][i] = sacc2[t][i] = 0.f;
+#pragma unroll
+        for (int kk = 0; kk < 8; kk += 2) {
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                uint32_t a0, a1, a2, a3, b0, b1, b2, b3;
+                const uint32_t c = (uint32_t)(2 * kk + kchunk_hi), c2 = c + 2;
+                ldsm_x4(sb[t] + koff + ((c ^ kswz) << 4), a0, a1, a2, a3);
+                ldsm_x4(sb[t] + koff + ((c2 ^ kswz) << 4), b0, b1, b2, b3);
+                if (!(wk.xflags & 1)) {
+                    mma_bf16_16816(sacc[t], a0, a1, a2, a3, qf[kk][0], qf[kk][1]);
+                    mma_bf16_16816(sacc2[t], b0, b1, b2, b3, qf[kk + 1][0], qf[kk + 1][1]);
+                } else {
+                    sacc[t][0] += __uint_as_float(a0 & b0); sacc2[t][1] += __uint_as_float(a1 & b3);
+                }
+            }
+        }
+        // online softmax (log2 domain) over the NT tiles
+        float x[NT][4];
+        float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+            x[t][0] = vlo[t] ? (sacc[t][0] + sacc2[t][0]) * p.scale_log2 : -INFINITY;   // row_lo, col 2 quad
+            x[t][1] = vlo[t] ? (sacc[t][1] + sacc2[t][1]) * p.scale_log2 : -INFINITY;   // row_lo, col 2 quad + 1
+            x[t][2] = vhi[t] ? (sacc[t][2] + sacc2[t][2]) * p.scale_log2 : -INFINITY;   // row_hi, col 2 quad
+            x[t][3] = vhi[t] ? (sacc[t][3] + sacc2[t][3]) * p.scale_log2 : -INFINITY;   // row_hi, col 2 quad + 1
+            mx0 = fmaxf(mx0, fmaxf(x[t][0], x[t][2]));
+            mx1 = fmaxf(mx1, fmaxf(x[t][1], x[t][3]));
+        }
+#pragma unroll
+        for (int o = 4; o < 32; o <<= 1) {
+            mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
+            mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
+        }
+        const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+        const float ms0 = mn0 == -INFINITY ? 0.f : mn0, ms1 = mn1 == -INFINITY ? 0.f : mn1;
+        const float al0 = fast_exp2(m0 - ms0), al1 = fast_exp2(m1 - ms1);
+        m0 = mn0;
+        m1 = mn1;
+        float pr[NT][4];
+        float ls0 = 0.f, ls1 = 0.f;
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+            pr[t][0] = fast_exp2(x[t][0] - ms0);
+            pr[t][1] = fast_exp2(x[t][1] - ms1);
+            pr[t][2] = fast_exp2(x[t][2] - ms0);
+            pr[t][3] = fast_exp2(x[t][3] - ms1);
+            ls0 += pr[t][0] + pr[t][2];
+            ls1 += pr[t][1] + pr[t][3];
+        }
+        l0 = l0 * al0 + ls0;
+        l1 = l1 * al1 + ls1;
+        if (__any_sync(0xffffffffu, al0 != 1.f || al1 != 1.f)) {   // running max moved somewhere
+#pragma unroll
+            for (int mt = 0; mt < 8; ++mt) {
+                oacc[mt][0] *= al0;
+                oacc[mt][1] *= al1;
+                oacc[mt][2] *= al0;
+                oacc[mt][3] *= al1;
+            }
+        }
+        // P^T B-fragments via movmatrix.trans (hardware RNE packs), then O^T += V^T . P^T
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+            const uint32_t hlo = cvt_bf16x2(pr[t][0], pr[t][1]), hhi = cvt_bf16x2(pr[t][2], pr[t][3]);
+            const uint32_t llo = cvt_bf16x2(pr[t][0] - bf16_lo(hlo), pr[t][1] - bf16_hi(hlo));
+            const uint32_t lhi = cvt_bf16x2(pr[t][2] - bf16_lo(hhi), pr[t][3] - bf16_hi(hhi));
+            if (packed) {
+                const uint32_t b0 = movmatrix_t(lo_lane ? llo : hlo), b1 = movmatrix_t(lo_lane ? lhi : hhi);
+#pragma unroll
+                for (int mt = 0; mt < 8; ++mt) {
+                    uint32_t a0, a1, a2, a3;
+                    const uint32_t c = (uint32_t)(2 * mt + vchunk_hi);
+                    ldsm_x4_t(sb[t] + voff + ((c ^ vswz) << 4), a0, a1, a2, a3);
+                    if (!(wk.xflags & 2)) mma_bf16_16816(oacc[mt], a0, a1, a2, a3, b0, b1);
+                    else oacc[mt][0] += __uint_as_float(a0 ^ a3 ^ b0);
+                }
+            } else {
+                const uint32_t bh0 = movmatrix_t(hlo), bh1 = movmatrix_t(hhi);
+                const uint32_t bl0 = movmatrix_t(llo), bl1 = movmatrix_t(lhi);
+#pragma unroll
+                for (int mt = 0; mt < 8; ++mt) {
+                    uint32_t a0, a1, a2, a3;
+                    const uint32_t c = (uint32_t)(2 * mt + vchunk_hi);
+                    ldsm_x4_t(sb[t] + voff + ((c ^ vswz) << 4), a0, a1, a2, a3);
+                    mma_bf16_16816(oacc[mt], a0, a1, a2, a3, bh0, bh1);
+                    mma_bf16_16816(oacc[mt], a0, a1, a2, a3, bl0, bl1);
+                }
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+            if (ik < nt) {                                  // refill the stages just consumed
+                if ((ik & (CT - 1)) == 0) load_chunk(ik >> logCT);
+                fence_proxy_async();
+                issue();
+            }
+        }
+    };
+
+    int k = 0;
+    while (k < nt) {
         if (seg_left == 0) {                                // new segment piece
             if (cs >= 0) flush();
             cs = cs < 0 ? s_first : cs + 1;
@@ -300,93 +450,21 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_kernel(StepParams p, Att
             m0 = m1 = -INFINITY;
             l0 = l1 = 0.f;
         }
-        --seg_left;
-        // token validity of this lane's two rows
-        const int2* ent = &s_ent[warp][(k >> logCT) & 1][(k & (CT - 1)) << logE];
-        const int2 elo = ent[row_lo >> logP], ehi = ent[row_hi >> logP];
-        const bool vlo = elo.x >= 0 && (elo.x << logP) + (row_lo & pm) < n_cur;
-        const bool vhi = ehi.x >= 0 && (ehi.x << logP) + (row_hi & pm) < n_cur;
-        mbar_wait(&my_bar[st], ph);
-        const uint32_t sbase = smem_u32(my_stage + (size_t)st * kTileBytes);
-
-        // S^T = K . Q^T as two independent accumulation chains (even / odd 16-dim slices)
-        float sacc[4] = {0.f, 0.f, 0.f, 0.f}, sacc2[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-        for (int kk = 0; kk < 8; kk += 2) {
-            uint32_t a0, a1, a2, a3, b0, b1, b2, b3;
-            const uint32_t c = (uint32_t)(2 * kk + kchunk_hi), c2 = c + 2;
-            ldsm_x4(sbase + koff + ((c ^ kswz) << 4), a0, a1, a2, a3);
-            ldsm_x4(sbase + koff + ((c2 ^ kswz) << 4), b0, b1, b2, b3);
-            mma_bf16_16816(sacc, a0, a1, a2, a3, qf[kk][0], qf[kk][1]);
-            mma_bf16_16816(sacc2, b0, b1, b2, b3, qf[kk + 1][0], qf[kk + 1][1]);
-        }
-#pragma unroll
-        for (int i = 0; i < 4; ++i) sacc[i] += sacc2[i];
-        // online softmax (log2 domain)
-        const float x0 = vlo ? sacc[0] * p.scale_log2 : -INFINITY;   // row_lo, col 2 quad
-        const float x1 = vlo ? sacc[1] * p.scale_log2 : -INFINITY;   // row_lo, col 2 quad + 1
-        const float x2 = vhi ? sacc[2] * p.scale_log2 : -INFINITY;   // row_hi, col 2 quad
-        const float x3 = vhi ? sacc[3] * p.scale_log2 : -INFINITY;   // row_hi, col 2 quad + 1
-        float mx0 = fmaxf(x0, x2), mx1 = fmaxf(x1, x3);
-#pragma unroll
-        for (int o = 4; o < 32; o <<= 1) {
-            mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
-            mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
-        }
-        const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
-        const float ms0 = mn0 == -INFINITY ? 0.f : mn0, ms1 = mn1 == -INFINITY ? 0.f : mn1;
-        const float al0 = fast_exp2(m0 - ms0), al1 = fast_exp2(m1 - ms1);
-        const float p0 = fast_exp2(x0 - ms0), p1 = fast_exp2(x1 - ms1);
-        const float p2 = fast_exp2(x2 - ms0), p3 = fast_exp2(x3 - ms1);
-        m0 = mn0;
-        m1 = mn1;
-        l0 = l0 * al0 + (p0 + p2);
-        l1 = l1 * al1 + (p1 + p3);
-        if (__any_sync(0xffffffffu, al0 != 1.f || al1 != 1.f)) {   // running max moved somewhere
-#pragma unroll
-            for (int mt = 0; mt < 8; ++mt) {
-                oacc[mt][0] *= al0;
-                oacc[mt][1] *= al1;
-                oacc[mt][2] *= al0;
-                oacc[mt][3] *= al1;
-            }
-        }
-        // P^T B-fragments via movmatrix.trans (hardware RNE packs)
-        const uint32_t hlo = cvt_bf16x2(p0, p1), hhi = cvt_bf16x2(p2, p3);
-        const uint32_t llo = cvt_bf16x2(p0 - bf16_lo(hlo), p1 - bf16_hi(hlo));
-        const uint32_t lhi = cvt_bf16x2(p2 - bf16_lo(hhi), p3 - bf16_hi(hhi));
-        if (packed) {
-            const uint32_t b0 = movmatrix_t(lo_lane ? llo : hlo), b1 = movmatrix_t(lo_lane ? lhi : hhi);
-#pragma unroll
-            for (int mt = 0; mt < 8; ++mt) {
-                uint32_t a0, a1, a2, a3;
-                const uint32_t c = (uint32_t)(2 * mt + vchunk_hi);
-                ldsm_x4_t(sbase + voff + ((c ^ vswz) << 4), a0, a1, a2, a3);
-                mma_bf16_16816(oacc[mt], a0, a1, a2, a3, b0, b1);
-            }
+        const int left = min(seg_left, nt - k);
+        if (left >= 2) {
+            step(std::integral_constant<int, 2>{}, k);
+            k += 2;
+            seg_left -= 2;
         } else {
-            const uint32_t bh0 = movmatrix_t(hlo), bh1 = movmatrix_t(hhi);
-            const uint32_t bl0 = movmatrix_t(llo), bl1 = movmatrix_t(lhi);
-#pragma unroll
-            for (int mt = 0; mt < 8; ++mt) {
-                uint32_t a0, a1, a2, a3;
-                const uint32_t c = (uint32_t)(2 * mt + vchunk_hi);
-                ldsm_x4_t(sbase + voff + ((c ^ vswz) << 4), a0, a1, a2, a3);
-                mma_bf16_16816(oacc[mt], a0, a1, a2, a3, bh0, bh1);
-                mma_bf16_16816(oacc[mt], a0, a1, a2, a3, bl0, bl1);
-            }
+            step(std::integral_constant<int, 1>{}, k);
+            k += 1;
+            seg_left -= 1;
         }
-        __syncwarp();
-        if (ik < nt) {                                      // refill the stage just consumed
-            if ((ik & (CT - 1)) == 0) load_chunk(ik >> logCT);
-            fence_proxy_async();
-            issue();
-        }
-        st = st + 1 == STAGES ? 0 : st + 1;
-        ph ^= st == 0 ? 1u : 0u;
     }
+    ATTN_STAMP(3);
     griddep_launch();
     flush();
+    ATTN_STAMP(6);
 }
 
 template <int STAGES>
@@ -414,11 +492,41 @@ static cudaError_t launch_attn_s(kvd_cache* c, const StepParams& p, const uint16
     nw = std::min(nw, S * (kMaxPieces - 1));
     nw = std::min(nw, wk.T);
     wk.NW = std::max(nw, 1);
+    static int xflags = -1;
+    if (xflags < 0) {
+        const char* env = getenv("KVD_ATTN_X");
+        xflags = env ? atoi(env) : 0;
+    }
+    wk.xflags = xflags;
+    static int trace = -1;
+    static unsigned long long* tbuf = nullptr;
+    if (trace < 0) {
+        trace = getenv("KVD_ATTN_TRACE") ? 1 : 0;
+        if (trace) cudaMalloc(&tbuf, sizeof(unsigned long long) * 8 * 8192);
+    }
+    wk.trace = trace ? tbuf : nullptr;
+    if (trace) cudaMemsetAsync(tbuf, 0, sizeof(unsigned long long) * 8 * 8192, s);
     AttnBufs ab{c->slots, c->ntok_dev, c->zero_rec, c->part_o, c->part_ml, c->split_ctr};
     const unsigned grid = (unsigned)((wk.NW + kAttnWarps - 1) / kAttnWarps);
     cudaError_t e = launch_pdl(attn_kernel<STAGES>, dim3(grid), dim3(kAttnThreads), smem, s, p, ab, wk, q, attn, out,
                                out_lse);
     if (e != cudaSuccess) return e;
+    if (trace) {   // experiments only: synchronous dump of per-warp phase times (us from first stamp)
+        cudaStreamSynchronize(s);
+        std::vector<unsigned long long> h((size_t)wk.NW * 8);
+        cudaMemcpy(h.data(), tbuf, h.size() * 8, cudaMemcpyDeviceToHost);
+        unsigned long long t0 = ~0ull;
+        for (int i = 0; i < wk.NW; ++i) if (h[i * 8] && h[i * 8] < t0) t0 = h[i * 8];
+        const char* names[7] = {"entry", "griddep", "tile0", "stream_end", "merge_begin", "merge_end", "exit"};
+        for (int j = 0; j < 7; ++j) {
+            std::vector<double> v;
+            for (int i = 0; i < wk.NW; ++i) if (h[i * 8 + j]) v.push_back((h[i * 8 + j] - t0) * 1e-3);
+            if (v.empty()) continue;
+            std::sort(v.begin(), v.end());
+            fprintf(stderr, "attn trace %-12s n=%5zu min %7.2f p50 %7.2f p90 %7.2f max %7.2f us\n", names[j], v.size(), v[0],
+                    v[v.size() / 2], v[v.size() * 9 / 10], v.back());
+        }
+    }
     return cudaGetLastError();
 }
 

@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(kResolveThreads) resolve_kernel(StepParams p, 
 }
 
 // (a4) grid-stride over (request, head, miss index); one warp per 8 KiB record.
-constexpr int kGatherThreads = 256;
+constexpr int kGatherThreads = 128;
 __global__ void __launch_bounds__(kGatherThreads) gather_kernel(StepParams p, const int32_t* __restrict__ miss,
                                                                 const int32_t* __restrict__ miss_count, int kmax,
                                                                 const uint8_t* __restrict__ host_store,
@@ -308,7 +308,13 @@ cudaError_t launch_resolve(kvd_cache* c, const StepParams& p, const int32_t* ids
     cudaError_t e = launch_pdl(resolve_kernel, dim3(p.Hkv, p.B), dim3(kResolveThreads), smem, s, p, rb, ids, out_attn);
     if (e != cudaSuccess) return e;
     if (!c->resident) {
-        e = launch_pdl(gather_kernel, dim3(148), dim3(kGatherThreads), 0, s, p, (const int32_t*)c->miss,
+        static int prio = 1;
+        if (prio == 1) {
+            int lo = 0, hi = 0;
+            cudaDeviceGetStreamPriorityRange(&lo, &hi);
+            prio = hi;                                   // greatest priority (numerically lowest)
+        }
+        e = launch_pdl_prio(prio, gather_kernel, dim3(148), dim3(kGatherThreads), 0, s, p, (const int32_t*)c->miss,
                        (const int32_t*)c->miss_count, (int)c->kmax, (const uint8_t*)c->host_store, c->slots);
         if (e != cudaSuccess) return e;
     }

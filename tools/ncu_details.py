@@ -59,3 +59,30 @@ if __name__ == "__main__":
     for k in sys.argv[2:]:
         stalls(rep, k)
         hot(rep, k)
+
+
+def by_line(rep, kernel, n=30):
+    """Stall samples and executed instructions aggregated per CUDA source line."""
+    txt = ncu(rep, "--page", "source", "--csv", "-k", kernel, "--print-source", "cuda,sass")
+    rows = list(csv.reader(io.StringIO(txt)))
+    out, fname, hdr = [], None, None
+    for r in rows:
+        if len(r) == 2 and r[0] == "File Path":
+            fname = r[1].split("/")[-1]
+            continue
+        if r and r[0] == "Line No":
+            hdr = r
+            continue
+        if hdr and fname and len(r) == len(hdr) and r[0].isdigit():
+            si = hdr.index("Warp Stall Sampling (All Samples)")
+            ei = hdr.index("Instructions Executed")
+            try:
+                s_, e_ = float(r[si] or 0), float(r[ei] or 0)
+            except ValueError:
+                continue
+            if s_ or e_:
+                out.append((s_, e_, fname, int(r[0]), r[1].strip()[:90]))
+    tot = sum(x[0] for x in out) or 1
+    print(f"-- {kernel}: stall samples by source line (top {n})")
+    for s_, e_, f, ln, src in sorted(out, reverse=True)[:n]:
+        print(f"   {s_ / tot:6.3f} {e_:10.0f}  {f}:{ln}  {src}")
