@@ -52,7 +52,7 @@ RECORD = 8192           # bytes of one 16-token K||V block record (bf16)
 SUMMARY = 256           # bytes of one block summary (128 bf16)
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
@@ -72,7 +72,7 @@ def parse():
                          "each run through all layers on its own stream inside the graph")
     ap.add_argument("--layers", type=int, default=None, help="override L (profiling only; not a bench number)")
     ap.add_argument("--cpu-sample-s", type=float, default=12.0, help="target seconds of oracle work")
-    return ap.parse_args()
+    return ap.parse_args(argv)
 
 
 def dist_env():
@@ -154,7 +154,9 @@ class Runner:
         self.A = A if (A and A < L) else L
         self.resident = C >= nb
         self.reqs = list(range(B))
-        self.greqs = [rank * B + r for r in range(B)]          # synthetic identity of this rank's requests
+        from paper_2605_18071_b200.dist import rank_requests
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.greqs = rank_requests(rank, world, B)              # synthetic identity of this rank's requests
         self.cache = KVCache(num_layers=L, num_q_heads=Hq, num_kv_heads=Hkv, block_tokens=P, max_requests=B,
                              max_context=n, slots_per_segment=C, max_select=k, sink_tokens=4, local_tokens=64,
                              policy=args.policy, host_layer_alias=(0 if self.A == L else self.A), device=dev.index)
@@ -229,6 +231,13 @@ class Runner:
                 s.wait_stream(cs)
         self.graph = g
 
+    def prepare_graph(self, s):
+        """Capture the step graph; the device step counter continues from the eager steps."""
+        torch = self.torch
+        self.step_dev.fill_(self.t)
+        torch.cuda.synchronize(self.dev)
+        self.capture(s)
+
     def graph_step(self, s, source="dev"):
         torch = self.torch
         with torch.cuda.stream(s):
@@ -265,19 +274,13 @@ def run_gpu(args):
             dist.barrier()
         torch.cuda.synchronize(dev)
 
+    from paper_2605_18071_b200 import dist as kdist
+
     def max_over_ranks(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return kdist.max_over_ranks(x, dev)
 
     def sum_over_ranks(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        return float(t.item())
+        return kdist.sum_over_ranks(x, dev)
 
     R = Runner(args, cfg, rank, dev)
     s = torch.cuda.Stream(device=dev)
@@ -288,10 +291,8 @@ def run_gpu(args):
         R.eager_step(s)
     s.synchronize()
     # capture one step as a CUDA graph (the step index is read on the device)
-    R.step_dev.fill_(R.t)
-    torch.cuda.synchronize(dev)
     if not args.no_graph:
-        R.capture(s)
+        R.prepare_graph(s)
     run = (lambda: R.eager_step(s)) if args.no_graph else (lambda: R.graph_step(s))
     clk = ClockSampler(local)          # sampled from warm-up through the e2e pass (GPU busy throughout)
     clk.start()
