@@ -128,6 +128,16 @@ __device__ __forceinline__ float fast_exp2(float x) {
     return y;
 }
 
+// 16-byte streaming load from host-mapped memory: no L1 allocation, 256-byte L2
+// fetch granularity (fewer, larger host-link read requests for a warp's 512 B).
+__device__ __forceinline__ int4 ld_host16(const void* p) {
+    int4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.s32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
 // 16-byte streaming load that does not allocate in L1 (host-mapped or HBM).
 __device__ __forceinline__ int4 ld_stream16(const void* p) {
     int4 r;

@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(kGatherThreads) gather_kernel(StepParams p, co
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 const int c = c0 + u * 32 + lane;
-                if (c < chunks) v[u] = ld_stream16(src + c);
+                if (c < chunks) v[u] = ld_host16(src + c);
             }
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
