@@ -70,6 +70,10 @@ def parse(argv=None):
     ap.add_argument("--chains", type=int, default=None,
                     help="micro-batch chains (SFC overlap): the batch is split into this many request groups, "
                          "each run through all layers on its own stream inside the graph")
+    ap.add_argument("--shard", default="requests", choices=["requests", "heads"],
+                    help="multi-GPU unit assignment: 'requests' = every rank serves its own B requests (weak "
+                         "scaling, no collective); 'heads' = the config's B*Hkv units are partitioned over the "
+                         "ranks (strong scaling; SURVEY 8.6) and the fp32 outputs are all-gathered each step")
     ap.add_argument("--layers", type=int, default=None, help="override L (profiling only; not a bench number)")
     ap.add_argument("--cpu-sample-s", type=float, default=12.0, help="target seconds of oracle work")
     return ap.parse_args(argv)
@@ -147,16 +151,27 @@ class Runner:
         from paper_2605_18071_b200 import KVCache
         self.torch, self.args, self.cfg, self.rank, self.dev = torch, args, cfg, rank, dev
         L, B, Hq, Hkv, n, P, k = (cfg[x] for x in ("L", "B", "Hq", "Hkv", "n", "P", "k"))
-        self.G = Hq // Hkv
+        self.G = G = Hq // Hkv
         nb = (n + P - 1) // P
         C = cfg["C"] if cfg["C"] is not None else nb
         A = args.alias if args.alias is not None else cfg["alias"]
         self.A = A if (A and A < L) else L
         self.resident = C >= nb
-        self.reqs = list(range(B))
-        from paper_2605_18071_b200.dist import rank_requests
+        from paper_2605_18071_b200 import dist as kdist
         world = int(os.environ.get("WORLD_SIZE", "1"))
-        self.greqs = rank_requests(rank, world, B)              # synthetic identity of this rank's requests
+        self.mode = getattr(args, "shard", "requests")
+        self.h0 = 0
+        if self.mode == "heads":
+            # strong scaling: this rank owns heads h0..h1-1 of some of the config's B requests
+            self.all_parts = kdist.unit_partition(B, Hkv, world)
+            self.greqs, self.h0, h1 = kdist.rank_heads(self.all_parts[rank])
+            Hkv = h1 - self.h0
+            Hq = Hkv * G
+            B = len(self.greqs)
+        else:
+            self.greqs = kdist.rank_requests(rank, world, B)   # synthetic identity of this rank's requests
+        self.B, self.Hkv, self.Hq = B, Hkv, Hq                  # this rank's (local) shapes
+        self.reqs = list(range(B))
         self.cache = KVCache(num_layers=L, num_q_heads=Hq, num_kv_heads=Hkv, block_tokens=P, max_requests=B,
                              max_context=n, slots_per_segment=C, max_select=k, sink_tokens=4, local_tokens=64,
                              policy=args.policy, host_layer_alias=(0 if self.A == L else self.A), device=dev.index)
@@ -166,7 +181,7 @@ class Runner:
         Vd = torch.empty_like(Kd)
         for sl in range(self.A):
             for r, gr in zip(self.reqs, self.greqs):
-                synth.request_kv_device(args.seed, sl, gr, Hkv, n, Kd, Vd)
+                synth.request_kv_device(args.seed, sl, gr, Hkv, n, Kd, Vd, head0=self.h0)
                 for l in range(sl, L, self.A):
                     self.cache.load_prefix(l, r, Kd, Vd, n)
         del Kd, Vd
@@ -175,7 +190,9 @@ class Runner:
         # queries for every step of the run, per synthetic layer: [T][L][B][Hq][128]
         self.fill = max(1, args.fill if args.fill is not None else (1 if self.resident else max(4, 2 * C // k)))
         self.T = self.fill + args.warmup + 3 * args.steps + 2
-        qs = [synth.batch_queries(args.seed, sl, self.greqs, Hkv, self.G, t0=0, nsteps=self.T, alpha=args.alpha)
+        Hkv_all = cfg["Hkv"]
+        qs = [synth.batch_queries(args.seed, sl, self.greqs, Hkv_all, G, t0=0, nsteps=self.T,
+                                  alpha=args.alpha)[:, :, self.h0 * G:(self.h0 + Hkv) * G]
               for sl in range(self.A)]
         qh = np.stack([qs[l % self.A] for l in range(L)], axis=1)        # [T][L][B][Hq][128]
         self.q_host = torch.from_numpy(qh.view(np.int16)).pin_memory()
@@ -284,8 +301,17 @@ def run_gpu(args):
 
     R = Runner(args, cfg, rank, dev)
     s = torch.cuda.Stream(device=dev)
-    L, B, Hkv = cfg["L"], cfg["B"], cfg["Hkv"]
+    L, B, Hkv = cfg["L"], R.B, R.Hkv                          # this rank's shapes
     segs_per_layer = B * Hkv
+    heads_mode = R.mode == "heads" and world > 1
+    # all_gather_into_tensor output: per-rank outputs concatenated along dim 0 ([world*L][B_r][Hq_r][128])
+    gathered = (torch.empty((world * R.out.shape[0],) + tuple(R.out.shape[1:]), dtype=R.out.dtype, device=dev)
+                if heads_mode else None)
+
+    def gather_outputs():
+        # head sharding: the step's per-rank fp32 outputs -> every rank (NCCL over NVLink)
+        with torch.cuda.stream(s):
+            dist.all_gather_into_tensor(gathered, R.out)
     # cache fill (cold start -> steady state; untimed, parity-checked in tests)
     for _ in range(R.fill):
         R.eager_step(s)
@@ -293,7 +319,12 @@ def run_gpu(args):
     # capture one step as a CUDA graph (the step index is read on the device)
     if not args.no_graph:
         R.prepare_graph(s)
-    run = (lambda: R.eager_step(s)) if args.no_graph else (lambda: R.graph_step(s))
+    step_fn = (lambda: R.eager_step(s)) if args.no_graph else (lambda: R.graph_step(s))
+
+    def run():
+        step_fn()
+        if heads_mode:
+            gather_outputs()
     clk = ClockSampler(local)          # sampled from warm-up through the e2e pass (GPU busy throughout)
     clk.start()
     for _ in range(args.warmup):
@@ -312,7 +343,9 @@ def run_gpu(args):
     ms = ev0.elapsed_time(ev1) / args.steps
     st = R.cache.stats()
     ms_max = max_over_ranks(ms)
-    tokens = sum_over_ranks(B * args.steps)
+    # whole-job tokens: requests mode sums every rank's requests; heads mode counts each
+    # of the config's requests once (its heads are spread over the ranks)
+    tokens = cfg["B"] * args.steps if heads_mode else sum_over_ranks(B * args.steps)
     value = tokens / (ms_max * args.steps * 1e-3)
     hit_rate = st["hits"] / max(1, st["selected"])
     misses_per_seg = st["misses"] / max(1, args.steps * L * segs_per_layer)
@@ -392,6 +425,8 @@ def run_gpu(args):
         e0.record(s)
         for _ in range(args.steps):
             R.graph_step(s, source="host")
+            if heads_mode:
+                gather_outputs()
         e1.record(s)
         e1.synchronize()
         barrier()
@@ -403,13 +438,14 @@ def run_gpu(args):
 
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
+        "scaling": "strong" if heads_mode else "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded; DESIGN.md §4)",
-        "config": {"workload": args.config, "desc": cfg["desc"], "global_batch": B * world, "seq_len": cfg["n"],
-                   "layers": L, "q_heads": cfg["Hq"], "kv_heads": Hkv, "block_tokens": cfg["P"],
+        "config": {"workload": args.config, "desc": cfg["desc"], "global_batch": cfg["B"] if heads_mode else B * world, "seq_len": cfg["n"],
+                   "layers": L, "q_heads": cfg["Hq"], "kv_heads": cfg["Hkv"], "block_tokens": cfg["P"],
                    "top_k_blocks": cfg["k"], "slots_per_segment": cfg["C"] or (cfg["n"] // cfg["P"]),
                    "policy": args.policy, "alpha": args.alpha, "host_layer_alias": R.A if not R.resident else None,
-                   "fill_steps": R.fill, "graph": not args.no_graph, "chains": len(R.chains), "parallelism": f"request-shard x{world}",
+                   "fill_steps": R.fill, "graph": not args.no_graph, "chains": len(R.chains), "parallelism": (f"head-shard x{world} + NCCL all-gather" if heads_mode else f"request-shard x{world}"),
                    "l2": "inputs larger than L2 (no flush)"},
         "hit_rate": hit_rate, "misses_per_segment": misses_per_seg,
         "roofline": roof, "roofline_attn": roof_attn, "kernels": kernels,

@@ -24,6 +24,7 @@ constexpr int kAttnWarps = 4;         // warps per attention CTA
 constexpr int kAttnStages = 3;        // smem stages per warp
 constexpr int kTileBytes = 8192;      // one 16-token K||V tile
 constexpr int kSplitTiles = 16;       // (legacy split size; StepParams.nsplit)
+constexpr int kMaxSelTiles = 128;     // select tiles per segment (k_select.cu s_off)
 constexpr int kMaxPieces = 32;        // attention partials per (request, KV head) (k_attn.cu)
 constexpr int64_t kSlotOfBytes = 64ll << 20;   // setup scratch for per-block slot targets
 
@@ -70,6 +71,10 @@ struct kvd_cache {
     float* part_ml = nullptr;
     uint32_t* split_ctr = nullptr;
     uint32_t* sel_ctr = nullptr;           // [R][Hkv] select arrival counters
+    uint32_t* cand_key = nullptr;          // [R][Hkv][max_sel_tiles][kmax] tile-local top-k keys
+    int32_t* cand_id = nullptr;            // [R][Hkv][max_sel_tiles][kmax] their block ids
+    int32_t* cand_cnt = nullptr;           // [R][Hkv][max_sel_tiles]
+    int32_t max_sel_tiles = 0;             // ceil(nb_pad / 512): tiles of the narrowest select CTA
     unsigned long long* stats = nullptr;   // [5] kvd_stats fields
     int32_t* err = nullptr;
     int32_t* ntok_dev = nullptr;

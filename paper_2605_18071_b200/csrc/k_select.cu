@@ -22,12 +22,15 @@
 // among the candidates; keys > T are taken and the kk lowest-id keys == T
 // (R10).  Two block scans give tie ranks and output positions, so ids come out
 // ascending with no sort.
+#include <algorithm>
+
 #include "common.cuh"
 #include "internal.h"
 
 namespace kvd {
 
 constexpr int kScoreThreads = 256;
+constexpr int64_t kDirectTopkMax = 16384;     // segments up to this many blocks: direct top-k
 
 template <int V>
 struct VecOf;
@@ -52,7 +55,7 @@ struct VecOf<8> {
 template <int V>
 __device__ __forceinline__ void score_tile(const StepParams& p, int bi, int h, int64_t nb, int64_t seg,
                                            const uint16_t* __restrict__ q, const uint16_t* __restrict__ summ,
-                                           float* __restrict__ scores, float* qbar) {
+                                           float* __restrict__ scores, float* qbar, float (&acc)[V]) {
     using Vec = typename VecOf<V>::T;
     const int64_t b0 = (int64_t)blockIdx.x * kScoreThreads * V + (int64_t)threadIdx.x * V;
     const bool ld = b0 < nb;                      // V-groups never straddle nb_pad (V | 128)
@@ -77,7 +80,6 @@ __device__ __forceinline__ void score_tile(const StepParams& p, int bi, int h, i
         qbar[threadIdx.x] = a;
     }
     __syncthreads();
-    float acc[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) acc[v] = 0.0f;
     auto consume = [&](const Vec (&buf)[R], int j0) {
@@ -124,36 +126,21 @@ struct TopkSmem {
     int above;
 };
 
-// Top-k of one segment by the whole CTA (kScoreThreads threads).
-template <int KPT>
-__device__ void topk_segment(const StepParams& p, const SegGeom& g, const float* __restrict__ sc, int reps,
-                             int32_t* __restrict__ ids_out, float* __restrict__ sc_out, TopkSmem& sm) {
+// CTA-wide top-k (blockDim.x threads, all call it).  Thread t owns `reps` chunks of KPT
+// consecutive positions; positions ascend with (t, chunk, i), so emission order is
+// ascending position.  load(c, key[KPT], &cm) fills chunk c's monotone keys and
+// candidate mask; emit(pos, c, i) writes output slot pos for element (c, i) of this
+// thread.  Selects the k largest keys among candidates, ties to the lowest position
+// (R10); k must not exceed the candidate count.  3-pass radix select (11 + 11 + 10
+// bits) with warp-aggregated shared histograms, then two block scans.
+template <int KPT, class Load, class Emit>
+__device__ void cta_topk(int k, int reps, Load load, Emit emit, TopkSmem& sm) {
     const int tid = threadIdx.x, nthr = blockDim.x;
     uint32_t key[KPT];
-    uint32_t cm = 0;                              // candidate mask of the chunk in registers
-    auto load = [&](int c) {
-        const int64_t b0 = ((int64_t)tid * reps + c) * KPT;
-        cm = 0;
-        if (b0 >= g.nb) return;
-        float f[KPT];
-#pragma unroll
-        for (int i = 0; i < KPT; i += 4) {
-            const float4 x = __ldcg(reinterpret_cast<const float4*>(sc + b0 + i));
-            f[i] = x.x; f[i + 1] = x.y; f[i + 2] = x.z; f[i + 3] = x.w;
-        }
-#pragma unroll
-        for (int i = 0; i < KPT; ++i) {
-            const int64_t b = b0 + i;
-            const bool cand = b < g.nb && b >= g.sink_end && b < g.local_begin;
-            key[i] = score_key32(f[i]);
-            cm |= (uint32_t)cand << i;
-        }
-    };
-    if (reps == 1) load(0);
-
-    // ---- radix select over candidates: T = k-th largest key (3 passes)
+    uint32_t cm = 0;
+    if (reps == 1) load(0, key, cm);
     uint32_t prefix = 0, mask = 0;
-    int kk = p.k;
+    int kk = k;
 #pragma unroll 1
     for (int pass = 0; pass < 3; ++pass) {
         const int shift = pass == 0 ? 21 : pass == 1 ? 10 : 0;
@@ -162,7 +149,7 @@ __device__ void topk_segment(const StepParams& p, const SegGeom& g, const float*
         __syncthreads();
 #pragma unroll 1
         for (int c = 0; c < reps; ++c) {
-            if (reps > 1) load(c);
+            if (reps > 1) load(c, key, cm);
 #pragma unroll
             for (int i = 0; i < KPT; ++i) {
                 const bool act = ((cm >> i) & 1u) && (key[i] & mask) == prefix;
@@ -171,7 +158,7 @@ __device__ void topk_segment(const StepParams& p, const SegGeom& g, const float*
         }
         __syncthreads();
         // bins in descending order; thread t owns bins [nbins - (t+1) bpt, nbins - t bpt)
-        const int bpt = nbins / nthr;             // 8 or 4 (256 threads)
+        const int bpt = nbins / nthr;
         int cnt = 0;
         for (int i = 0; i < bpt; ++i) cnt += sm.hist[nbins - 1 - (tid * bpt + i)];
         int tot;
@@ -194,13 +181,11 @@ __device__ void topk_segment(const StepParams& p, const SegGeom& g, const float*
         kk -= sm.above;
         __syncthreads();
     }
-    const uint32_t T = prefix;                    // take keys > T, and the kk lowest-id keys == T
-
-    // ---- tie ranks and output positions (thread-contiguous ownership => ascending ids)
+    const uint32_t T = prefix;                    // take keys > T, and the kk lowest-position keys == T
     int ngt = 0, neq = 0;
 #pragma unroll 1
     for (int c = 0; c < reps; ++c) {
-        if (reps > 1) load(c);
+        if (reps > 1) load(c, key, cm);
 #pragma unroll
         for (int i = 0; i < KPT; ++i) {
             const bool cand = (cm >> i) & 1u;
@@ -211,93 +196,236 @@ __device__ void topk_segment(const StepParams& p, const SegGeom& g, const float*
     int tot;
     const int tie0 = block_exclusive_scan(neq, sm.scan, &tot);
     const int ntake = min(max(kk - tie0, 0), neq);
-    const int pos0 = block_exclusive_scan(ngt + ntake, sm.scan, &tot);
-    int pos = pos0, tie = tie0;
+    int pos = block_exclusive_scan(ngt + ntake, sm.scan, &tot);
+    int tie = tie0;
 #pragma unroll 1
     for (int c = 0; c < reps; ++c) {
-        if (reps > 1) load(c);
-        const int64_t b0 = ((int64_t)tid * reps + c) * KPT;
+        if (reps > 1) load(c, key, cm);
 #pragma unroll
         for (int i = 0; i < KPT; ++i) {
             if (!((cm >> i) & 1u)) continue;
             bool take = key[i] > T;
             if (key[i] == T) take = tie++ < kk;
-            if (take) {
-                ids_out[pos] = (int32_t)(b0 + i);
-                if (sc_out) sc_out[pos] = sc[b0 + i];
-                ++pos;
-            }
+            if (take) emit(pos++, c, i);
         }
     }
 }
 
+// Two-level top-k (a2).  Every scoring CTA first keeps its tile's local top-k
+// candidates (the k largest (key, -id) pairs of its V*256 blocks, or all of them):
+// the segment's top-k is a subset of the union of the tiles' local top-k, so the
+// final selection only ranks ntiles*k candidates.  Candidates are stored per tile
+// in ascending id order, so the concatenation over tiles is ascending too.  The
+// last CTA of the segment to finish (arrival counter) runs the final selection.
+struct SelBufs {
+    uint32_t* cand_key;     // [R][Hkv][max_tiles][kmax]
+    int32_t* cand_id;       // [R][Hkv][max_tiles][kmax]
+    int32_t* cand_cnt;      // [R][Hkv][max_tiles]
+    uint32_t* ctr;          // [R][Hkv]
+    int32_t max_tiles, kmax;
+};
+
 // grid (tiles per segment, Hkv, B); CTA = kScoreThreads threads scoring kScoreThreads*V blocks.
-template <int V, int KPT>
+// TWO = two-level selection (tile-local candidates first; used when nb > 16384) or the
+// direct selection over all of the segment's scores by the last CTA.
+template <int V, int KPT, bool TWO>
 __global__ void __launch_bounds__(kScoreThreads, 2) select_kernel(StepParams p, const uint16_t* __restrict__ q,
                                                                   const uint16_t* __restrict__ summ,
                                                                   float* __restrict__ scores,
-                                                                  const int32_t* __restrict__ ntok,
-                                                                  uint32_t* __restrict__ sel_ctr, int reps,
-                                                                  int32_t* __restrict__ out_ids,
+                                                                  const int32_t* __restrict__ ntok, SelBufs sb,
+                                                                  int reps, int32_t* __restrict__ out_ids,
                                                                   float* __restrict__ out_scores) {
     __shared__ float qbar[kHeadDim];
     __shared__ TopkSmem sm;
-    __shared__ int s_last;
-    const int bi = blockIdx.z, h = blockIdx.y;
+    __shared__ int s_last, s_off[kMaxSelTiles + 1];
+    const int bi = blockIdx.z, h = blockIdx.y, tile = blockIdx.x;
     const int r = p.req[bi];
     const int n = ntok[r];                        // written only by kvd_load_prefix (setup)
     const int64_t nb = (n + p.P - 1) / p.P;
     const int64_t bpc = (int64_t)kScoreThreads * V;
-    if ((int64_t)blockIdx.x * bpc >= nb) return;  // whole CTA past this request's end (does not arrive)
+    if ((int64_t)tile * bpc >= nb) return;        // whole CTA past this request's end (does not arrive)
     const int64_t seg = ((int64_t)p.layer * p.R + r) * p.Hkv + h;
-    score_tile<V>(p, bi, h, nb, seg, q, summ, scores, qbar);
+    float acc[V];
+    score_tile<V>(p, bi, h, nb, seg, q, summ, scores, qbar, acc);
     if (p.k == 0) return;
-    // ---- the last CTA of the segment to finish runs its top-k
+    const SegGeom g = seg_geom(n, p.P, p.sink_tokens, p.local_tokens);
     const int64_t rs = (int64_t)r * p.Hkv + h;
+    const int64_t b0 = (int64_t)tile * bpc + (int64_t)threadIdx.x * V;
+
+    if (TWO) {
+    // ---- tile-local candidates
+    uint32_t lkey[V];
+    uint32_t lcm = 0;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+        const int64_t b = b0 + v;
+        lkey[v] = score_key32(acc[v]);
+        lcm |= (uint32_t)(b < g.nb && b >= g.sink_end && b < g.local_begin) << v;
+    }
+    int tot;
+    const int cpos = block_exclusive_scan(__popc(lcm), sm.scan, &tot);   // candidates of the tile
+    const int kl = min(p.k, tot);
+    uint32_t* ck = sb.cand_key + (rs * sb.max_tiles + tile) * sb.kmax;
+    int32_t* ci = sb.cand_id + (rs * sb.max_tiles + tile) * sb.kmax;
+    if (tot <= p.k) {                             // every candidate of the tile survives
+        int pos = cpos;
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+            if ((lcm >> v) & 1u) {
+                ck[pos] = lkey[v];
+                ci[pos] = (int32_t)(b0 + v);
+                ++pos;
+            }
+    } else {
+        cta_topk<V>(
+            kl, 1,
+            [&](int, uint32_t (&key)[V], uint32_t& cm) {
+#pragma unroll
+                for (int v = 0; v < V; ++v) key[v] = lkey[v];
+                cm = lcm;
+            },
+            [&](int pos, int, int v) {
+                ck[pos] = lkey[v];
+                ci[pos] = (int32_t)(b0 + v);
+            },
+            sm);
+    }
+    if (threadIdx.x == 0) sb.cand_cnt[rs * sb.max_tiles + tile] = kl;
+    }
+
+    // ---- the last CTA of the segment to finish runs the final selection
     const uint32_t ntiles = (uint32_t)((nb + bpc - 1) / bpc);
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
-        s_last = atomicAdd(&sel_ctr[rs], 1u) == ntiles - 1;
+        s_last = atomicAdd(&sb.ctr[rs], 1u) == ntiles - 1;
         if (s_last) {
-            sel_ctr[rs] = 0u;
+            sb.ctr[rs] = 0u;
             __threadfence();
         }
     }
     __syncthreads();
     if (!s_last) return;
-    const SegGeom g = seg_geom(n, p.P, p.sink_tokens, p.local_tokens);
     int32_t* ids_out = out_ids + ((int64_t)bi * p.Hkv + h) * p.k;
     float* sc_out = out_scores ? out_scores + ((int64_t)bi * p.Hkv + h) * p.k : nullptr;
-    topk_segment<KPT>(p, g, scores + seg * p.nb_pad, reps, ids_out, sc_out, sm);
+    const float* sc = scores + seg * p.nb_pad;
+    if (!TWO) {
+        // direct: thread t owns blocks [t*KPT*reps, (t+1)*KPT*reps), scores re-read from L2
+        cta_topk<KPT>(
+            p.k, reps,
+            [&](int c, uint32_t (&key)[KPT], uint32_t& cm) {
+                const int64_t bb = ((int64_t)threadIdx.x * reps + c) * KPT;
+                cm = 0;
+                if (bb >= g.nb) return;
+#pragma unroll
+                for (int i = 0; i < KPT; i += 4) {
+                    const float4 x = __ldcg(reinterpret_cast<const float4*>(sc + bb + i));
+                    key[i] = score_key32(x.x); key[i + 1] = score_key32(x.y);
+                    key[i + 2] = score_key32(x.z); key[i + 3] = score_key32(x.w);
+                }
+#pragma unroll
+                for (int i = 0; i < KPT; ++i) {
+                    const int64_t b = bb + i;
+                    cm |= (uint32_t)(b < g.nb && b >= g.sink_end && b < g.local_begin) << i;
+                }
+            },
+            [&](int pos, int c, int i) {
+                const int64_t b = ((int64_t)threadIdx.x * reps + c) * KPT + i;
+                ids_out[pos] = (int32_t)b;
+                if (sc_out) sc_out[pos] = __ldcg(&sc[b]);
+            },
+            sm);
+        return;
+    }
+    // candidate offsets per tile (ntiles <= max_tiles <= 128 per pass of this loop)
+    int total = 0;
+    for (int t0 = 0; t0 < (int)ntiles; t0 += kScoreThreads) {
+        const int t = t0 + (int)threadIdx.x;
+        const int c = t < (int)ntiles ? __ldcg(&sb.cand_cnt[rs * sb.max_tiles + t]) : 0;
+        int tt;
+        const int off = block_exclusive_scan(c, sm.scan, &tt);
+        if (t < (int)ntiles) s_off[t] = total + off;
+        total += tt;
+    }
+    if (threadIdx.x == 0) s_off[ntiles] = total;
+    __syncthreads();
+    const int nt_ = (int)ntiles;
+    // candidate j (concatenated, ascending id) -> (tile, index): tiles hold kl_t <= kmax entries
+    auto cand_at = [&](int j, uint32_t& key, int32_t& id) {
+        int lo = 0, hi = nt_;                     // largest t with s_off[t] <= j
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (s_off[mid] <= j) lo = mid; else hi = mid;
+        }
+        const int64_t base = (rs * sb.max_tiles + lo) * sb.kmax + (j - s_off[lo]);
+        key = __ldcg(&sb.cand_key[base]);
+        id = __ldcg(&sb.cand_id[base]);
+    };
+    const int per = (total + kScoreThreads * reps - 1) / (kScoreThreads * reps);   // <= KPT
+    cta_topk<KPT>(
+        p.k, reps,
+        [&](int c, uint32_t (&key)[KPT], uint32_t& cm) {
+            const int j0 = ((int)threadIdx.x * reps + c) * per;
+            cm = 0;
+#pragma unroll
+            for (int i = 0; i < KPT; ++i) {
+                key[i] = 0u;
+                if (i < per && j0 + i < total) {
+                    int32_t id;
+                    cand_at(j0 + i, key[i], id);
+                    cm |= 1u << i;
+                }
+            }
+        },
+        [&](int pos, int c, int i) {
+            const int j = ((int)threadIdx.x * reps + c) * per + i;
+            uint32_t key;
+            int32_t id;
+            cand_at(j, key, id);
+            ids_out[pos] = id;
+            if (sc_out) sc_out[pos] = __ldcg(&sc[id]);
+        },
+        sm);
 }
 
-template <int V, int KPT>
+template <int V, int KPT, bool TWO>
 static cudaError_t launch_sel(kvd_cache* c, const StepParams& p, const uint16_t* q, int reps, int32_t* out_ids,
                               float* out_scores, cudaStream_t s) {
     const unsigned tiles = (unsigned)((c->nb_pad + kScoreThreads * V - 1) / (kScoreThreads * V));
-    return launch_pdl(select_kernel<V, KPT>, dim3(tiles, p.Hkv, p.B), dim3(kScoreThreads), 0, s, p, q,
-                      (const uint16_t*)c->summ, c->scores, (const int32_t*)c->ntok_dev, c->sel_ctr, reps, out_ids,
+    SelBufs sb{c->cand_key, c->cand_id, c->cand_cnt, c->sel_ctr, c->max_sel_tiles, c->kmax > 0 ? c->kmax : 1};
+    return launch_pdl(select_kernel<V, KPT, TWO>, dim3(tiles, p.Hkv, p.B), dim3(kScoreThreads), 0, s, p, q,
+                      (const uint16_t*)c->summ, c->scores, (const int32_t*)c->ntok_dev, sb, reps, out_ids,
                       out_scores);
 }
 
 template <int V>
 static cudaError_t launch_sel_v(kvd_cache* c, const StepParams& p, const uint16_t* q, int32_t* out_ids,
                                 float* out_scores, cudaStream_t s) {
-    const int64_t per = (c->nb_pad + kScoreThreads - 1) / kScoreThreads;   // blocks per top-k thread
-    if (per <= 4) return launch_sel<V, 4>(c, p, q, 1, out_ids, out_scores, s);
-    if (per <= 8) return launch_sel<V, 8>(c, p, q, 1, out_ids, out_scores, s);
-    if (per <= 16) return launch_sel<V, 16>(c, p, q, 1, out_ids, out_scores, s);
-    return launch_sel<V, 32>(c, p, q, (int)((per + 31) / 32), out_ids, out_scores, s);
+    if (c->nb_pad <= kDirectTopkMax) {
+        // direct selection over the segment's nb scores: KPT per thread, keys re-read per chunk
+        const int64_t per = (c->nb_pad + kScoreThreads - 1) / kScoreThreads;
+        if (per <= 4) return launch_sel<V, 4, false>(c, p, q, 1, out_ids, out_scores, s);
+        if (per <= 8) return launch_sel<V, 8, false>(c, p, q, 1, out_ids, out_scores, s);
+        if (per <= 16) return launch_sel<V, 16, false>(c, p, q, 1, out_ids, out_scores, s);
+        return launch_sel<V, 32, false>(c, p, q, (int)((per + 31) / 32), out_ids, out_scores, s);
+    }
+    // two-level: final selection over at most tiles * k candidates
+    const int64_t tiles = (c->nb_pad + kScoreThreads * V - 1) / (kScoreThreads * V);
+    const int64_t cand = std::min<int64_t>(tiles * std::max(p.k, 1), c->nb_pad);
+    const int64_t per = (cand + kScoreThreads - 1) / kScoreThreads;
+    if (per <= 8) return launch_sel<V, 8, true>(c, p, q, 1, out_ids, out_scores, s);
+    if (per <= 16) return launch_sel<V, 16, true>(c, p, q, 1, out_ids, out_scores, s);
+    return launch_sel<V, 16, true>(c, p, q, (int)((per + 15) / 16), out_ids, out_scores, s);
 }
 
 cudaError_t launch_select(kvd_cache* c, const StepParams& p, const uint16_t* q, int32_t* out_ids, float* out_scores,
                           cudaStream_t s) {
-    // V: largest of 8, 4, 2 blocks per thread that still gives >= 2 CTAs per SM
+    // V: largest of 8, 4, 2 blocks per thread that still gives >= 2 CTAs per SM; the
+    // two-level path always takes V = 8 (fewest tiles -> fewest candidates)
     const int64_t segs = (int64_t)p.B * p.Hkv;
     auto ctas = [&](int V) { return segs * ((c->nb_pad + kScoreThreads * V - 1) / (kScoreThreads * V)); };
     cudaError_t e;
-    if (ctas(8) >= 2 * 148) e = launch_sel_v<8>(c, p, q, out_ids, out_scores, s);
+    if (c->nb_pad > kDirectTopkMax || ctas(8) >= 2 * 148) e = launch_sel_v<8>(c, p, q, out_ids, out_scores, s);
     else if (ctas(4) >= 2 * 148) e = launch_sel_v<4>(c, p, q, out_ids, out_scores, s);
     else e = launch_sel_v<2>(c, p, q, out_ids, out_scores, s);
     if (e != cudaSuccess) return e;

@@ -79,12 +79,15 @@ kvd_status check_config(const kvd_config* cfg, Geometry* g) {
     (void)wmax;
     g->max_splits = kMaxPieces;
     if ((int64_t)g->Hkv * g->nb_max * 4 > kSlotOfBytes) return fail(KVD_EINVAL, "context too long for setup scratch");
+    if (g->nb_pad > (int64_t)kMaxSelTiles * 2048) return fail(KVD_EINVAL, "context too long: > %d blocks", kMaxSelTiles * 2048);
     return KVD_OK;
 }
 
 struct Sizes {
-    size_t slots, summ, scores, table, meta4, meta1, miss, part_o, part_ml, small, host;
-    size_t dev_total() const { return slots + summ + scores + table + 3 * meta4 + meta1 + miss + part_o + part_ml + small; }
+    size_t slots, summ, scores, table, meta4, meta1, miss, part_o, part_ml, small, host, cand;
+    size_t dev_total() const {
+        return slots + summ + scores + table + 3 * meta4 + meta1 + miss + part_o + part_ml + small + cand;
+    }
 };
 
 Sizes sizes_of(const Geometry& g) {
@@ -101,6 +104,7 @@ Sizes sizes_of(const Geometry& g) {
     s.part_o = rsegs * g.max_splits * 8 * kHeadDim * 4;
     s.part_ml = rsegs * g.max_splits * 8 * 2 * 4;
     s.small = rsegs * 8 + 64 + 4 + (size_t)g.R * 4 + g.rec_bytes;
+    s.cand = rsegs * (size_t)((g.nb_pad + 511) / 512) * ((size_t)(g.kmax > 0 ? g.kmax : 1) * 8 + 4);
     s.host = g.resident ? 0 : (size_t)g.A * g.R * g.Hkv * g.nb_max * g.rec_bytes;
     return s;
 }
@@ -216,6 +220,10 @@ kvd_status kvd_create_cache(const kvd_config* cfg, kvd_cache** out) {
     ALLOC(part_ml, s.part_ml);
     ALLOC(split_ctr, rsegs * 4);
     ALLOC(sel_ctr, rsegs * 4);
+    c->max_sel_tiles = (int32_t)((g.nb_pad + 511) / 512);
+    ALLOC(cand_key, rsegs * (size_t)c->max_sel_tiles * (g.kmax > 0 ? g.kmax : 1) * 4);
+    ALLOC(cand_id, rsegs * (size_t)c->max_sel_tiles * (g.kmax > 0 ? g.kmax : 1) * 4);
+    ALLOC(cand_cnt, rsegs * (size_t)c->max_sel_tiles * 4);
     ALLOC(stats, 64);
     ALLOC(err, 4);
     ALLOC(ntok_dev, (size_t)g.R * 4);
@@ -250,7 +258,7 @@ void kvd_destroy_cache(kvd_cache* c) {
     cudaSetDevice(c->cfg.device);
     cudaDeviceSynchronize();
     void* dev[] = {c->slots, c->summ, c->scores, c->table, c->slot_block, c->last_use, c->phase,
-                   c->use_count, c->miss, c->miss_count, c->part_o, c->part_ml, c->split_ctr, c->sel_ctr, c->stats,
+                   c->use_count, c->miss, c->miss_count, c->part_o, c->part_ml, c->split_ctr, c->sel_ctr, c->cand_key, c->cand_id, c->cand_cnt, c->stats,
                    c->err, c->ntok_dev, c->zero_rec, c->stage_kv, c->stage_rec};
     for (void* p : dev)
         if (p) cudaFree(p);

@@ -41,6 +41,28 @@ def unit_partition(B, Hkv, world):
     return out
 
 
+def rank_heads(parts):
+    """(requests, head_begin, head_end) of one rank's unit_partition entry; the head
+    range must be the same for every request of the rank (true for c4 and for any
+    partition into whole requests)."""
+    h0, h1 = parts[0][1], parts[0][2]
+    if any((a, b) != (h0, h1) for _, a, b in parts):
+        raise ValueError("ranks must own the same head range of each of their requests")
+    return [req for req, _, _ in parts], h0, h1
+
+
+def assemble_heads(gathered, all_parts, B, Hkv, G):
+    """Per-rank outputs [world][L][B_r][Hq_r][d] (all_gather_into_tensor of each
+    rank's fp32 attention outputs) -> the global [L][B][Hq][d] tensor."""
+    world, L, _, _, d = gathered.shape
+    out = gathered.new_empty((L, B, Hkv * G, d))
+    for r in range(world):
+        reqs, h0, h1 = rank_heads(all_parts[r])
+        for i, req in enumerate(reqs):
+            out[:, req, h0 * G:h1 * G] = gathered[r, :, i, :(h1 - h0) * G]
+    return out
+
+
 def _reduce(x, op, device):
     if not dist.is_available() or not dist.is_initialized() or dist.get_world_size() == 1:
         return float(x)

@@ -88,10 +88,11 @@ def request_kv(seed, layer, req, Hkv, n, d=128, out_k=None, out_v=None):
     return K, V
 
 
-def request_kv_device(seed, layer, req, Hkv, n, K, V, d=128, stream=None):
+def request_kv_device(seed, layer, req, Hkv, n, K, V, d=128, stream=None, head0=0):
     """Same bytes as request_kv, generated on the GPU into device torch tensors
-    K, V [Hkv][n][d] (int16 / uint16 views of bf16).  Host computes the per-token
-    topic runs and topic centres; the device expands them."""
+    K, V [Hkv][n][d] (int16 / uint16 views of bf16) for KV heads head0 ..
+    head0+Hkv-1.  Host computes the per-token topic runs and topic centres; the
+    device expands them."""
     import torch
     topic = np.empty(n, np.uint8)
     mu = np.empty((32, d), np.float32)
@@ -99,7 +100,7 @@ def request_kv_device(seed, layer, req, Hkv, n, K, V, d=128, stream=None):
     dev = K.device
     s = stream.cuda_stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
     for h in range(Hkv):
-        lib().synth_segment_plan(seed, layer, req, h, n, d, _ptr(topic), _ptr(mu), _ptr(keys))
+        lib().synth_segment_plan(seed, layer, req, head0 + h, n, d, _ptr(topic), _ptr(mu), _ptr(keys))
         t_d = torch.from_numpy(topic).to(dev)
         m_d = torch.from_numpy(mu).to(dev)
         rc = glib().synth_gpu_segment_kv(n, d, t_d.data_ptr(), m_d.data_ptr(), int(keys[0]), int(keys[1]),

@@ -66,3 +66,45 @@ def test_two_gloo_ranks_reduce_like_bench():
     assert res[0][1] == [0, 1, 2] and res[1][1] == [3, 4, 5]
     for _, _, mx, sm in res:
         assert mx == 2.0 and sm == 6.0            # max-over-ranks time, whole-job token count
+
+
+def _gather_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    from paper_2605_18071_b200 import dist as kdist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        B, Hkv, G, L, d = 1, 4, 7, 2, 3           # c4-like grouping (G = 7), 2 heads per rank
+        parts = kdist.unit_partition(B, Hkv, world)
+        reqs, h0, h1 = kdist.rank_heads(parts[rank])
+        # this rank's "attention output" [L][B_r][Hq_r][d]: value encodes (layer, global request, global q-head)
+        out = torch.empty((L, len(reqs), (h1 - h0) * G, d))
+        for l in range(L):
+            for i, req in enumerate(reqs):
+                for hq in range((h1 - h0) * G):
+                    out[l, i, hq] = 1000 * l + 100 * req + (h0 * G + hq)
+        gathered = torch.empty((world * out.shape[0],) + tuple(out.shape[1:]))   # concatenated along dim 0
+        dist.all_gather_into_tensor(gathered, out)
+        full = kdist.assemble_heads(gathered.view((world,) + tuple(out.shape)), parts, B, Hkv, G)
+        ok = all(float(full[l, r, hq, 0]) == 1000 * l + 100 * r + hq
+                 for l in range(L) for r in range(B) for hq in range(Hkv * G))
+        q.put((rank, ok, tuple(full.shape)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_head_sharded_output_all_gather_two_ranks():
+    # head sharding: each rank attends 2 of the 4 KV heads; one all-gather
+    # of the fp32 outputs reassembles [L][B][Hq][d] in global head order on every rank
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gather_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    assert all(ok for _, ok, _ in res) and all(shape == (2, 1, 28, 3) for _, _, shape in res)
