@@ -23,6 +23,9 @@
 // (R10).  Two block scans give tie ranks and output positions, so ids come out
 // ascending with no sort.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
 
 #include "common.cuh"
 #include "internal.h"
@@ -122,6 +125,7 @@ __device__ __forceinline__ void score_tile(const StepParams& p, int bi, int h, i
 struct TopkSmem {
     int hist[2048];
     int scan[33];
+    uint32_t wmin[32], wmax[32];
     uint32_t digit;
     int above;
 };
@@ -134,39 +138,82 @@ struct TopkSmem {
 // (R10); k must not exceed the candidate count.  3-pass radix select (11 + 11 + 10
 // bits) with warp-aggregated shared histograms, then two block scans.
 template <int KPT, class Load, class Emit>
-__device__ void cta_topk(int k, int reps, Load load, Emit emit, TopkSmem& sm) {
+__device__ void cta_topk(int k, int reps, Load load, Emit emit, TopkSmem& sm,
+                         unsigned long long* ph = nullptr) {
     const int tid = threadIdx.x, nthr = blockDim.x;
+    auto phs = [&](int i) {
+        if (ph && tid == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+            ph[i] = t;
+        }
+    };
     uint32_t key[KPT];
     uint32_t cm = 0;
     if (reps == 1) load(0, key, cm);
-    uint32_t prefix = 0, mask = 0;
-    int kk = k;
+    phs(0);
+    // ---- key range of the candidates: the digits start at the highest bit where the
+    // candidate keys differ (bits above it are common), so the first histogram is not
+    // concentrated in one bin and plain shared atomics suffice
+    uint32_t kmin = 0xFFFFFFFFu, kmax = 0u;
 #pragma unroll 1
-    for (int pass = 0; pass < 3; ++pass) {
-        const int shift = pass == 0 ? 21 : pass == 1 ? 10 : 0;
-        const int nbins = pass == 2 ? 1024 : 2048;
+    for (int c = 0; c < reps; ++c) {
+        if (reps > 1) load(c, key, cm);
+#pragma unroll
+        for (int i = 0; i < KPT; ++i)
+            if ((cm >> i) & 1u) {
+                kmin = min(kmin, key[i]);
+                kmax = max(kmax, key[i]);
+            }
+    }
+    kmin = __reduce_min_sync(0xffffffffu, kmin);
+    kmax = __reduce_max_sync(0xffffffffu, kmax);
+    if ((tid & 31) == 0) {
+        sm.wmin[tid >> 5] = kmin;
+        sm.wmax[tid >> 5] = kmax;
+    }
+    __syncthreads();
+    kmin = 0xFFFFFFFFu;
+    kmax = 0u;
+    for (int w = 0; w < (nthr >> 5); ++w) {
+        kmin = min(kmin, sm.wmin[w]);
+        kmax = max(kmax, sm.wmax[w]);
+    }
+    const uint32_t diff = kmin ^ kmax;
+    int lo = diff ? 32 - __clz(diff) : 0;         // bits [0, lo) still to resolve
+    uint32_t mask = lo == 32 ? 0u : ~((1u << lo) - 1u);
+    uint32_t prefix = kmin & mask;
+    int kk = k;
+    phs(0);
+#pragma unroll 1
+    for (int pass = 0; lo > 0; ++pass) {
+        const int width = min(11, lo);
+        const int shift = lo - width;
+        const int nbins = 1 << width;
         for (int i = tid; i < nbins; i += nthr) sm.hist[i] = 0;
         __syncthreads();
 #pragma unroll 1
         for (int c = 0; c < reps; ++c) {
             if (reps > 1) load(c, key, cm);
 #pragma unroll
-            for (int i = 0; i < KPT; ++i) {
-                const bool act = ((cm >> i) & 1u) && (key[i] & mask) == prefix;
-                warp_hist_add(sm.hist, (key[i] >> shift) & (uint32_t)(nbins - 1), act);
-            }
+            for (int i = 0; i < KPT; ++i)
+                if (((cm >> i) & 1u) && (key[i] & mask) == prefix)
+                    atomicAdd(&sm.hist[(key[i] >> shift) & (uint32_t)(nbins - 1)], 1);
         }
         __syncthreads();
         // bins in descending order; thread t owns bins [nbins - (t+1) bpt, nbins - t bpt)
-        const int bpt = nbins / nthr;
+        const int bpt = (nbins + nthr - 1) / nthr;
         int cnt = 0;
-        for (int i = 0; i < bpt; ++i) cnt += sm.hist[nbins - 1 - (tid * bpt + i)];
+        for (int i = 0; i < bpt; ++i) {
+            const int d = nbins - 1 - (tid * bpt + i);
+            if (d >= 0) cnt += sm.hist[d];
+        }
         int tot;
         int above = block_exclusive_scan(cnt, sm.scan, &tot);
         if (above < kk && kk <= above + cnt) {
             for (int i = 0; i < bpt; ++i) {
                 const int d = nbins - 1 - (tid * bpt + i);
-                const int ci = sm.hist[d];
+                const int ci = d >= 0 ? sm.hist[d] : 0;
                 if (above + ci >= kk) {
                     sm.digit = (uint32_t)d;
                     sm.above = above;
@@ -179,7 +226,9 @@ __device__ void cta_topk(int k, int reps, Load load, Emit emit, TopkSmem& sm) {
         prefix |= sm.digit << shift;
         mask |= (uint32_t)(nbins - 1) << shift;
         kk -= sm.above;
+        lo = shift;
         __syncthreads();
+        phs(1 + min(pass, 2));
     }
     const uint32_t T = prefix;                    // take keys > T, and the kk lowest-position keys == T
     int ngt = 0, neq = 0;
@@ -197,6 +246,7 @@ __device__ void cta_topk(int k, int reps, Load load, Emit emit, TopkSmem& sm) {
     const int tie0 = block_exclusive_scan(neq, sm.scan, &tot);
     const int ntake = min(max(kk - tie0, 0), neq);
     int pos = block_exclusive_scan(ngt + ntake, sm.scan, &tot);
+    phs(4);
     int tie = tie0;
 #pragma unroll 1
     for (int c = 0; c < reps; ++c) {
@@ -218,6 +268,7 @@ __device__ void cta_topk(int k, int reps, Load load, Emit emit, TopkSmem& sm) {
 // in ascending id order, so the concatenation over tiles is ascending too.  The
 // last CTA of the segment to finish (arrival counter) runs the final selection.
 struct SelBufs {
+    unsigned long long* trace;   // KVD_SEL_TRACE: per-CTA globaltimer stamps [ctas][4] (experiments only)
     uint32_t* cand_key;     // [R][Hkv][max_tiles][kmax]
     int32_t* cand_id;       // [R][Hkv][max_tiles][kmax]
     int32_t* cand_cnt;      // [R][Hkv][max_tiles]
@@ -246,7 +297,17 @@ __global__ void __launch_bounds__(kScoreThreads, 2) select_kernel(StepParams p, 
     if ((int64_t)tile * bpc >= nb) return;        // whole CTA past this request's end (does not arrive)
     const int64_t seg = ((int64_t)p.layer * p.R + r) * p.Hkv + h;
     float acc[V];
+    const int64_t cta_lin = ((int64_t)bi * p.Hkv + h) * gridDim.x + tile;
+    auto stamp = [&](int i) {
+        if (sb.trace && threadIdx.x == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+            sb.trace[cta_lin * 4 + i] = t;
+        }
+    };
+    stamp(0);
     score_tile<V>(p, bi, h, nb, seg, q, summ, scores, qbar, acc);
+    stamp(1);
     if (p.k == 0) return;
     const SegGeom g = seg_geom(n, p.P, p.sink_tokens, p.local_tokens);
     const int64_t rs = (int64_t)r * p.Hkv + h;
@@ -306,6 +367,7 @@ __global__ void __launch_bounds__(kScoreThreads, 2) select_kernel(StepParams p, 
     }
     __syncthreads();
     if (!s_last) return;
+    stamp(2);
     int32_t* ids_out = out_ids + ((int64_t)bi * p.Hkv + h) * p.k;
     float* sc_out = out_scores ? out_scores + ((int64_t)bi * p.Hkv + h) * p.k : nullptr;
     const float* sc = scores + seg * p.nb_pad;
@@ -334,7 +396,8 @@ __global__ void __launch_bounds__(kScoreThreads, 2) select_kernel(StepParams p, 
                 ids_out[pos] = (int32_t)b;
                 if (sc_out) sc_out[pos] = __ldcg(&sc[b]);
             },
-            sm);
+            sm, sb.trace ? sb.trace + (1 << 18) + cta_lin * 8 : nullptr);
+        stamp(3);
         return;
     }
     // candidate offsets per tile (ntiles <= max_tiles <= 128 per pass of this loop)
@@ -392,10 +455,48 @@ template <int V, int KPT, bool TWO>
 static cudaError_t launch_sel(kvd_cache* c, const StepParams& p, const uint16_t* q, int reps, int32_t* out_ids,
                               float* out_scores, cudaStream_t s) {
     const unsigned tiles = (unsigned)((c->nb_pad + kScoreThreads * V - 1) / (kScoreThreads * V));
-    SelBufs sb{c->cand_key, c->cand_id, c->cand_cnt, c->sel_ctr, c->max_sel_tiles, c->kmax > 0 ? c->kmax : 1};
-    return launch_pdl(select_kernel<V, KPT, TWO>, dim3(tiles, p.Hkv, p.B), dim3(kScoreThreads), 0, s, p, q,
-                      (const uint16_t*)c->summ, c->scores, (const int32_t*)c->ntok_dev, sb, reps, out_ids,
-                      out_scores);
+    static int trace = -1;
+    static unsigned long long* tbuf = nullptr;
+    if (trace < 0) {
+        trace = getenv("KVD_SEL_TRACE") ? 1 : 0;
+        if (trace) cudaMalloc(&tbuf, sizeof(unsigned long long) * ((1 << 18) + 8 * (1 << 16)));
+    }
+    const int64_t nctas = (int64_t)tiles * p.Hkv * p.B;
+    if (trace) cudaMemsetAsync(tbuf, 0, sizeof(unsigned long long) * ((1 << 18) + 8 * (1 << 16)), s);
+    SelBufs sb{trace && nctas <= (1 << 16) ? tbuf : nullptr, c->cand_key, c->cand_id, c->cand_cnt, c->sel_ctr, c->max_sel_tiles, c->kmax > 0 ? c->kmax : 1};
+    cudaError_t e = launch_pdl(select_kernel<V, KPT, TWO>, dim3(tiles, p.Hkv, p.B), dim3(kScoreThreads), 0, s, p, q,
+                               (const uint16_t*)c->summ, c->scores, (const int32_t*)c->ntok_dev, sb, reps, out_ids,
+                               out_scores);
+    if (trace && sb.trace) {   // experiments only: synchronous dump of per-CTA phase times
+        cudaStreamSynchronize(s);
+        std::vector<unsigned long long> h((size_t)nctas * 4);
+        cudaMemcpy(h.data(), tbuf, h.size() * 8, cudaMemcpyDeviceToHost);
+        unsigned long long t0 = ~0ull;
+        for (int64_t i = 0; i < nctas; ++i) if (h[i * 4] && h[i * 4] < t0) t0 = h[i * 4];
+        const char* names[4] = {"entry", "scored", "topk_begin", "topk_end"};
+        for (int j = 0; j < 4; ++j) {
+            std::vector<double> v;
+            for (int64_t i = 0; i < nctas; ++i) if (h[i * 4 + j]) v.push_back((h[i * 4 + j] - t0) * 1e-3);
+            if (v.empty()) continue;
+            std::sort(v.begin(), v.end());
+            fprintf(stderr, "sel trace V=%d %-10s n=%5zu min %7.2f p50 %7.2f p90 %7.2f max %7.2f us\n", V, names[j],
+                    v.size(), v[0], v[v.size() / 2], v[v.size() * 9 / 10], v.back());
+        }
+        // top-k phases relative to topk_begin of the same CTA
+        std::vector<unsigned long long> h2((size_t)nctas * 8);
+        cudaMemcpy(h2.data(), tbuf + (1 << 18), h2.size() * 8, cudaMemcpyDeviceToHost);
+        const char* pn[5] = {"loaded", "pass0", "pass1", "pass2", "scans"};
+        for (int j = 0; j < 5; ++j) {
+            std::vector<double> v;
+            for (int64_t i = 0; i < nctas; ++i)
+                if (h2[i * 8 + j] && h[i * 4 + 2]) v.push_back(((double)h2[i * 8 + j] - (double)h[i * 4 + 2]) * 1e-3);
+            if (v.empty()) continue;
+            std::sort(v.begin(), v.end());
+            fprintf(stderr, "sel topk phase %-7s n=%5zu p50 %7.2f max %7.2f us (from topk_begin)\n", pn[j], v.size(),
+                    v[v.size() / 2], v.back());
+        }
+    }
+    return e;
 }
 
 template <int V>
