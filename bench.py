@@ -155,7 +155,14 @@ class Runner:
         nb = (n + P - 1) // P
         C = cfg["C"] if cfg["C"] is not None else nb
         A = args.alias if args.alias is not None else cfg["alias"]
-        self.A = A if (A and A < L) else L
+        A = A if (A and A < L) else L
+        if C < nb and args.alias is None:
+            # keep every rank's pinned host store under ~40 % of the box's RAM (all ranks share it)
+            world_ = int(os.environ.get("WORLD_SIZE", "1"))
+            per_layer = cfg["B"] * cfg["Hkv"] * nb * RECORD
+            ram = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
+            A = max(1, min(A, int(0.4 * ram / world_ // per_layer)))
+        self.A = A
         self.resident = C >= nb
         from paper_2605_18071_b200 import dist as kdist
         world = int(os.environ.get("WORLD_SIZE", "1"))

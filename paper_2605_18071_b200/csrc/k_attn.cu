@@ -10,7 +10,7 @@
 // streams the same number of tiles whatever B, Hkv and k are; a worker whose
 // range crosses a segment boundary produces one partial per segment piece.
 //
-// Per worker (one warp): a private STAGES-deep ring of 8 KiB tiles in shared
+// Per worker (one warp; 8 per SM by default): a private STAGES-deep ring of 8 KiB tiles in shared
 // memory fed by bulk async copies (TMA engine) completing on mbarriers; the
 // (block, slot) entries are staged through shared memory 128 at a time so a
 // copy is never issued behind a dependent global load.  Per tile, on tensor
@@ -49,7 +49,6 @@ struct AttnBufs {
     uint32_t* ctr;      // [R][Hkv] pieces arrived
 };
 
-constexpr int kAttnThreads = kAttnWarps * 32;
 constexpr int kEntChunk = 128;                      // list entries staged per chunk (>= STAGES * 16)
 
 struct Work {
@@ -75,17 +74,17 @@ __device__ __forceinline__ int worker_of(int t, const Work& wk) {
     return (int)(((int64_t)(t + 1) * wk.NW - 1) / wk.T);
 }
 
-template <int STAGES>
-__global__ void __launch_bounds__(kAttnThreads, 1) attn_kernel(StepParams p, AttnBufs ab, Work wk,
+template <int STAGES, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, 1) attn_kernel(StepParams p, AttnBufs ab, Work wk,
                                                                const uint16_t* __restrict__ q,
                                                                const int32_t* __restrict__ attn,
                                                                float* __restrict__ out, float* __restrict__ out_lse) {
     extern __shared__ __align__(1024) uint8_t stage[];
-    __shared__ __align__(8) uint64_t bar[kAttnWarps][STAGES];
-    __shared__ int2 s_ent[kAttnWarps][2][kEntChunk];
-    __shared__ float s_scale[kAttnWarps][kMaxPieces][8];    // merge weights of the pieces
+    __shared__ __align__(8) uint64_t bar[WARPS][STAGES];
+    __shared__ int2 s_ent[WARPS][2][kEntChunk];
+    __shared__ float s_scale[WARPS][kMaxPieces][8];         // merge weights of the pieces
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int w = blockIdx.x * kAttnWarps + warp;
+    const int w = blockIdx.x * WARPS + warp;
     uint8_t* my_stage = stage + (size_t)warp * STAGES * kTileBytes;
     uint64_t* my_bar = bar[warp];
     if (lane == 0) {
@@ -467,18 +466,18 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_kernel(StepParams p, Att
     ATTN_STAMP(6);
 }
 
-template <int STAGES>
+template <int STAGES, int WARPS>
 static cudaError_t launch_attn_s(kvd_cache* c, const StepParams& p, const uint16_t* q, const int32_t* attn, float* out,
                                  float* out_lse, cudaStream_t s) {
-    constexpr size_t smem = (size_t)kAttnWarps * STAGES * kTileBytes;
+    constexpr size_t smem = (size_t)WARPS * STAGES * kTileBytes;
     static int max_ctas = 0;
     if (!max_ctas) {
-        cudaError_t e = cudaFuncSetAttribute(attn_kernel<STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e = cudaFuncSetAttribute(attn_kernel<STAGES, WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         int per_sm = 0, sms = 0, dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, attn_kernel<STAGES>, kAttnThreads, smem);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, attn_kernel<STAGES, WARPS>, WARPS * 32, smem);
         if (e != cudaSuccess) return e;
         max_ctas = sms * (per_sm > 0 ? per_sm : 1);
     }
@@ -488,7 +487,7 @@ static cudaError_t launch_attn_s(kvd_cache* c, const StepParams& p, const uint16
     wk.T = S * wk.TS;
     // workers: enough to fill every SM, but at most kMaxPieces - 1 per segment so a
     // segment never has more than kMaxPieces pieces (<= ceil(NW/S) + 1), and at most T
-    int nw = max_ctas * kAttnWarps;
+    int nw = max_ctas * WARPS;
     nw = std::min(nw, S * (kMaxPieces - 1));
     nw = std::min(nw, wk.T);
     wk.NW = std::max(nw, 1);
@@ -507,8 +506,8 @@ static cudaError_t launch_attn_s(kvd_cache* c, const StepParams& p, const uint16
     wk.trace = trace ? tbuf : nullptr;
     if (trace) cudaMemsetAsync(tbuf, 0, sizeof(unsigned long long) * 8 * 8192, s);
     AttnBufs ab{c->slots, c->ntok_dev, c->zero_rec, c->part_o, c->part_ml, c->split_ctr};
-    const unsigned grid = (unsigned)((wk.NW + kAttnWarps - 1) / kAttnWarps);
-    cudaError_t e = launch_pdl(attn_kernel<STAGES>, dim3(grid), dim3(kAttnThreads), smem, s, p, ab, wk, q, attn, out,
+    const unsigned grid = (unsigned)((wk.NW + WARPS - 1) / WARPS);
+    cudaError_t e = launch_pdl(attn_kernel<STAGES, WARPS>, dim3(grid), dim3(WARPS * 32), smem, s, p, ab, wk, q, attn, out,
                                out_lse);
     if (e != cudaSuccess) return e;
     if (trace) {   // experiments only: synchronous dump of per-warp phase times (us from first stamp)
@@ -532,15 +531,19 @@ static cudaError_t launch_attn_s(kvd_cache* c, const StepParams& p, const uint16
 
 cudaError_t launch_attention(kvd_cache* c, const StepParams& p, const uint16_t* q, const int32_t* attn, float* out,
                              float* out_lse, cudaStream_t s) {
-    // ring depth per warp worker; KVD_ATTN_STAGES (3 or 6) overrides for experiments
-    static int stages = 0;
-    if (!stages) {
-        const char* env = getenv("KVD_ATTN_STAGES");
-        stages = env ? atoi(env) : 6;
-        if (stages != 3 && stages != 6) stages = 6;
+    // (warps per CTA, ring depth per warp): KVD_ATTN_CFG = 3 (4 warps x 3 stages, 2 CTAs per
+    // SM: 8 warp workers per SM, default), 1 (4 x 6, 1 CTA per SM), 2 (2 x 12).  Measured at
+    // c2 / c3: 28.9 / 37.7 us (3), 28.7 / 41.2 us (1), 35.4 / 53.1 us (2): the per-warp
+    // dependent chain of MMA + softmax needs >= 2 warps per scheduler.
+    static int cfg = 0;
+    if (!cfg) {
+        const char* env = getenv("KVD_ATTN_CFG");
+        cfg = env ? atoi(env) : 3;
+        if (cfg < 1 || cfg > 3) cfg = 3;
     }
-    if (stages == 3) return launch_attn_s<3>(c, p, q, attn, out, out_lse, s);
-    return launch_attn_s<6>(c, p, q, attn, out, out_lse, s);
+    if (cfg == 2) return launch_attn_s<12, 2>(c, p, q, attn, out, out_lse, s);
+    if (cfg == 3) return launch_attn_s<3, 4>(c, p, q, attn, out, out_lse, s);
+    return launch_attn_s<6, 4>(c, p, q, attn, out, out_lse, s);
 }
 
 }  // namespace kvd
