@@ -1,8 +1,10 @@
 """bench.py — decode-step throughput of the KVDrive hot path on B200 (libkvd).
 
 One "step" = one decode token for every request of the batch through all L
-layers: per layer, kvd_select_topk (a1+a2) -> kvd_resolve_and_fetch (a3+a4)
--> kvd_sparse_decode (a5+a6), layers serially.  The whole step
+layers: per layer, kvd_select_resolve_fetch (a1+a2+a3+a4: score kernel, then
+one fused top-k + resolve + fetch kernel; --unfused: kvd_select_topk then
+kvd_resolve_and_fetch) -> kvd_sparse_decode (a5+a6), layers serially
+(DESIGN.md §2).  The per-kernel roofline pass times the three separate calls.  The whole step
 is captured once as a CUDA graph and replayed; the decode-step index lives in
 device memory (kvd_set_device_step) so every replay is a new step.
 
@@ -29,6 +31,11 @@ import threading
 import time
 
 import numpy as np
+
+
+def kvd_launch_count():
+    from paper_2605_18071_b200 import kvd
+    return int(kvd.lib().kvd_launch_count())
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -74,6 +81,9 @@ def parse(argv=None):
                     help="multi-GPU unit assignment: 'requests' = every rank serves its own B requests (weak "
                          "scaling, no collective); 'heads' = the config's B*Hkv units are partitioned over the "
                          "ranks (strong scaling; SURVEY 8.6) and the fp32 outputs are all-gathered each step")
+    ap.add_argument("--unfused", action="store_true",
+                    help="step through kvd_select_topk + kvd_resolve_and_fetch instead of the fused "
+                         "kvd_select_resolve_fetch (same results)")
     ap.add_argument("--layers", type=int, default=None, help="override L (profiling only; not a bench number)")
     ap.add_argument("--cpu-sample-s", type=float, default=12.0, help="target seconds of oracle work")
     return ap.parse_args(argv)
@@ -217,7 +227,8 @@ class Runner:
         edges = [round(i * B / m) for i in range(m + 1)]
         self.chains = [(edges[i], edges[i + 1]) for i in range(m) if edges[i + 1] > edges[i]]
         self.chain_streams = [torch.cuda.Stream(device=dev) for _ in self.chains]
-        self.launches_per_step = L * (3 if self.resident else 4) * len(self.chains)
+        self.fused = not args.unfused
+        self.launches_per_step = None  # counted by libkvd (kvd_launch_count) over one eager step / the capture
 
     # one layer of one chain (requests b0..b1-1) through the three ABI calls
     def layer(self, l, s, step=0, chain=None):
@@ -225,8 +236,11 @@ class Runner:
         b0, b1 = chain if chain else (0, len(self.reqs))
         reqs = self.reqs[b0:b1]
         q = self.q_cur[l, b0:b1]
-        c.select_topk(l, q, reqs, k, self.ids[l, b0:b1], None, stream=s)
-        c.resolve_and_fetch(l, reqs, self.ids[l, b0:b1], k, step, self.attn[l, b0:b1], stream=s)
+        if self.fused:   # kvd_select_resolve_fetch: top-k, resolve and fetch with no kernel boundary
+            c.select_resolve_fetch(l, q, reqs, k, step, self.ids[l, b0:b1], self.attn[l, b0:b1], stream=s)
+        else:
+            c.select_topk(l, q, reqs, k, self.ids[l, b0:b1], None, stream=s)
+            c.resolve_and_fetch(l, reqs, self.ids[l, b0:b1], k, step, self.attn[l, b0:b1], stream=s)
         c.sparse_decode(l, q, reqs, self.attn[l, b0:b1], self.W, self.out[l, b0:b1], self.lse[l, b0:b1], stream=s)
 
     def eager_step(self, s):
@@ -235,13 +249,16 @@ class Runner:
             self.q_cur.copy_(self.q_dev[self.t], non_blocking=True)
         self.t += 1
         self.cache.set_device_step(None)
+        n0 = kvd_launch_count()
         for l in range(self.cfg["L"]):
             self.layer(l, s, step=self.t)
+        self.launches_per_step = kvd_launch_count() - n0
 
     def capture(self, s):
         torch = self.torch
         self.cache.set_device_step(self.step_dev)
         g = torch.cuda.CUDAGraph()
+        n0 = kvd_launch_count()
         with torch.cuda.graph(g, stream=s):
             self.step_dev.add_(1)
             # SFC overlap: each request group runs its own chain of layers on its own stream
@@ -253,6 +270,7 @@ class Runner:
                     self.layer(l, cs, chain=ch)
             for cs in self.chain_streams:
                 s.wait_stream(cs)
+        self.launches_per_step = kvd_launch_count() - n0
         self.graph = g
 
     def prepare_graph(self, s):
@@ -452,7 +470,7 @@ def run_gpu(args):
                    "layers": L, "q_heads": cfg["Hq"], "kv_heads": cfg["Hkv"], "block_tokens": cfg["P"],
                    "top_k_blocks": cfg["k"], "slots_per_segment": cfg["C"] or (cfg["n"] // cfg["P"]),
                    "policy": args.policy, "alpha": args.alpha, "host_layer_alias": R.A if not R.resident else None,
-                   "fill_steps": R.fill, "graph": not args.no_graph, "chains": len(R.chains), "parallelism": (f"head-shard x{world} + NCCL all-gather" if heads_mode else f"request-shard x{world}"),
+                   "fill_steps": R.fill, "graph": not args.no_graph, "chains": len(R.chains), "fused_select_resolve": R.fused, "parallelism": (f"head-shard x{world} + NCCL all-gather" if heads_mode else f"request-shard x{world}"),
                    "l2": "inputs larger than L2 (no flush)"},
         "hit_rate": hit_rate, "misses_per_segment": misses_per_seg,
         "roofline": roof, "roofline_attn": roof_attn, "kernels": kernels,

@@ -89,7 +89,11 @@ typedef struct {
     int32_t max_requests;        /* request slots 0 .. max_requests-1 */
     int64_t max_context;         /* tokens per request (upper bound) */
     int64_t slots_per_segment;   /* C, including the pinned blocks.  C >= ceil(max_context/P)
-                                    => fully resident: no host store, block b lives in slot b */
+                                    => fully resident: no host store, block b lives in slot b.
+                                    A host-backed cache ranks its victims on chip: it needs
+                                    8*C + 20*max_select + ceil(max_context/P)/8 <= 227 KiB
+                                    (C <= ~27,000 at max_select 128), else KVD_EINVAL.
+                                    Blocks per request <= 262,144 (top-k cluster capacity). */
     int32_t max_select;          /* largest k_blocks any step call will use (sizes scratch) */
     int32_t sink_tokens;         /* 4 */
     int32_t local_tokens;        /* 64 */
@@ -170,6 +174,17 @@ kvd_status kvd_resolve_and_fetch(kvd_cache* c, int32_t layer, const int32_t* req
                                  int32_t B, const int32_t* ids, int32_t k_blocks,
                                  uint32_t step, int32_t* out_attn, kvd_stream stream);
 
+/* (1)+(2) fused: exactly kvd_select_topk followed by kvd_resolve_and_fetch (same
+ * arguments, same results, same cache state, bit for bit), but the top-k, the
+ * resolve and the miss fetch of a segment run in one kernel (one thread-block
+ * cluster per segment; rank 0 resolves and copies the misses), so the step has
+ * no kernel boundary between selection and fetch.  out_ids is still written.
+ * Errors as for the two calls. */
+kvd_status kvd_select_resolve_fetch(kvd_cache* c, int32_t layer, const uint16_t* q,
+                                    const int32_t* req_ids, int32_t B, int32_t k_blocks,
+                                    uint32_t step, int32_t* out_ids, float* out_scores,
+                                    int32_t* out_attn, kvd_stream stream);
+
 /* CUDA-graph support for (2): when dev_step != NULL, every later resolve reads
  * the decode-step index from *dev_step (device uint32) when the kernel runs and
  * ignores its host `step` argument, so one captured step can be replayed for
@@ -216,8 +231,14 @@ kvd_status kvd_reset_stats(kvd_cache* c);                 /* synchronises the de
 kvd_status kvd_check(kvd_cache* c);
 const char* kvd_last_error(void);
 
-/* Library build identity, e.g. "kvd 0.1 sm_100a". */
+/* Library build identity, e.g. "kvd 0.2 sm_100a". */
 const char* kvd_version(void);
+
+/* Number of step kernels (select, resolve, gather, attention, merge) this process
+ * has launched through libkvd so far (thread-safe counter; a launch recorded into
+ * a CUDA graph counts once, when it is captured).  The difference across one
+ * step call sequence is that step's launch count.  Never fails. */
+uint64_t kvd_launch_count(void);
 
 #ifdef __cplusplus
 }

@@ -155,6 +155,10 @@ __device__ __forceinline__ int4 ld_stream16(const void* p) {
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// Process-wide count of step-kernel launches issued by libkvd (kvd_launch_count;
+// a launch recorded into a CUDA graph counts once, at capture).
+void count_launch();
+
 // `priority` (optional, cudaLaunchAttributePriority): the host-link gather is launched at the
 // device's greatest priority so its CTAs are scheduled ahead of concurrent HBM-bound kernels
 // of other micro-batch chains (keeps the link busy).
@@ -173,6 +177,7 @@ inline cudaError_t launch_pdl_prio(int priority, void (*kern)(KArgs...), dim3 gr
     attr[1].val.priority = priority;
     cfg.attrs = attr;
     cfg.numAttrs = priority ? 2 : 1;
+    count_launch();
     return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 template <typename... KArgs, typename... Args>

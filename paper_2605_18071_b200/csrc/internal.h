@@ -24,7 +24,7 @@ constexpr int kAttnWarps = 4;         // warps per attention CTA
 constexpr int kAttnStages = 3;        // smem stages per warp
 constexpr int kTileBytes = 8192;      // one 16-token K||V tile
 constexpr int kSplitTiles = 16;       // (legacy split size; StepParams.nsplit)
-constexpr int kMaxSelTiles = 128;     // select tiles per segment (k_select.cu s_off)
+constexpr int kMaxSelectBlocks = 8 * 1024 * 32;   // top-k cluster capacity: 8 CTAs x 1024 threads x 32 keys
 constexpr int kMaxPieces = 32;        // attention partials per (request, KV head) (k_attn.cu)
 constexpr int64_t kSlotOfBytes = 64ll << 20;   // setup scratch for per-block slot targets
 
@@ -69,12 +69,6 @@ struct kvd_cache {
     int32_t* miss_count = nullptr;
     float* part_o = nullptr;
     float* part_ml = nullptr;
-    uint32_t* split_ctr = nullptr;
-    uint32_t* sel_ctr = nullptr;           // [R][Hkv] select arrival counters
-    uint32_t* cand_key = nullptr;          // [R][Hkv][max_sel_tiles][kmax] tile-local top-k keys
-    int32_t* cand_id = nullptr;            // [R][Hkv][max_sel_tiles][kmax] their block ids
-    int32_t* cand_cnt = nullptr;           // [R][Hkv][max_sel_tiles]
-    int32_t max_sel_tiles = 0;             // ceil(nb_pad / 512): tiles of the narrowest select CTA
     unsigned long long* stats = nullptr;   // [5] kvd_stats fields
     int32_t* err = nullptr;
     int32_t* ntok_dev = nullptr;
@@ -94,7 +88,11 @@ cudaError_t launch_prefix(kvd_cache* c, int layer, int req, const uint16_t* dk, 
                           cudaStream_t s);
 cudaError_t launch_select(kvd_cache* c, const StepParams& p, const uint16_t* q, int32_t* out_ids, float* out_scores,
                           cudaStream_t s);
+size_t resolve_smem_bytes(int64_t nkeys, int64_t kmax, int64_t nb_pad);   // k_resolve.cu
+constexpr size_t kMaxSmemBytes = 227 * 1024;
 cudaError_t launch_resolve(kvd_cache* c, const StepParams& p, const int32_t* ids, int32_t* out_attn, cudaStream_t s);
+cudaError_t launch_select_resolve(kvd_cache* c, const StepParams& p, const uint16_t* q, int32_t* out_ids,
+                                  float* out_scores, int32_t* out_attn, cudaStream_t s);
 cudaError_t launch_attention(kvd_cache* c, const StepParams& p, const uint16_t* q, const int32_t* attn, float* out,
                              float* out_lse, cudaStream_t s);
 

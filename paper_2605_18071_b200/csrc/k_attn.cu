@@ -25,7 +25,10 @@
 // parts take two MMAs.  The S^T accumulator becomes the P^T B-fragment with
 // movmatrix.trans.  Online softmax in the log2 domain (exp2).
 //
-// (a6) Pieces of a segment merge in the last-arriving worker:
+// (a6) A segment handled by one worker is finalised in place; otherwise each
+// piece writes its unnormalised partial (o~_j, m_j, l_j) and merge_kernel,
+// launched behind attn_kernel (PDL, so no fences or arrival counters on the
+// streaming path), combines them with one warp per query head:
 //     m = max_j m_j;  l = sum_j l_j 2^(m_j-m);  o = sum_j 2^(m_j-m) o~_j / l;
 //     lse = (m + log2 l) ln 2.
 // HBM-bound: 8 KiB per 16-token tile; 4*G flop per 4 B of K/V.
@@ -46,7 +49,6 @@ struct AttnBufs {
     const uint8_t* zero_rec;
     float* part_o;      // [R][Hkv][kMaxPieces][8][128]
     float* part_ml;     // [R][Hkv][kMaxPieces][8][2]
-    uint32_t* ctr;      // [R][Hkv] pieces arrived
 };
 
 constexpr int kEntChunk = 128;                      // list entries staged per chunk (>= STAGES * 16)
@@ -82,7 +84,6 @@ __global__ void __launch_bounds__(WARPS * 32, 1) attn_kernel(StepParams p, AttnB
     extern __shared__ __align__(1024) uint8_t stage[];
     __shared__ __align__(8) uint64_t bar[WARPS][STAGES];
     __shared__ int2 s_ent[WARPS][2][kEntChunk];
-    __shared__ float s_scale[WARPS][kMaxPieces][8];         // merge weights of the pieces
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int w = blockIdx.x * WARPS + warp;
     uint8_t* my_stage = stage + (size_t)warp * STAGES * kTileBytes;
@@ -232,67 +233,6 @@ __global__ void __launch_bounds__(WARPS * 32, 1) attn_kernel(StepParams p, AttnB
                 pml[h1 * 2 + 1] = l1;
             }
         }
-        __threadfence();
-        __syncwarp();
-        uint32_t last = 0;
-        if (lane == 0) last = atomicAdd(&ab.ctr[rs], 1u) == (uint32_t)(np - 1);
-        last = __shfl_sync(0xffffffffu, last, 0);
-        if (!last) return;
-        ATTN_STAMP(4);
-        __threadfence();
-        // (a6) merge the np <= 32 pieces, all heads at once.  Phase 1: lane jj holds piece jj's
-        // (m, l) of every head; per-head max / weighted sum by warp reductions; the weights
-        // 2^(m_jj - M) go to shared memory.  Phase 2: lane owns dims 4 lane .. +3 of every head
-        // and sums the np partials with independent loads.
-        const float* po0 = ab.part_o + (rs * kMaxPieces * 8) * (int64_t)kHeadDim;
-        const float* pml0 = ab.part_ml + (rs * kMaxPieces * 8) * 2;
-        float Mh[8], lh[8];
-        float mj[8], lj[8];
-#pragma unroll
-        for (int hh = 0; hh < 8; ++hh) {
-            mj[hh] = (lane < np && hh < p.G) ? __ldcg(&pml0[(lane * 8 + hh) * 2]) : -INFINITY;
-            lj[hh] = (lane < np && hh < p.G) ? __ldcg(&pml0[(lane * 8 + hh) * 2 + 1]) : 0.f;
-        }
-#pragma unroll
-        for (int hh = 0; hh < 8; ++hh) {
-            float M = mj[hh];
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-            const float scj = (lane < np && M != -INFINITY) ? fast_exp2(mj[hh] - M) : 0.f;
-            float l = scj * lj[hh];
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
-            s_scale[warp][lane][hh] = scj;
-            Mh[hh] = M;
-            lh[hh] = l;
-        }
-        __syncwarp();
-        float4 acc[8];
-#pragma unroll
-        for (int hh = 0; hh < 8; ++hh) acc[hh] = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 2
-        for (int jj = 0; jj < np; ++jj) {
-#pragma unroll
-            for (int hh = 0; hh < 8; ++hh) {
-                if (hh < p.G) {
-                    const float sc = s_scale[warp][jj][hh];
-                    const float4 x = __ldcg(reinterpret_cast<const float4*>(po0 + (jj * 8 + hh) * kHeadDim) + lane);
-                    acc[hh].x += sc * x.x; acc[hh].y += sc * x.y; acc[hh].z += sc * x.z; acc[hh].w += sc * x.w;
-                }
-            }
-        }
-#pragma unroll
-        for (int hh = 0; hh < 8; ++hh) {
-            if (hh < p.G) {
-                const float il = lh[hh] > 0.f ? 1.f / lh[hh] : 0.f;
-                const int64_t oh = (int64_t)bi * p.Hq + (int64_t)h * p.G + hh;
-                reinterpret_cast<float4*>(out + oh * kHeadDim)[lane] =
-                    make_float4(acc[hh].x * il, acc[hh].y * il, acc[hh].z * il, acc[hh].w * il);
-                if (out_lse && lane == 0) out_lse[oh] = lh[hh] > 0.f ? (Mh[hh] + log2f(lh[hh])) * kLn2 : -INFINITY;
-            }
-        }
-        if (lane == 0) ab.ctr[rs] = 0u;
-        ATTN_STAMP(5);
     };
 
     int seg_left = 0;                                       // tiles left in the current segment
@@ -466,6 +406,50 @@ __global__ void __launch_bounds__(WARPS * 32, 1) attn_kernel(StepParams p, AttnB
     ATTN_STAMP(6);
 }
 
+
+// (a6) grid (S), 32*G threads: warp hh merges query head hh of segment s; lane jj holds piece
+// jj's (m, l); lane owns dims 4 lane .. 4 lane + 3 and sums the pieces with independent loads.
+__global__ void __launch_bounds__(256) merge_kernel(StepParams p, AttnBufs ab, Work wk, float* __restrict__ out,
+                                                    float* __restrict__ out_lse) {
+    const int cs = blockIdx.x;
+    const int lane = threadIdx.x & 31, hh = threadIdx.x >> 5;
+    const int s0 = cs * wk.TS;
+    const int fw = worker_of(s0, wk), lw = worker_of(s0 + wk.TS - 1, wk);
+    const int np = lw - fw + 1;
+    griddep_wait();                               // partials come from attn_kernel
+    if (np == 1) return;                          // finalised by its only worker
+    const int bi = cs / p.Hkv, h = cs - bi * p.Hkv;
+    const int64_t rs = (int64_t)p.req[bi] * p.Hkv + h;
+    const float* po0 = ab.part_o + (rs * kMaxPieces * 8) * (int64_t)kHeadDim;
+    const float* pml0 = ab.part_ml + (rs * kMaxPieces * 8) * 2;
+    // every load of the segment up front (one memory round trip): the np <= 32 partial rows of
+    // this head and this lane's piece statistics
+    const float4* src = reinterpret_cast<const float4*>(po0 + hh * kHeadDim) + lane;
+    float4 x[kMaxPieces];
+#pragma unroll
+    for (int u = 0; u < kMaxPieces; ++u)
+        x[u] = u < np ? __ldcg(src + u * 8 * (kHeadDim / 4)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float mj = lane < np ? __ldcg(&pml0[(lane * 8 + hh) * 2]) : -INFINITY;
+    const float lj = lane < np ? __ldcg(&pml0[(lane * 8 + hh) * 2 + 1]) : 0.f;
+    float M = mj;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+    const float scj = (lane < np && M != -INFINITY) ? fast_exp2(mj - M) : 0.f;
+    float l = scj * lj;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int u = 0; u < kMaxPieces; ++u) {
+        const float sc = __shfl_sync(0xffffffffu, scj, u);   // 0 for u >= np
+        acc.x += sc * x[u].x; acc.y += sc * x[u].y; acc.z += sc * x[u].z; acc.w += sc * x[u].w;
+    }
+    const float il = l > 0.f ? 1.f / l : 0.f;
+    const int64_t oh = (int64_t)bi * p.Hq + (int64_t)h * p.G + hh;
+    reinterpret_cast<float4*>(out + oh * kHeadDim)[lane] = make_float4(acc.x * il, acc.y * il, acc.z * il, acc.w * il);
+    if (out_lse && lane == 0) out_lse[oh] = l > 0.f ? (M + log2f(l)) * 0.69314718055994531f : -INFINITY;
+}
+
 template <int STAGES, int WARPS>
 static cudaError_t launch_attn_s(kvd_cache* c, const StepParams& p, const uint16_t* q, const int32_t* attn, float* out,
                                  float* out_lse, cudaStream_t s) {
@@ -505,11 +489,20 @@ static cudaError_t launch_attn_s(kvd_cache* c, const StepParams& p, const uint16
     }
     wk.trace = trace ? tbuf : nullptr;
     if (trace) cudaMemsetAsync(tbuf, 0, sizeof(unsigned long long) * 8 * 8192, s);
-    AttnBufs ab{c->slots, c->ntok_dev, c->zero_rec, c->part_o, c->part_ml, c->split_ctr};
+    AttnBufs ab{c->slots, c->ntok_dev, c->zero_rec, c->part_o, c->part_ml};
     const unsigned grid = (unsigned)((wk.NW + WARPS - 1) / WARPS);
     cudaError_t e = launch_pdl(attn_kernel<STAGES, WARPS>, dim3(grid), dim3(WARPS * 32), smem, s, p, ab, wk, q, attn, out,
                                out_lse);
     if (e != cudaSuccess) return e;
+    bool split = false;                           // some segment spans more than one worker
+    for (int sg = 0; sg < S && !split; ++sg) {
+        const int64_t a = (int64_t)sg * wk.TS, b = a + wk.TS - 1;
+        split = ((a + 1) * wk.NW - 1) / wk.T != ((b + 1) * wk.NW - 1) / wk.T;
+    }
+    if (split) {
+        e = launch_pdl(merge_kernel, dim3(S), dim3(32 * p.G), 0, s, p, ab, wk, out, out_lse);
+        if (e != cudaSuccess) return e;
+    }
     if (trace) {   // experiments only: synchronous dump of per-warp phase times (us from first stamp)
         cudaStreamSynchronize(s);
         std::vector<unsigned long long> h((size_t)wk.NW * 8);

@@ -4,36 +4,44 @@
 // block's score is the dot product of the KV head's group query with the
 // block's mean-key summary, computed as one fp32 FMA chain
 // over the 128 dims in order (DESIGN.md §3 R3, R5) so that ids are bit-exact.
-// HBM-bound: 256 B of summary per block.  The summaries are dim-major, so a
-// thread owning V consecutive blocks reads one V*2-byte vector per dim row and
-// a warp reads 64*V contiguous bytes per row (coalesced).  No shared-memory
-// staging: each thread keeps 16-32 rows of its blocks in flight (two ping-pong
-// register batches) and runs V independent chains.  V in {2, 4, 8} is picked so the
-// grid has >= 2 CTAs per SM.  Rows for the first batch are requested before
-// griddepcontrol.wait (summaries are immutable during a step), overlapping
-// the previous kernel's tail.
+// HBM-bound: 256 B of summary per block.  score_kernel is a pure streaming
+// kernel: the summaries are dim-major, so a thread owning V consecutive blocks
+// reads one V*2-byte vector per dim row and a warp reads 64*V contiguous bytes
+// per row (coalesced).  No shared-memory staging: each thread keeps 2R rows of
+// its blocks in flight (two ping-pong register batches) and runs V independent
+// chains.  Small CTAs (256 threads x V = 2 blocks, up to 4 per SM) keep the
+// wave tail short.  Rows of the first batch are requested before
+// griddepcontrol.wait (summaries are immutable during a step), overlapping the
+// previous kernel's tail.  Scores go to HBM/L2 as fp32 (4 B per 256 B read).
 //
-// (a2) "retrieving only the Top-K important chunks", fused:
-// the last scoring CTA of a segment to finish (arrival counter per segment)
-// selects that segment's top-k while other CTAs keep streaming summaries.
-// Thread t owns the contiguous blocks [t*KPT*reps, (t+1)*KPT*reps) (keys in
-// registers when reps == 1).  A 3-pass radix select (11 + 11 + 10 bits,
-// warp-aggregated shared histograms) finds the k-th largest monotone key T
-// among the candidates; keys > T are taken and the kk lowest-id keys == T
-// (R10).  Two block scans give tie ranks and output positions, so ids come out
+// (a2) "retrieving only the Top-K important chunks": topk_kernel,
+// launched behind score_kernel (PDL), runs one thread-block cluster of CL CTAs x
+// 1024 threads per segment (CL = 1 up to 16,384 blocks, 4 at 65,536).  Each CTA
+// stages its span of keys in shared memory.  Radix select over monotone
+// 32-bit keys (R10), 8-bit digits starting at the highest bit where the
+// candidates differ (warp-aggregated shared histogram adds); per-CTA histograms are summed over the cluster
+// through distributed shared memory.  The digit loop stops as soon as the
+// threshold bin is taken whole, holds <= 32 keys (ranked directly: key desc, id
+// asc), or is a single key value (equal keys: lowest ids first).  After the first
+// digit the threshold bin's members are compacted, so later digits touch only
+// them.  Emission: warps own contiguous position ranges, per-warp counts get
+// cluster-wide offsets, and ballots place each taken id, so ids come out
 // ascending with no sort.
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
 
-#include "common.cuh"
-#include "internal.h"
+#include "resolve.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace kvd {
 
 constexpr int kScoreThreads = 256;
-constexpr int64_t kDirectTopkMax = 16384;     // segments up to this many blocks: direct top-k
+constexpr int kTieList = 32;                  // threshold bins up to this size are ranked directly
 
 template <int V>
 struct VecOf;
@@ -47,26 +55,30 @@ struct VecOf<4> {
     using T = uint2;
     static __device__ __forceinline__ uint32_t word(const T& x, int i) { return i ? x.y : x.x; }
 };
-template <>
-struct VecOf<8> {
-    using T = uint4;
-    static __device__ __forceinline__ uint32_t word(const T& x, int i) {
-        return i == 0 ? x.x : i == 1 ? x.y : i == 2 ? x.z : x.w;
-    }
-};
 
+// grid (tiles, Hkv, B); CTA = kScoreThreads threads scoring kScoreThreads*V blocks of one segment.
 template <int V>
-__device__ __forceinline__ void score_tile(const StepParams& p, int bi, int h, int64_t nb, int64_t seg,
-                                           const uint16_t* __restrict__ q, const uint16_t* __restrict__ summ,
-                                           float* __restrict__ scores, float* qbar, float (&acc)[V]) {
+__global__ void __launch_bounds__(kScoreThreads, 4) score_kernel(StepParams p, const uint16_t* __restrict__ q,
+                                                                 const uint16_t* __restrict__ summ,
+                                                                 float* __restrict__ scores,
+                                                                 const int32_t* __restrict__ ntok) {
     using Vec = typename VecOf<V>::T;
+    __shared__ float qbar[kHeadDim];
+    const int bi = blockIdx.z, h = blockIdx.y;
+    const int r = p.req[bi];
+    const int64_t nb = (ntok[r] + p.P - 1) / p.P;   // ntok is written only by kvd_load_prefix (setup)
     const int64_t b0 = (int64_t)blockIdx.x * kScoreThreads * V + (int64_t)threadIdx.x * V;
+    if ((int64_t)blockIdx.x * kScoreThreads * V >= nb) {
+        griddep_launch();
+        return;                                   // whole CTA past this request's end
+    }
+    const int64_t seg = ((int64_t)p.layer * p.R + r) * p.Hkv + h;
     const bool ld = b0 < nb;                      // V-groups never straddle nb_pad (V | 128)
     const Vec* base = reinterpret_cast<const Vec*>(summ + seg * kHeadDim * p.nb_pad + (ld ? b0 : 0));
     const int64_t rstride = p.nb_pad / V;         // Vec elements per dim row
     // two register batches of R rows (ping-pong): while one batch is consumed the
     // other is in flight, so 2R rows of this thread's blocks are always requested
-    constexpr int R = V == 8 ? 8 : 16;
+    constexpr int R = V == 2 ? 16 : 8;
     Vec bufA[R], bufB[R];
 #pragma unroll
     for (int u = 0; u < R; ++u)
@@ -83,6 +95,7 @@ __device__ __forceinline__ void score_tile(const StepParams& p, int bi, int h, i
         qbar[threadIdx.x] = a;
     }
     __syncthreads();
+    float acc[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) acc[v] = 0.0f;
     auto consume = [&](const Vec (&buf)[R], int j0) {
@@ -122,413 +135,577 @@ __device__ __forceinline__ void score_tile(const StepParams& p, int bi, int h, i
     }
 }
 
-struct TopkSmem {
-    int hist[2048];
-    int scan[33];
-    uint32_t wmin[32], wmax[32];
-    uint32_t digit;
-    int above;
+// ------------------------------------------------------------------ (a2) top-k
+constexpr int kListCap = 4096;                // compacted threshold-bin members per CTA
+
+struct TopkShared {
+    int hist[2][256];                 // per-pass digit histograms (double-buffered: read remotely)
+    int tot[256];                     // cluster-summed histogram
+    int wcnt[2][32];                  // per-warp counts of the emission pre-pass (above, bin)
+    int woff[2][32];                  // their cluster-wide exclusive offsets
+    uint32_t wred[2][32];
+    uint32_t cmin[2], cmax[2];        // this CTA's key ranges: candidates, threshold-bin members (read remotely)
+    int mm_slot;                      // next cmin/cmax slot
+    int digit, above, cnt;            // pass decision (broadcast)
+    int ctot[2];                      // CTA totals of the emission counts (read remotely)
+    int ncomp;                        // compacted members of the first threshold bin (this CTA)
+    int lcount;                       // threshold-bin members of this CTA (LIST mode)
+    uint32_t lkey[kTieList];
+    int32_t lid[kTieList];
 };
 
-// CTA-wide top-k (blockDim.x threads, all call it).  Thread t owns `reps` chunks of KPT
-// consecutive positions; positions ascend with (t, chunk, i), so emission order is
-// ascending position.  load(c, key[KPT], &cm) fills chunk c's monotone keys and
-// candidate mask; emit(pos, c, i) writes output slot pos for element (c, i) of this
-// thread.  Selects the k largest keys among candidates, ties to the lowest position
-// (R10); k must not exceed the candidate count.  3-pass radix select (11 + 11 + 10
-// bits) with warp-aggregated shared histograms, then two block scans.
-template <int KPT, class Load, class Emit>
-__device__ void cta_topk(int k, int reps, Load load, Emit emit, TopkSmem& sm,
-                         unsigned long long* ph = nullptr) {
-    const int tid = threadIdx.x, nthr = blockDim.x;
-    auto phs = [&](int i) {
-        if (ph && tid == 0) {
-            unsigned long long t;
-            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-            ph[i] = t;
-        }
-    };
-    uint32_t key[KPT];
-    uint32_t cm = 0;
-    if (reps == 1) load(0, key, cm);
-    phs(0);
-    // ---- key range of the candidates: the digits start at the highest bit where the
-    // candidate keys differ (bits above it are common), so the first histogram is not
-    // concentrated in one bin and plain shared atomics suffice
-    uint32_t kmin = 0xFFFFFFFFu, kmax = 0u;
-#pragma unroll 1
-    for (int c = 0; c < reps; ++c) {
-        if (reps > 1) load(c, key, cm);
-#pragma unroll
-        for (int i = 0; i < KPT; ++i)
-            if ((cm >> i) & 1u) {
-                kmin = min(kmin, key[i]);
-                kmax = max(kmax, key[i]);
-            }
-    }
-    kmin = __reduce_min_sync(0xffffffffu, kmin);
-    kmax = __reduce_max_sync(0xffffffffu, kmax);
-    if ((tid & 31) == 0) {
-        sm.wmin[tid >> 5] = kmin;
-        sm.wmax[tid >> 5] = kmax;
+template <int CL>
+__device__ __forceinline__ void cl_sync() {
+    if constexpr (CL == 1) __syncthreads();
+    else cg::this_cluster().sync();
+}
+template <int CL, class T>
+__device__ __forceinline__ T* cl_remote(T* p, int rank) {
+    if constexpr (CL == 1) return p;
+    else return cg::this_cluster().map_shared_rank(p, rank);
+}
+
+enum { kModeWhole = 0, kModeList = 1, kModeEqual = 2 };
+
+// inverse of score_key32 for non-NaN keys (key 0 = NaN -> -inf here)
+__device__ __forceinline__ float key_to_score(uint32_t key) {
+    if (key == 0u) return -INFINITY;
+    return __uint_as_float((key >> 31) ? (key & 0x7FFFFFFFu) : ~key);
+}
+
+// cluster-wide min / max of (kmn, kmx); every thread returns the cluster values
+template <int CL>
+__device__ __forceinline__ void cta_minmax(uint32_t& kmn, uint32_t& kmx, TopkShared& sm) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    kmn = __reduce_min_sync(0xffffffffu, kmn);
+    kmx = __reduce_max_sync(0xffffffffu, kmx);
+    if (lane == 0) {
+        sm.wred[0][warp] = kmn;
+        sm.wred[1][warp] = kmx;
     }
     __syncthreads();
-    kmin = 0xFFFFFFFFu;
-    kmax = 0u;
-    for (int w = 0; w < (nthr >> 5); ++w) {
-        kmin = min(kmin, sm.wmin[w]);
-        kmax = max(kmax, sm.wmax[w]);
+    if (warp == 0) {
+        const bool v = lane < (int)(blockDim.x >> 5);
+        const uint32_t a = __reduce_min_sync(0xffffffffu, v ? sm.wred[0][lane] : 0xFFFFFFFFu);
+        const uint32_t b = __reduce_max_sync(0xffffffffu, v ? sm.wred[1][lane] : 0u);
+        if (lane == 0) {
+            sm.cmin[sm.mm_slot] = a;
+            sm.cmax[sm.mm_slot] = b;
+        }
     }
-    const uint32_t diff = kmin ^ kmax;
-    int lo = diff ? 32 - __clz(diff) : 0;         // bits [0, lo) still to resolve
-    uint32_t mask = lo == 32 ? 0u : ~((1u << lo) - 1u);
-    uint32_t prefix = kmin & mask;
-    int kk = k;
-    phs(0);
-#pragma unroll 1
-    for (int pass = 0; lo > 0; ++pass) {
-        const int width = min(11, lo);
-        const int shift = lo - width;
-        const int nbins = 1 << width;
-        for (int i = tid; i < nbins; i += nthr) sm.hist[i] = 0;
-        __syncthreads();
-#pragma unroll 1
-        for (int c = 0; c < reps; ++c) {
-            if (reps > 1) load(c, key, cm);
+    cl_sync<CL>();
+    const int slot = sm.mm_slot;
+    kmn = 0xFFFFFFFFu;
+    kmx = 0u;
 #pragma unroll
-            for (int i = 0; i < KPT; ++i)
-                if (((cm >> i) & 1u) && (key[i] & mask) == prefix)
-                    atomicAdd(&sm.hist[(key[i] >> shift) & (uint32_t)(nbins - 1)], 1);
-        }
-        __syncthreads();
-        // bins in descending order; thread t owns bins [nbins - (t+1) bpt, nbins - t bpt)
-        const int bpt = (nbins + nthr - 1) / nthr;
-        int cnt = 0;
-        for (int i = 0; i < bpt; ++i) {
-            const int d = nbins - 1 - (tid * bpt + i);
-            if (d >= 0) cnt += sm.hist[d];
-        }
-        int tot;
-        int above = block_exclusive_scan(cnt, sm.scan, &tot);
-        if (above < kk && kk <= above + cnt) {
-            for (int i = 0; i < bpt; ++i) {
-                const int d = nbins - 1 - (tid * bpt + i);
-                const int ci = d >= 0 ? sm.hist[d] : 0;
-                if (above + ci >= kk) {
-                    sm.digit = (uint32_t)d;
-                    sm.above = above;
-                    break;
-                }
-                above += ci;
+    for (int c = 0; c < CL; ++c) {
+        kmn = min(kmn, cl_remote<CL>(sm.cmin, c)[slot]);
+        kmx = max(kmx, cl_remote<CL>(sm.cmax, c)[slot]);
+    }
+    __syncthreads();                              // everyone read mm_slot before it advances
+    if (threadIdx.x == 0) sm.mm_slot = slot + 1;
+    __syncthreads();
+}
+
+// warp 0: find the bin (descending) holding the kk-th largest member; lane l owns bins
+// d = nbins-1-(8l+j), j < 8.  Writes sm.digit / sm.above (members in higher bins) / sm.cnt.
+__device__ __forceinline__ void pick_digit(TopkShared& sm, int nbins, int kk, int lane) {
+    int c8[8], t = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const int d = nbins - 1 - (8 * lane + j);
+        c8[j] = d >= 0 ? sm.tot[d] : 0;
+        t += c8[j];
+    }
+    int incl = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    int above = incl - t;
+    if (above < kk && kk <= incl) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            if (above + c8[j] >= kk) {
+                sm.digit = nbins - 1 - (8 * lane + j);
+                sm.above = above;
+                sm.cnt = c8[j];
+                break;
             }
-        }
-        __syncthreads();
-        prefix |= sm.digit << shift;
-        mask |= (uint32_t)(nbins - 1) << shift;
-        kk -= sm.above;
-        lo = shift;
-        __syncthreads();
-        phs(1 + min(pass, 2));
-    }
-    const uint32_t T = prefix;                    // take keys > T, and the kk lowest-position keys == T
-    int ngt = 0, neq = 0;
-#pragma unroll 1
-    for (int c = 0; c < reps; ++c) {
-        if (reps > 1) load(c, key, cm);
-#pragma unroll
-        for (int i = 0; i < KPT; ++i) {
-            const bool cand = (cm >> i) & 1u;
-            ngt += (cand && key[i] > T) ? 1 : 0;
-            neq += (cand && key[i] == T) ? 1 : 0;
-        }
-    }
-    int tot;
-    const int tie0 = block_exclusive_scan(neq, sm.scan, &tot);
-    const int ntake = min(max(kk - tie0, 0), neq);
-    int pos = block_exclusive_scan(ngt + ntake, sm.scan, &tot);
-    phs(4);
-    int tie = tie0;
-#pragma unroll 1
-    for (int c = 0; c < reps; ++c) {
-        if (reps > 1) load(c, key, cm);
-#pragma unroll
-        for (int i = 0; i < KPT; ++i) {
-            if (!((cm >> i) & 1u)) continue;
-            bool take = key[i] > T;
-            if (key[i] == T) take = tie++ < kk;
-            if (take) emit(pos++, c, i);
+            above += c8[j];
         }
     }
 }
 
-// Two-level top-k (a2).  Every scoring CTA first keeps its tile's local top-k
-// candidates (the k largest (key, -id) pairs of its V*256 blocks, or all of them):
-// the segment's top-k is a subset of the union of the tiles' local top-k, so the
-// final selection only ranks ntiles*k candidates.  Candidates are stored per tile
-// in ascending id order, so the concatenation over tiles is ascending too.  The
-// last CTA of the segment to finish (arrival counter) runs the final selection.
-struct SelBufs {
-    unsigned long long* trace;   // KVD_SEL_TRACE: per-CTA globaltimer stamps [ctas][4] (experiments only)
-    uint32_t* cand_key;     // [R][Hkv][max_tiles][kmax]
-    int32_t* cand_id;       // [R][Hkv][max_tiles][kmax]
-    int32_t* cand_cnt;      // [R][Hkv][max_tiles]
-    uint32_t* ctr;          // [R][Hkv]
-    int32_t max_tiles, kmax;
+// grid (CL, Hkv, B), cluster (CL, 1, 1), NT threads.  CTA rank c owns blocks
+// [c*span, (c+1)*span), span = NT*kpt, staged as monotone keys in shared memory.
+// Candidates = [sink_end, local_begin) (not pinned, < nb).  Every phase walks the keys in
+// 32-wide strips (conflict-free shared loads); warp w owns the contiguous strip range
+// [w*span/32, (w+1)*span/32) for the ordered emission.
+// Fused variant (RESOLVE): after the selection, CTA rank 0 resolves the segment against the
+// cache (a3, resolve.cuh) and copies its misses from the host store (a4) in the same CTA,
+// reusing the dynamic shared memory: select -> resolve -> fetch without kernel boundaries.
+struct FuseArgs {
+    ResolveBufs rb;
+    int32_t* out_attn;
+    const uint8_t* host_store;    // NULL: fully resident (no misses)
+    uint8_t* slots;
 };
 
-// grid (tiles per segment, Hkv, B); CTA = kScoreThreads threads scoring kScoreThreads*V blocks.
-// TWO = two-level selection (tile-local candidates first; used when nb > 16384) or the
-// direct selection over all of the segment's scores by the last CTA.
-template <int V, int KPT, bool TWO>
-__global__ void __launch_bounds__(kScoreThreads, 2) select_kernel(StepParams p, const uint16_t* __restrict__ q,
-                                                                  const uint16_t* __restrict__ summ,
-                                                                  float* __restrict__ scores,
-                                                                  const int32_t* __restrict__ ntok, SelBufs sb,
-                                                                  int reps, int32_t* __restrict__ out_ids,
-                                                                  float* __restrict__ out_scores) {
-    __shared__ float qbar[kHeadDim];
-    __shared__ TopkSmem sm;
-    __shared__ int s_last, s_off[kMaxSelTiles + 1];
-    const int bi = blockIdx.z, h = blockIdx.y, tile = blockIdx.x;
+template <int CL, int NT, bool RESOLVE>
+__global__ void __launch_bounds__(NT, 1) topk_kernel(FuseArgs fa, StepParams p, const float* __restrict__ scores,
+                                                               const int32_t* __restrict__ ntok, int kpt,
+                                                               int32_t* __restrict__ out_ids,
+                                                               float* __restrict__ out_scores,
+                                                               unsigned long long* __restrict__ trace) {
+    extern __shared__ __align__(16) uint32_t skey[];   // [span] keys | [kListCap] compacted (key, index) pairs
+    __shared__ TopkShared sm;
+    const int crank = CL > 1 ? (int)cg::this_cluster().block_rank() : 0;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int h = blockIdx.y, bi = blockIdx.z;
     const int r = p.req[bi];
-    const int n = ntok[r];                        // written only by kvd_load_prefix (setup)
-    const int64_t nb = (n + p.P - 1) / p.P;
-    const int64_t bpc = (int64_t)kScoreThreads * V;
-    if ((int64_t)tile * bpc >= nb) return;        // whole CTA past this request's end (does not arrive)
+    const int span = NT * kpt;
+    uint2* comp = reinterpret_cast<uint2*>(skey + span);
+    uint8_t* sbin = reinterpret_cast<uint8_t*>(comp + kListCap);   // first-digit bin of every key
+    const int64_t base = (int64_t)crank * span;
+    const SegGeom g = seg_geom(ntok[r], p.P, p.sink_tokens, p.local_tokens);
     const int64_t seg = ((int64_t)p.layer * p.R + r) * p.Hkv + h;
-    float acc[V];
-    const int64_t cta_lin = ((int64_t)bi * p.Hkv + h) * gridDim.x + tile;
-    auto stamp = [&](int i) {
-        if (sb.trace && threadIdx.x == 0) {
+    auto clampi = [](int64_t x, int64_t lo_, int64_t hi_) { return (int)(x < lo_ ? lo_ : x > hi_ ? hi_ : x); };
+    const int lim = clampi(p.nb_pad - base, 0, span);
+    const int c_lo = clampi(g.sink_end - base, 0, lim);
+    const int c_hi = clampi(g.local_begin - base, 0, lim);
+    const int ncand = g.local_begin - g.sink_end;
+    const float* sc = scores + seg * p.nb_pad + base;
+    unsigned long long* tr = trace ? trace + ((((int64_t)blockIdx.z * gridDim.y + blockIdx.y) * CL + crank) * 8) : nullptr;
+    auto stamp = [&](int i, unsigned long long v = 0) {   // KVD_TOPK_TRACE (experiments only)
+        if (tr && tid == 0) {
             unsigned long long t;
             asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-            sb.trace[cta_lin * 4 + i] = t;
+            tr[i] = v ? v : t;
         }
     };
     stamp(0);
-    score_tile<V>(p, bi, h, nb, seg, q, summ, scores, qbar, acc);
+    __shared__ ResolveShared rsm;
+    if (RESOLVE && crank == 0) resolve_pre(p, fa.rb, bi, h, rsm);
+    if (tid == 0) {
+        sm.lcount = 0;
+        sm.ncomp = 0;
+        sm.mm_slot = 0;
+    }
+    griddep_wait();                               // scores come from score_kernel
     stamp(1);
-    if (p.k == 0) return;
-    const SegGeom g = seg_geom(n, p.P, p.sink_tokens, p.local_tokens);
-    const int64_t rs = (int64_t)r * p.Hkv + h;
-    const int64_t b0 = (int64_t)tile * bpc + (int64_t)threadIdx.x * V;
-
-    if (TWO) {
-    // ---- tile-local candidates
-    uint32_t lkey[V];
-    uint32_t lcm = 0;
+    // ---- stage keys; candidate key range (NaN keys are 0; every other key is >= 1)
+    uint32_t kmn = 0xFFFFFFFFu, kmx = 0u;
+    for (int i = tid * 4; i < lim; i += NT * 4) {
+        const float4 x = __ldcg(reinterpret_cast<const float4*>(sc + i));
+        const uint32_t k4[4] = {score_key32(x.x), score_key32(x.y), score_key32(x.z), score_key32(x.w)};
+        *reinterpret_cast<uint4*>(&skey[i]) = make_uint4(k4[0], k4[1], k4[2], k4[3]);
 #pragma unroll
-    for (int v = 0; v < V; ++v) {
-        const int64_t b = b0 + v;
-        lkey[v] = score_key32(acc[v]);
-        lcm |= (uint32_t)(b < g.nb && b >= g.sink_end && b < g.local_begin) << v;
-    }
-    int tot;
-    const int cpos = block_exclusive_scan(__popc(lcm), sm.scan, &tot);   // candidates of the tile
-    const int kl = min(p.k, tot);
-    uint32_t* ck = sb.cand_key + (rs * sb.max_tiles + tile) * sb.kmax;
-    int32_t* ci = sb.cand_id + (rs * sb.max_tiles + tile) * sb.kmax;
-    if (tot <= p.k) {                             // every candidate of the tile survives
-        int pos = cpos;
-#pragma unroll
-        for (int v = 0; v < V; ++v)
-            if ((lcm >> v) & 1u) {
-                ck[pos] = lkey[v];
-                ci[pos] = (int32_t)(b0 + v);
-                ++pos;
+        for (int u = 0; u < 4; ++u)
+            if (i + u >= c_lo && i + u < c_hi && k4[u] != 0u) {
+                kmn = min(kmn, k4[u]);
+                kmx = max(kmx, k4[u]);
             }
-    } else {
-        cta_topk<V>(
-            kl, 1,
-            [&](int, uint32_t (&key)[V], uint32_t& cm) {
+    }
+    cta_minmax<CL>(kmn, kmx, sm);
+    stamp(2);
+    // ---- first digit: 256 bins linear in the score value over [vmin, vmax] (monotone: fp32
+    // subtract, multiply by a positive scale and truncate never invert an order; equal scores
+    // share a bin; NaN -> bin 0).  Float keys crowd a few leading bits, linear bins do not,
+    // so plain shared atomics suffice.  Skipped (single "bin") for non-finite or equal ends.
+    int kk = p.k, cnt = ncand;                    // still to take / members of the threshold bin
+    const float vmin = key_to_score(kmn), vmax = key_to_score(kmx);
+    const bool lin = kmn <= kmx && isfinite(vmin) && isfinite(vmax) && vmax > vmin && isfinite(vmax - vmin) &&
+                     kk != cnt && cnt > kTieList;
+    const float scale = lin ? 256.0f / (vmax - vmin) : 0.f;
+    auto bin_of = [&](uint32_t key) {
+        if (!lin || key == 0u) return 0;
+        const int b = (int)((key_to_score(key) - vmin) * scale);
+        return b > 255 ? 255 : b;
+    };
+    auto bin_at = [&](int i) { return lin ? (int)sbin[i] : 0; };   // i in [c_lo, c_hi)
+    int bstar = 0;
+    if (lin) {
+        int* hb = sm.hist[1];
+        if (tid < 256) hb[tid] = 0;
+        __syncthreads();
+        for (int i = c_lo + tid; i < c_hi; i += NT) {
+            const int b = bin_of(skey[i]);
+            sbin[i] = (uint8_t)b;
+            atomicAdd(&hb[b], 1);
+        }
+        cl_sync<CL>();
+        if (tid < 256) {
+            int t = 0;
 #pragma unroll
-                for (int v = 0; v < V; ++v) key[v] = lkey[v];
-                cm = lcm;
-            },
-            [&](int pos, int, int v) {
-                ck[pos] = lkey[v];
-                ci[pos] = (int32_t)(b0 + v);
-            },
-            sm);
+            for (int c = 0; c < CL; ++c) t += cl_remote<CL>(hb, c)[tid];
+            sm.tot[tid] = t;
+        }
+        __syncthreads();
+        if (warp == 0) pick_digit(sm, 256, kk, lane);
+        __syncthreads();
+        bstar = sm.digit;
+        kk -= sm.above;
+        cnt = sm.cnt;
     }
-    if (threadIdx.x == 0) sb.cand_cnt[rs * sb.max_tiles + tile] = kl;
+    // ---- threshold-bin members: compact them (when they fit) and take their key range
+    bool compacted = false;
+    kmn = 0xFFFFFFFFu;
+    kmx = 0u;
+    if (kk != cnt && cnt > kTieList) {
+        for (int i0 = (c_lo & ~31) + warp * 32; i0 < c_hi; i0 += NT) {
+            const int i = i0 + lane;
+            const uint32_t key = skey[i];
+            const bool in = i >= c_lo && i < c_hi && bin_at(i) == bstar;
+            if (in) {
+                kmn = min(kmn, key);
+                kmx = max(kmx, key);
+            }
+            const uint32_t bal = __ballot_sync(0xffffffffu, in);
+            int wbase = 0;
+            if (lane == 0 && bal) wbase = atomicAdd(&sm.ncomp, __popc(bal));
+            wbase = __shfl_sync(0xffffffffu, wbase, 0);
+            const int slot = wbase + __popc(bal & ((1u << lane) - 1u));
+            if (in && slot < kListCap) comp[slot] = make_uint2(key, (uint32_t)i);
+        }
+        cta_minmax<CL>(kmn, kmx, sm);             // contains the barriers that publish ncomp
+        compacted = sm.ncomp <= kListCap;         // uniform over the CTA
     }
-
-    // ---- the last CTA of the segment to finish runs the final selection
-    const uint32_t ntiles = (uint32_t)((nb + bpc - 1) / bpc);
+    const uint32_t diff = kmn ^ kmx;
+    int lo = (kk != cnt && cnt > kTieList && diff) ? 32 - __clz(diff) : 0;   // bits [0, lo) still to resolve
+    uint32_t mask = lo == 32 ? 0u : ~((1u << lo) - 1u);
+    uint32_t prefix = kmn & mask;
+    if (kk == cnt || cnt <= kTieList) {           // the bin decides by itself: no key digits
+        mask = 0u;
+        prefix = 0u;
+    }
+    int mode;
+    // ---- radix digits of the members' keys, most significant first
+#pragma unroll 1
+    for (int pass = 0;; ++pass) {
+        if (kk == cnt) { mode = kModeWhole; break; }
+        if (cnt <= kTieList) { mode = kModeList; break; }
+        if (lo == 0) { mode = kModeEqual; break; }
+        const int width = min(8, lo), shift = lo - width, nbins = 1 << width;
+        int* hb = sm.hist[pass & 1];
+        if (tid < 256) hb[tid] = 0;
+        __syncthreads();
+        if (compacted) {
+            const int nc = sm.ncomp;
+            for (int j0 = warp * 32; j0 < nc; j0 += NT) {
+                const int j = j0 + lane;
+                const uint32_t key = j < nc ? comp[j].x : 0u;
+                warp_hist_add(hb, (key >> shift) & (uint32_t)(nbins - 1), j < nc && (key & mask) == prefix);
+            }
+        } else {
+            for (int i0 = (c_lo & ~31) + warp * 32; i0 < c_hi; i0 += NT) {
+                const int i = i0 + lane;
+                const uint32_t key = skey[i];
+                warp_hist_add(hb, (key >> shift) & (uint32_t)(nbins - 1),
+                              i >= c_lo && i < c_hi && bin_at(i) == bstar && (key & mask) == prefix);
+            }
+        }
+        cl_sync<CL>();
+        if (tid < nbins) {
+            int t = 0;
+#pragma unroll
+            for (int c = 0; c < CL; ++c) t += cl_remote<CL>(hb, c)[tid];
+            sm.tot[tid] = t;
+        }
+        __syncthreads();
+        if (warp == 0) pick_digit(sm, nbins, kk, lane);
+        __syncthreads();
+        prefix |= (uint32_t)sm.digit << shift;
+        mask |= (uint32_t)(nbins - 1) << shift;
+        kk -= sm.above;
+        cnt = sm.cnt;
+        lo = shift;
+    }
+    stamp(3);
+    // ---- LIST: the <= 32 threshold-bin members of the cluster, ranked by (key desc, id asc)
+    if (mode == kModeList) {
+        auto add = [&](uint32_t key, int i) {
+            const int slot = atomicAdd(&sm.lcount, 1);
+            sm.lkey[slot] = key;
+            sm.lid[slot] = (int32_t)(base + i);
+        };
+        if (compacted) {
+            for (int j = tid; j < sm.ncomp; j += NT)
+                if ((comp[j].x & mask) == prefix) add(comp[j].x, (int)comp[j].y);
+        } else {
+            for (int i = c_lo + tid; i < c_hi; i += NT)
+                if (bin_at(i) == bstar && (skey[i] & mask) == prefix) add(skey[i], i);
+        }
+        cl_sync<CL>();
+    }
+    auto bin_rank = [&](uint32_t key, int32_t id) {   // members beating (key, id)
+        int rank = 0;
+#pragma unroll 1
+        for (int c = 0; c < CL; ++c) {
+            TopkShared* rs = cl_remote<CL>(&sm, c);
+            const int m = rs->lcount;
+            for (int j = 0; j < m; ++j) {
+                const uint32_t kj = rs->lkey[j];
+                rank += (kj > key || (kj == key && rs->lid[j] < id)) ? 1 : 0;
+            }
+        }
+        return rank;
+    };
+    // ---- emission.  Warp w owns positions [w0, w1) and walks them in 32-wide strips: pre-pass
+    // counts (above, bin members), cluster-wide exclusive offsets in position order, then
+    // ballots place every taken id at its ascending output position.
+    const int per_w = span / (NT / 32);
+    const int w0 = max(warp * per_w, c_lo), w1 = min((warp + 1) * per_w, c_hi);
+    auto classify = [&](int i, bool& gt, bool& eq) {   // above the threshold / in it
+        const bool in = i >= w0 && i < w1;
+        const uint32_t key = in ? skey[i] : 0u;
+        const int b = in ? bin_at(i) : 0;
+        gt = in && (b > bstar || (b == bstar && (key & mask) > prefix));
+        eq = in && b == bstar && (key & mask) == prefix;
+    };
+    int cgt = 0, ceq = 0;
+    for (int i0 = warp * per_w; i0 < w1; i0 += 32) {
+        bool gt, eq;
+        classify(i0 + lane, gt, eq);
+        cgt += __popc(__ballot_sync(0xffffffffu, gt));
+        ceq += __popc(__ballot_sync(0xffffffffu, eq));
+    }
+    if (lane == 0) {
+        sm.wcnt[0][warp] = cgt;
+        sm.wcnt[1][warp] = ceq;
+    }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        s_last = atomicAdd(&sb.ctr[rs], 1u) == ntiles - 1;
-        if (s_last) {
-            sb.ctr[rs] = 0u;
-            __threadfence();
+    if (warp < 2) {                               // warp 0: "above" offsets, warp 1: bin offsets
+        const int v = lane < NT / 32 ? sm.wcnt[warp][lane] : 0;
+        int incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        sm.woff[warp][lane] = incl - v;
+        if (lane == 31) sm.ctot[warp] = incl;
+    }
+    cl_sync<CL>();
+    int before_gt = 0, before_eq = 0;
+#pragma unroll
+    for (int c = 0; c < CL; ++c) {
+        if (c < crank) {
+            before_gt += *cl_remote<CL>(&sm.ctot[0], c);
+            before_eq += *cl_remote<CL>(&sm.ctot[1], c);
         }
     }
-    __syncthreads();
-    if (!s_last) return;
-    stamp(2);
+    stamp(4);
+    // position of a taken id: ids above the bin before it + taken bin members before it
+    int gt_before = before_gt + sm.woff[0][warp];     // above-bin keys before this strip
+    int eq_before = before_eq + sm.woff[1][warp];     // bin members before this strip (position order)
+    int taken_eq_before = 0;                          // LIST mode: taken bin members before this strip
+    if (mode == kModeList) {
+        // taken bin members at positions before this warp's range (ids ascend with positions)
+        int t = 0;
+        for (int c = 0; c < CL; ++c) {
+            TopkShared* rs = cl_remote<CL>(&sm, c);
+            for (int j = lane; j < rs->lcount; j += 32) {
+                const int32_t id = rs->lid[j];
+                if (id < base + warp * per_w && bin_rank(rs->lkey[j], id) < kk) ++t;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        taken_eq_before = t;
+    }
     int32_t* ids_out = out_ids + ((int64_t)bi * p.Hkv + h) * p.k;
     float* sc_out = out_scores ? out_scores + ((int64_t)bi * p.Hkv + h) * p.k : nullptr;
-    const float* sc = scores + seg * p.nb_pad;
-    if (!TWO) {
-        // direct: thread t owns blocks [t*KPT*reps, (t+1)*KPT*reps), scores re-read from L2
-        cta_topk<KPT>(
-            p.k, reps,
-            [&](int c, uint32_t (&key)[KPT], uint32_t& cm) {
-                const int64_t bb = ((int64_t)threadIdx.x * reps + c) * KPT;
-                cm = 0;
-                if (bb >= g.nb) return;
-#pragma unroll
-                for (int i = 0; i < KPT; i += 4) {
-                    const float4 x = __ldcg(reinterpret_cast<const float4*>(sc + bb + i));
-                    key[i] = score_key32(x.x); key[i + 1] = score_key32(x.y);
-                    key[i + 2] = score_key32(x.z); key[i + 3] = score_key32(x.w);
-                }
-#pragma unroll
-                for (int i = 0; i < KPT; ++i) {
-                    const int64_t b = bb + i;
-                    cm |= (uint32_t)(b < g.nb && b >= g.sink_end && b < g.local_begin) << i;
-                }
-            },
-            [&](int pos, int c, int i) {
-                const int64_t b = ((int64_t)threadIdx.x * reps + c) * KPT + i;
-                ids_out[pos] = (int32_t)b;
-                if (sc_out) sc_out[pos] = __ldcg(&sc[b]);
-            },
-            sm, sb.trace ? sb.trace + (1 << 18) + cta_lin * 8 : nullptr);
-        stamp(3);
-        return;
-    }
-    // candidate offsets per tile (ntiles <= max_tiles <= 128 per pass of this loop)
-    int total = 0;
-    for (int t0 = 0; t0 < (int)ntiles; t0 += kScoreThreads) {
-        const int t = t0 + (int)threadIdx.x;
-        const int c = t < (int)ntiles ? __ldcg(&sb.cand_cnt[rs * sb.max_tiles + t]) : 0;
-        int tt;
-        const int off = block_exclusive_scan(c, sm.scan, &tt);
-        if (t < (int)ntiles) s_off[t] = total + off;
-        total += tt;
-    }
-    if (threadIdx.x == 0) s_off[ntiles] = total;
-    __syncthreads();
-    const int nt_ = (int)ntiles;
-    // candidate j (concatenated, ascending id) -> (tile, index): tiles hold kl_t <= kmax entries
-    auto cand_at = [&](int j, uint32_t& key, int32_t& id) {
-        int lo = 0, hi = nt_;                     // largest t with s_off[t] <= j
-        while (hi - lo > 1) {
-            const int mid = (lo + hi) >> 1;
-            if (s_off[mid] <= j) lo = mid; else hi = mid;
+    for (int i0 = warp * per_w; i0 < w1; i0 += 32) {
+        const int i = i0 + lane;
+        bool gt, eq;
+        classify(i, gt, eq);
+        const uint32_t bgt = __ballot_sync(0xffffffffu, gt), beq = __ballot_sync(0xffffffffu, eq);
+        const uint32_t lt = (1u << lane) - 1u;
+        bool take_eq = false;
+        if (mode == kModeWhole) take_eq = eq;
+        else if (mode == kModeEqual) take_eq = eq && eq_before + __popc(beq & lt) < kk;
+        else if (eq) take_eq = bin_rank(skey[i], (int32_t)(base + i)) < kk;
+        const uint32_t btk = __ballot_sync(0xffffffffu, take_eq);
+        const int eq_taken_before = mode == kModeWhole ? eq_before
+                                  : mode == kModeEqual ? min(eq_before, kk)
+                                                       : taken_eq_before;
+        if (gt || take_eq) {
+            const int pos = gt_before + eq_taken_before + __popc((bgt | btk) & lt);
+            ids_out[pos] = (int32_t)(base + i);
+            if (sc_out) sc_out[pos] = __ldcg(sc + i);
         }
-        const int64_t base = (rs * sb.max_tiles + lo) * sb.kmax + (j - s_off[lo]);
-        key = __ldcg(&sb.cand_key[base]);
-        id = __ldcg(&sb.cand_id[base]);
-    };
-    const int per = (total + kScoreThreads * reps - 1) / (kScoreThreads * reps);   // <= KPT
-    cta_topk<KPT>(
-        p.k, reps,
-        [&](int c, uint32_t (&key)[KPT], uint32_t& cm) {
-            const int j0 = ((int)threadIdx.x * reps + c) * per;
-            cm = 0;
-#pragma unroll
-            for (int i = 0; i < KPT; ++i) {
-                key[i] = 0u;
-                if (i < per && j0 + i < total) {
-                    int32_t id;
-                    cand_at(j0 + i, key[i], id);
-                    cm |= 1u << i;
-                }
-            }
-        },
-        [&](int pos, int c, int i) {
-            const int j = ((int)threadIdx.x * reps + c) * per + i;
-            uint32_t key;
-            int32_t id;
-            cand_at(j, key, id);
-            ids_out[pos] = id;
-            if (sc_out) sc_out[pos] = __ldcg(&sc[id]);
-        },
-        sm);
+        gt_before += __popc(bgt);
+        eq_before += __popc(beq);
+        taken_eq_before += __popc(btk);
+    }
+    stamp(5);
+    stamp(6, 1000ull * mode + (32 - lo) + (compacted ? 100 : 0));
+    if constexpr (!RESOLVE) {
+        griddep_launch();
+        if (CL > 1) cl_sync<CL>();               // remote readers of this CTA's shared memory are done
+    } else {
+        // every CTA's ids are written (cluster barrier: release / acquire) and no CTA reads
+        // another's shared memory any more; rank 0 resolves and fetches
+        cl_sync<CL>();
+        if (crank != 0) return;
+        uint8_t* smraw = reinterpret_cast<uint8_t*>(skey);
+        const int nm = resolve_main(p, fa.rb, bi, h, out_ids, fa.out_attn, smraw, rsm, true);
+        if (nm > 0 && fa.host_store) {
+            const int32_t* S = reinterpret_cast<const int32_t*>(reinterpret_cast<uint64_t*>(smraw) + fa.rb.nkeys);
+            gather_segment(p, bi, h, S + 2 * fa.rb.kmax, S + 3 * fa.rb.kmax, nm, fa.host_store, fa.slots);
+        }
+    }
 }
 
-template <int V, int KPT, bool TWO>
-static cudaError_t launch_sel(kvd_cache* c, const StepParams& p, const uint16_t* q, int reps, int32_t* out_ids,
-                              float* out_scores, cudaStream_t s) {
+template <int V>
+static cudaError_t launch_score(kvd_cache* c, const StepParams& p, const uint16_t* q, cudaStream_t s) {
     const unsigned tiles = (unsigned)((c->nb_pad + kScoreThreads * V - 1) / (kScoreThreads * V));
+    return launch_pdl(score_kernel<V>, dim3(tiles, p.Hkv, p.B), dim3(kScoreThreads), 0, s, p, q,
+                      (const uint16_t*)c->summ, c->scores, (const int32_t*)c->ntok_dev);
+}
+
+template <int CL, int NT, bool RESOLVE>
+static cudaError_t launch_topk(kvd_cache* c, const StepParams& p, int kpt, int32_t* out_ids, float* out_scores,
+                               const FuseArgs& fa, cudaStream_t s) {
+    size_t smem = (size_t)NT * kpt * 5 + (size_t)kListCap * 8;   // keys | compacted pairs | bins
+    if (RESOLVE) smem = std::max(smem, resolve_smem_bytes(fa.rb.nkeys, c->kmax, c->nb_pad));
+    static size_t smem_set = 0;                   // dynamic + static must fit: always opt in
+    if (smem > smem_set) {
+        cudaError_t e = cudaFuncSetAttribute(topk_kernel<CL, NT, RESOLVE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        smem_set = smem;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CL, p.Hkv, p.B);
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[3];
+    int na = 0;
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na++].val.programmaticStreamSerializationAllowed = 1;
+    if (CL > 1) {
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = CL;
+        attr[na].val.clusterDim.y = 1;
+        attr[na++].val.clusterDim.z = 1;
+    }
+    if (RESOLVE && fa.host_store) {               // the host-link fetch is inside: schedule it first
+        static int prio = 1;
+        if (prio == 1) {
+            int lo = 0, hi = 0;
+            cudaDeviceGetStreamPriorityRange(&lo, &hi);
+            prio = hi;
+        }
+        attr[na].id = cudaLaunchAttributePriority;
+        attr[na++].val.priority = prio;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
     static int trace = -1;
     static unsigned long long* tbuf = nullptr;
     if (trace < 0) {
-        trace = getenv("KVD_SEL_TRACE") ? 1 : 0;
-        if (trace) cudaMalloc(&tbuf, sizeof(unsigned long long) * ((1 << 18) + 8 * (1 << 16)));
+        trace = getenv("KVD_TOPK_TRACE") ? 1 : 0;
+        if (trace) cudaMalloc(&tbuf, sizeof(unsigned long long) * 8 * 65536);
     }
-    const int64_t nctas = (int64_t)tiles * p.Hkv * p.B;
-    if (trace) cudaMemsetAsync(tbuf, 0, sizeof(unsigned long long) * ((1 << 18) + 8 * (1 << 16)), s);
-    SelBufs sb{trace && nctas <= (1 << 16) ? tbuf : nullptr, c->cand_key, c->cand_id, c->cand_cnt, c->sel_ctr, c->max_sel_tiles, c->kmax > 0 ? c->kmax : 1};
-    cudaError_t e = launch_pdl(select_kernel<V, KPT, TWO>, dim3(tiles, p.Hkv, p.B), dim3(kScoreThreads), 0, s, p, q,
-                               (const uint16_t*)c->summ, c->scores, (const int32_t*)c->ntok_dev, sb, reps, out_ids,
-                               out_scores);
-    if (trace && sb.trace) {   // experiments only: synchronous dump of per-CTA phase times
+    const int nctas = CL * p.Hkv * p.B;
+    if (trace) cudaMemsetAsync(tbuf, 0, sizeof(unsigned long long) * 8 * nctas, s);
+    count_launch();
+    cudaError_t e = cudaLaunchKernelEx(&cfg, topk_kernel<CL, NT, RESOLVE>, fa, p, (const float*)c->scores, (const int32_t*)c->ntok_dev,
+                                       kpt, out_ids, out_scores, trace ? tbuf : nullptr);
+    if (trace && e == cudaSuccess) {   // experiments only: synchronous dump of per-CTA phase times
         cudaStreamSynchronize(s);
-        std::vector<unsigned long long> h((size_t)nctas * 4);
+        std::vector<unsigned long long> h((size_t)nctas * 8);
         cudaMemcpy(h.data(), tbuf, h.size() * 8, cudaMemcpyDeviceToHost);
         unsigned long long t0 = ~0ull;
-        for (int64_t i = 0; i < nctas; ++i) if (h[i * 4] && h[i * 4] < t0) t0 = h[i * 4];
-        const char* names[4] = {"entry", "scored", "topk_begin", "topk_end"};
-        for (int j = 0; j < 4; ++j) {
+        for (int i = 0; i < nctas; ++i) t0 = std::min(t0, h[i * 8]);
+        const char* names[6] = {"entry", "griddep", "minmax", "passes", "counted", "end"};
+        for (int j = 0; j < 6; ++j) {
             std::vector<double> v;
-            for (int64_t i = 0; i < nctas; ++i) if (h[i * 4 + j]) v.push_back((h[i * 4 + j] - t0) * 1e-3);
-            if (v.empty()) continue;
+            for (int i = 0; i < nctas; ++i) v.push_back((h[i * 8 + j] - t0) * 1e-3);
             std::sort(v.begin(), v.end());
-            fprintf(stderr, "sel trace V=%d %-10s n=%5zu min %7.2f p50 %7.2f p90 %7.2f max %7.2f us\n", V, names[j],
-                    v.size(), v[0], v[v.size() / 2], v[v.size() * 9 / 10], v.back());
+            fprintf(stderr, "topk trace CL=%d NT=%d kpt=%d %-8s p50 %7.2f max %7.2f us\n", CL, NT, kpt, names[j], v[v.size() / 2], v.back());
         }
-        // top-k phases relative to topk_begin of the same CTA
-        std::vector<unsigned long long> h2((size_t)nctas * 8);
-        cudaMemcpy(h2.data(), tbuf + (1 << 18), h2.size() * 8, cudaMemcpyDeviceToHost);
-        const char* pn[5] = {"loaded", "pass0", "pass1", "pass2", "scans"};
-        for (int j = 0; j < 5; ++j) {
-            std::vector<double> v;
-            for (int64_t i = 0; i < nctas; ++i)
-                if (h2[i * 8 + j] && h[i * 4 + 2]) v.push_back(((double)h2[i * 8 + j] - (double)h[i * 4 + 2]) * 1e-3);
-            if (v.empty()) continue;
-            std::sort(v.begin(), v.end());
-            fprintf(stderr, "sel topk phase %-7s n=%5zu p50 %7.2f max %7.2f us (from topk_begin)\n", pn[j], v.size(),
-                    v[v.size() / 2], v.back());
-        }
+        fprintf(stderr, "topk trace mode*1000+bits: cta0 %llu cta_last %llu\n", h[6], h[(nctas - 1) * 8 + 6]);
     }
     return e;
 }
 
-template <int V>
-static cudaError_t launch_sel_v(kvd_cache* c, const StepParams& p, const uint16_t* q, int32_t* out_ids,
-                                float* out_scores, cudaStream_t s) {
-    if (c->nb_pad <= kDirectTopkMax) {
-        // direct selection over the segment's nb scores: KPT per thread, keys re-read per chunk
-        const int64_t per = (c->nb_pad + kScoreThreads - 1) / kScoreThreads;
-        if (per <= 4) return launch_sel<V, 4, false>(c, p, q, 1, out_ids, out_scores, s);
-        if (per <= 8) return launch_sel<V, 8, false>(c, p, q, 1, out_ids, out_scores, s);
-        if (per <= 16) return launch_sel<V, 16, false>(c, p, q, 1, out_ids, out_scores, s);
-        return launch_sel<V, 32, false>(c, p, q, (int)((per + 31) / 32), out_ids, out_scores, s);
+// Cluster size and keys per thread for a segment span of nb_pad blocks with nt threads per
+// CTA: at most 16 keys per thread while the cluster is small (clusters of whole-SM CTAs do not
+// all fit at once), at most 8 CTAs per cluster (portable), kpt a multiple of 4 (float4 staging).
+void topk_geometry(int64_t nb_pad, int nt, int* cl, int* kpt) {
+    int c = 1;
+    while (c < 8 && (int64_t)c * nt * 16 < nb_pad) c <<= 1;
+    int64_t per = (nb_pad + (int64_t)c * nt - 1) / ((int64_t)c * nt);
+    per = (per + 3) / 4 * 4;
+    *cl = c;
+    *kpt = (int)per;
+}
+
+template <int NT, bool RESOLVE>
+static cudaError_t launch_topk_nt(kvd_cache* c, const StepParams& p, int32_t* out_ids, float* out_scores,
+                                  const FuseArgs& fa, cudaStream_t s) {
+    int cl, kpt;
+    topk_geometry(c->nb_pad, NT, &cl, &kpt);
+    switch (cl) {
+        case 1: return launch_topk<1, NT, RESOLVE>(c, p, kpt, out_ids, out_scores, fa, s);
+        case 2: return launch_topk<2, NT, RESOLVE>(c, p, kpt, out_ids, out_scores, fa, s);
+        case 4: return launch_topk<4, NT, RESOLVE>(c, p, kpt, out_ids, out_scores, fa, s);
+        default: return launch_topk<8, NT, RESOLVE>(c, p, kpt, out_ids, out_scores, fa, s);
     }
-    // two-level: final selection over at most tiles * k candidates
-    const int64_t tiles = (c->nb_pad + kScoreThreads * V - 1) / (kScoreThreads * V);
-    const int64_t cand = std::min<int64_t>(tiles * std::max(p.k, 1), c->nb_pad);
-    const int64_t per = (cand + kScoreThreads - 1) / kScoreThreads;
-    if (per <= 8) return launch_sel<V, 8, true>(c, p, q, 1, out_ids, out_scores, s);
-    if (per <= 16) return launch_sel<V, 16, true>(c, p, q, 1, out_ids, out_scores, s);
-    return launch_sel<V, 16, true>(c, p, q, (int)((per + 15) / 16), out_ids, out_scores, s);
+}
+
+static int topk_threads() {
+    static int nt = 0;
+    if (!nt) {
+        const char* env = getenv("KVD_TOPK_THREADS");   // experiments only: 256, 512 or 1024
+        nt = env ? atoi(env) : 1024;
+        if (nt != 256 && nt != 512) nt = 1024;
+    }
+    return nt;
 }
 
 cudaError_t launch_select(kvd_cache* c, const StepParams& p, const uint16_t* q, int32_t* out_ids, float* out_scores,
                           cudaStream_t s) {
-    // V: largest of 8, 4, 2 blocks per thread that still gives >= 2 CTAs per SM; the
-    // two-level path always takes V = 8 (fewest tiles -> fewest candidates)
-    const int64_t segs = (int64_t)p.B * p.Hkv;
-    auto ctas = [&](int V) { return segs * ((c->nb_pad + kScoreThreads * V - 1) / (kScoreThreads * V)); };
-    cudaError_t e;
-    if (c->nb_pad > kDirectTopkMax || ctas(8) >= 2 * 148) e = launch_sel_v<8>(c, p, q, out_ids, out_scores, s);
-    else if (ctas(4) >= 2 * 148) e = launch_sel_v<4>(c, p, q, out_ids, out_scores, s);
-    else e = launch_sel_v<2>(c, p, q, out_ids, out_scores, s);
+    static int V = 0;
+    if (!V) {
+        const char* env = getenv("KVD_SEL_V");   // experiments only: blocks per scoring thread (2 or 4)
+        V = env && atoi(env) == 4 ? 4 : 2;
+    }
+    cudaError_t e = V == 4 ? launch_score<4>(c, p, q, s) : launch_score<2>(c, p, q, s);
+    if (e != cudaSuccess || p.k == 0) return e != cudaSuccess ? e : cudaGetLastError();
+    const FuseArgs fa{};
+    const int nt = topk_threads();
+    e = nt == 256 ? launch_topk_nt<256, false>(c, p, out_ids, out_scores, fa, s)
+      : nt == 512 ? launch_topk_nt<512, false>(c, p, out_ids, out_scores, fa, s)
+                  : launch_topk_nt<1024, false>(c, p, out_ids, out_scores, fa, s);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
+// kvd_select_resolve_fetch: score_kernel, then the fused top-k + resolve + fetch kernel.
+cudaError_t launch_select_resolve(kvd_cache* c, const StepParams& p, const uint16_t* q, int32_t* out_ids,
+                                  float* out_scores, int32_t* out_attn, cudaStream_t s) {
+    static int V = 0;
+    if (!V) {
+        const char* env = getenv("KVD_SEL_V");
+        V = env && atoi(env) == 4 ? 4 : 2;
+    }
+    cudaError_t e = V == 4 ? launch_score<4>(c, p, q, s) : launch_score<2>(c, p, q, s);
+    if (e != cudaSuccess) return e;
+    if (p.k == 0) return launch_resolve(c, p, out_ids, out_attn, s);   // nothing to select
+    FuseArgs fa;
+    fa.rb = resolve_bufs(c);
+    fa.out_attn = out_attn;
+    fa.host_store = c->resident ? nullptr : c->host_store;
+    fa.slots = c->slots;
+    const int nt = topk_threads();
+    e = nt == 256 ? launch_topk_nt<256, true>(c, p, out_ids, out_scores, fa, s)
+      : nt == 512 ? launch_topk_nt<512, true>(c, p, out_ids, out_scores, fa, s)
+                  : launch_topk_nt<1024, true>(c, p, out_ids, out_scores, fa, s);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }

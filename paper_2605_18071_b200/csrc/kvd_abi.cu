@@ -1,6 +1,7 @@
 // kvd_abi.cu — the C ABI of libkvd.so (include/kvd.h): configuration and
 // allocation, synchronous argument validation, step-call dispatch to the
 // kernels, introspection.  No exception crosses this boundary.
+#include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -72,21 +73,25 @@ kvd_status check_config(const kvd_config* cfg, Geometry* g) {
     g->resident = g->C >= g->nb_max;
     g->kmax = cfg->max_select;
     if (g->kmax > g->nb_max) return fail(KVD_EINVAL, "max_select > blocks per request");
+    if (resolve_smem_bytes(g->resident ? 0 : g->C, g->kmax, g->nb_pad) > kMaxSmemBytes)
+        return fail(KVD_EINVAL, "slots_per_segment=%lld too large for on-chip victim selection (host-backed cache)",
+                    (long long)g->C);
     g->pmax = (cfg->sink_tokens + P - 1) / P + (cfg->local_tokens > 0 ? (cfg->local_tokens + P - 1) / P + 1 : 0);
     g->A = (cfg->host_layer_alias <= 0 || cfg->host_layer_alias > g->L) ? g->L : cfg->host_layer_alias;
     g->rec_bytes = 2ll * P * kRowBytes;
+    if (g->pmax > 256) return fail(KVD_EINVAL, "sink/local tokens pin %d blocks (> 256)", g->pmax);
     const int64_t wmax = g->kmax + g->pmax;
     (void)wmax;
     g->max_splits = kMaxPieces;
     if ((int64_t)g->Hkv * g->nb_max * 4 > kSlotOfBytes) return fail(KVD_EINVAL, "context too long for setup scratch");
-    if (g->nb_pad > (int64_t)kMaxSelTiles * 2048) return fail(KVD_EINVAL, "context too long: > %d blocks", kMaxSelTiles * 2048);
+    if (g->nb_pad > kMaxSelectBlocks) return fail(KVD_EINVAL, "context too long: > %d blocks", kMaxSelectBlocks);
     return KVD_OK;
 }
 
 struct Sizes {
-    size_t slots, summ, scores, table, meta4, meta1, miss, part_o, part_ml, small, host, cand;
+    size_t slots, summ, scores, table, meta4, meta1, miss, part_o, part_ml, small, host;
     size_t dev_total() const {
-        return slots + summ + scores + table + 3 * meta4 + meta1 + miss + part_o + part_ml + small + cand;
+        return slots + summ + scores + table + 3 * meta4 + meta1 + miss + part_o + part_ml + small;
     }
 };
 
@@ -104,7 +109,6 @@ Sizes sizes_of(const Geometry& g) {
     s.part_o = rsegs * g.max_splits * 8 * kHeadDim * 4;
     s.part_ml = rsegs * g.max_splits * 8 * 2 * 4;
     s.small = rsegs * 8 + 64 + 4 + (size_t)g.R * 4 + g.rec_bytes;
-    s.cand = rsegs * (size_t)((g.nb_pad + 511) / 512) * ((size_t)(g.kmax > 0 ? g.kmax : 1) * 8 + 4);
     s.host = g.resident ? 0 : (size_t)g.A * g.R * g.Hkv * g.nb_max * g.rec_bytes;
     return s;
 }
@@ -164,6 +168,8 @@ kvd_status check_step(kvd_cache* c, int32_t layer, const int32_t* req_ids, int32
     return KVD_OK;
 }
 
+std::atomic<uint64_t> g_launches{0};
+
 kvd_status launched(cudaError_t e) {
     if (e != cudaSuccess) return fail(KVD_ECUDA, "kernel launch: %s", cudaGetErrorString(e));
     return KVD_OK;
@@ -171,11 +177,15 @@ kvd_status launched(cudaError_t e) {
 
 }  // namespace
 
+void kvd::count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
 extern "C" {
 
 const char* kvd_last_error(void) { return g_err.c_str(); }
 
-const char* kvd_version(void) { return "kvd 0.1 sm_100a"; }
+const char* kvd_version(void) { return "kvd 0.2 sm_100a"; }
+
+uint64_t kvd_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 kvd_status kvd_required_bytes(const kvd_config* cfg, size_t* dev_bytes, size_t* host_pinned_bytes) {
     Geometry g;
@@ -218,12 +228,6 @@ kvd_status kvd_create_cache(const kvd_config* cfg, kvd_cache** out) {
     ALLOC(miss_count, rsegs * 4);
     ALLOC(part_o, s.part_o);
     ALLOC(part_ml, s.part_ml);
-    ALLOC(split_ctr, rsegs * 4);
-    ALLOC(sel_ctr, rsegs * 4);
-    c->max_sel_tiles = (int32_t)((g.nb_pad + 511) / 512);
-    ALLOC(cand_key, rsegs * (size_t)c->max_sel_tiles * (g.kmax > 0 ? g.kmax : 1) * 4);
-    ALLOC(cand_id, rsegs * (size_t)c->max_sel_tiles * (g.kmax > 0 ? g.kmax : 1) * 4);
-    ALLOC(cand_cnt, rsegs * (size_t)c->max_sel_tiles * 4);
     ALLOC(stats, 64);
     ALLOC(err, 4);
     ALLOC(ntok_dev, (size_t)g.R * 4);
@@ -233,8 +237,6 @@ kvd_status kvd_create_cache(const kvd_config* cfg, kvd_cache** out) {
     if (e == cudaSuccess) e = cudaMemset(c->table, 0xFF, s.table);
     if (e == cudaSuccess) e = cudaMemset(c->slot_block, 0xFF, s.meta4);
     if (e == cudaSuccess) e = cudaMemset(c->miss_count, 0, rsegs * 4);
-    if (e == cudaSuccess) e = cudaMemset(c->split_ctr, 0, rsegs * 4);
-    if (e == cudaSuccess) e = cudaMemset(c->sel_ctr, 0, rsegs * 4);
     if (e == cudaSuccess) e = cudaMemset(c->stats, 0, 64);
     if (e == cudaSuccess) e = cudaMemset(c->err, 0, 4);
     if (e == cudaSuccess) e = cudaMemset(c->ntok_dev, 0, (size_t)g.R * 4);
@@ -258,7 +260,7 @@ void kvd_destroy_cache(kvd_cache* c) {
     cudaSetDevice(c->cfg.device);
     cudaDeviceSynchronize();
     void* dev[] = {c->slots, c->summ, c->scores, c->table, c->slot_block, c->last_use, c->phase,
-                   c->use_count, c->miss, c->miss_count, c->part_o, c->part_ml, c->split_ctr, c->sel_ctr, c->cand_key, c->cand_id, c->cand_cnt, c->stats,
+                   c->use_count, c->miss, c->miss_count, c->part_o, c->part_ml, c->stats,
                    c->err, c->ntok_dev, c->zero_rec, c->stage_kv, c->stage_rec};
     for (void* p : dev)
         if (p) cudaFree(p);
@@ -339,6 +341,17 @@ kvd_status kvd_resolve_and_fetch(kvd_cache* c, int32_t layer, const int32_t* req
     if ((!ids && k_blocks > 0) || !out_attn) return fail(KVD_EINVAL, "ids / out_attn is NULL");
     p.step = step;
     return launched(launch_resolve(c, p, ids, out_attn, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+kvd_status kvd_select_resolve_fetch(kvd_cache* c, int32_t layer, const uint16_t* q, const int32_t* req_ids,
+                                    int32_t B, int32_t k_blocks, uint32_t step, int32_t* out_ids, float* out_scores,
+                                    int32_t* out_attn, kvd_stream stream) {
+    StepParams p;
+    kvd_status st = check_step(c, layer, req_ids, B, k_blocks, &p);
+    if (st) return st;
+    if (!q || (!out_ids && k_blocks > 0) || !out_attn) return fail(KVD_EINVAL, "q / out_ids / out_attn is NULL");
+    p.step = step;
+    return launched(launch_select_resolve(c, p, q, out_ids, out_scores, out_attn, reinterpret_cast<cudaStream_t>(stream)));
 }
 
 kvd_status kvd_sparse_decode(kvd_cache* c, int32_t layer, const uint16_t* q, const int32_t* req_ids, int32_t B,

@@ -55,7 +55,8 @@ EXPORTS = ["kvd_required_bytes", "kvd_create_cache", "kvd_destroy_cache", "kvd_g
            "kvd_load_prefix", "kvd_select_topk", "kvd_resolve_and_fetch", "kvd_sparse_decode",
            "kvd_read_segment", "kvd_read_slot", "kvd_read_host_record", "kvd_read_summaries",
            "kvd_read_scores", "kvd_get_stats", "kvd_reset_stats", "kvd_check", "kvd_last_error",
-           "kvd_version", "kvd_set_device_step"]
+           "kvd_version", "kvd_set_device_step", "kvd_launch_count",
+           "kvd_select_resolve_fetch"]
 
 
 def lib():
@@ -87,6 +88,8 @@ def lib():
             "kvd_check": ([p], i32),
             "kvd_last_error": ([], ctypes.c_char_p),
             "kvd_version": ([], ctypes.c_char_p),
+            "kvd_launch_count": ([], ctypes.c_uint64),
+            "kvd_select_resolve_fetch": ([p, i32, p, p, i32, i32, u32, p, p, p, p], i32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -187,6 +190,13 @@ class KVCache:
         r, B = _reqs(req_ids)
         _check(lib().kvd_resolve_and_fetch(self.h, layer, r.ctypes.data, B, ptr(ids), k_blocks, step,
                                            ptr(out_attn), _stream(stream)))
+
+    def select_resolve_fetch(self, layer, q, req_ids, k_blocks, step, out_ids, out_attn, out_scores=None,
+                             stream=None):
+        """select_topk + resolve_and_fetch in one fused launch sequence (identical results)."""
+        r, B = _reqs(req_ids)
+        _check(lib().kvd_select_resolve_fetch(self.h, layer, ptr(q), r.ctypes.data, B, k_blocks, step,
+                                              ptr(out_ids), ptr(out_scores), ptr(out_attn), _stream(stream)))
 
     def sparse_decode(self, layer, q, req_ids, attn, W, out, out_lse=None, stream=None):
         r, B = _reqs(req_ids)

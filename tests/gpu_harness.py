@@ -26,7 +26,9 @@ def row_normwise_err(o, ref):
 
 class Case:
     def __init__(self, *, L=1, B=1, Hq=8, Hkv=2, n=4096, P=16, k=32, C=None, policy="lru", seed=0,
-                 alpha=0.9, ragged=False, sink=4, local=64, alias=0, reqs=None, R=None, device=0):
+                 alpha=0.9, ragged=False, sink=4, local=64, alias=0, reqs=None, R=None, device=0,
+                 fused=False):
+        self.fused = fused            # kvd_select_resolve_fetch instead of select_topk + resolve_and_fetch
         self.L, self.B, self.Hq, self.Hkv, self.P, self.k = L, B, Hq, Hkv, P, k
         self.G = Hq // Hkv
         self.policy, self.pol = policy, oracle.POLICIES[policy]
@@ -67,8 +69,11 @@ class Case:
     def gpu_layer(self, l, q_np, step):
         q = torch.from_numpy(q_np.view(np.int16)).to(self.dev)
         c = self.cache
-        c.select_topk(l, q, self.reqs, self.k, self.ids, self.sel_scores)
-        c.resolve_and_fetch(l, self.reqs, self.ids, self.k, step, self.attn)
+        if self.fused:
+            c.select_resolve_fetch(l, q, self.reqs, self.k, step, self.ids, self.attn, self.sel_scores)
+        else:
+            c.select_topk(l, q, self.reqs, self.k, self.ids, self.sel_scores)
+            c.resolve_and_fetch(l, self.reqs, self.ids, self.k, step, self.attn)
         c.sparse_decode(l, q, self.reqs, self.attn, self.W, self.out, self.lse)
         torch.cuda.synchronize()
         c.check()

@@ -128,3 +128,54 @@ def test_deterministic_across_runs():
         for key in ("ids", "attn"):
             assert np.array_equal(ga[key], gb[key])
         assert np.array_equal(ga["out"], gb["out"])
+
+
+# ---- top-k cluster geometries (k_select.cu topk_geometry): P = 1 makes blocks == tokens, so
+# the segment spans 1, 2, 4 and 8 CTAs of the selection cluster; every id, score and list is
+# compared with the oracle's sort-based top-k (O3).
+@pytest.mark.parametrize("n", [3000, 9000, 20000, 40000])
+def test_topk_cluster_spans(n):
+    c = Case(L=1, B=2, Hq=8, Hkv=2, n=n, P=1, k=96, seed=21, ragged=True)
+    c.run(steps=2)
+
+
+def _bf16(x):
+    return (np.asarray(x, np.float32).view(np.uint32) >> 16).astype(np.uint16)
+
+
+@pytest.mark.parametrize("mode", ["zero", "one_dim"])
+def test_topk_ties_lowest_id(mode):
+    """R10 ties: a zero query makes every score +0 (all keys equal: the k lowest candidate ids);
+    a query on one dim makes scores = one bf16 summary coordinate (many exact ties inside the
+    threshold bin)."""
+    c = Case(L=1, B=2, Hq=8, Hkv=2, n=16384, P=16, k=128, C=300, policy="la", seed=22)
+
+    def queries(l, t):
+        q = np.zeros((c.B, c.Hq, 128), np.float32)
+        if mode == "one_dim":
+            q[:, :, 0] = 1.0 + t
+        return _bf16(q)
+    c.queries = queries
+    c.run(steps=3)
+    if mode == "zero":
+        ids = c.ids.cpu().numpy()
+        assert (ids[:, :, :c.k] == np.arange(1, 1 + c.k)).all()   # block 0 is pinned (sink)
+
+
+# ---- the fused select + resolve + fetch call (kvd_select_resolve_fetch) against the oracle:
+# same decisions, slot maps, metadata, slot bytes and attention as the two separate calls
+@pytest.mark.parametrize("policy", ["lru", "lfu", "la"])
+def test_fused_select_resolve_fetch_evict(policy):
+    c = Case(L=1, B=2, Hq=8, Hkv=2, n=4096, P=16, k=32, C=69, policy=policy, alpha=0.0, seed=31, fused=True)
+    c.run(steps=8, check_slots_every=2)
+
+
+@pytest.mark.parametrize("n,P,C", [(3000, 16, 60), (20000, 1, None), (40000, 1, 2000)])
+def test_fused_ragged_and_cluster_spans(n, P, C):
+    c = Case(L=2, B=3, Hq=8, Hkv=2, n=n, P=P, k=40, C=C, policy="la", ragged=True, seed=32, fused=True)
+    c.run(steps=3)
+
+
+def test_fused_k_zero_and_group_of_seven():
+    Case(L=1, B=1, Hq=8, Hkv=2, n=1000, P=16, k=0, C=10, seed=33, fused=True).run(steps=2)
+    Case(L=1, B=2, Hq=14, Hkv=2, n=2048, P=16, k=24, C=48, policy="lfu", seed=34, fused=True).run(steps=4)
