@@ -44,7 +44,7 @@ sys.path.insert(0, ROOT)
 CONFIGS = {
     "c1": dict(chains=1, L=1, B=1, Hq=8, Hkv=2, n=4096, P=16, k=32, C=None, alias=0,
                desc="1 req, 1 layer, 8q/2kv, d128, 4k ctx, block 16, top-k 32, resident"),
-    "c2": dict(chains=1, L=32, B=8, Hq=32, Hkv=8, n=32768, P=16, k=128, C=None, alias=0,
+    "c2": dict(chains=8, L=32, B=8, Hq=32, Hkv=8, n=32768, P=16, k=128, C=None, alias=0,
                desc="Llama-3.1-8B shapes (32 layers, 32q/8kv, d128) bf16, 32k ctx, batch 8, top-k 2048 tokens, resident"),
     "c3": dict(chains=16, L=32, B=16, Hq=32, Hkv=8, n=131072, P=16, k=128, C=2048, alias=4,
                desc="Llama-3.1-8B shapes, 128k ctx, batch 16, GPU cache 25% of KV (2048 slots/segment), misses "

@@ -91,6 +91,7 @@ cudaError_t launch_select(kvd_cache* c, const StepParams& p, const uint16_t* q, 
 size_t resolve_smem_bytes(int64_t nkeys, int64_t kmax, int64_t nb_pad);   // k_resolve.cu
 constexpr size_t kMaxSmemBytes = 227 * 1024;
 cudaError_t launch_resolve(kvd_cache* c, const StepParams& p, const int32_t* ids, int32_t* out_attn, cudaStream_t s);
+cudaError_t launch_gather(kvd_cache* c, const StepParams& p, cudaStream_t s);
 cudaError_t launch_select_resolve(kvd_cache* c, const StepParams& p, const uint16_t* q, int32_t* out_ids,
                                   float* out_scores, int32_t* out_attn, cudaStream_t s);
 cudaError_t launch_attention(kvd_cache* c, const StepParams& p, const uint16_t* q, const int32_t* attn, float* out,

@@ -84,6 +84,17 @@ ResolveBufs resolve_bufs(kvd_cache* c) {
     return rb;
 }
 
+cudaError_t launch_gather(kvd_cache* c, const StepParams& p, cudaStream_t s) {
+    static int prio = 1;
+    if (prio == 1) {
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        prio = hi;                                   // greatest priority (numerically lowest)
+    }
+    return launch_pdl_prio(prio, gather_kernel, dim3(148), dim3(kGatherThreads), 0, s, p, (const int32_t*)c->miss,
+                           (const int32_t*)c->miss_count, (int)c->kmax, (const uint8_t*)c->host_store, c->slots);
+}
+
 cudaError_t launch_resolve(kvd_cache* c, const StepParams& p, const int32_t* ids, int32_t* out_attn,
                            cudaStream_t s) {
     const ResolveBufs rb = resolve_bufs(c);
@@ -97,14 +108,7 @@ cudaError_t launch_resolve(kvd_cache* c, const StepParams& p, const int32_t* ids
     cudaError_t e = launch_pdl(resolve_kernel, dim3(p.Hkv, p.B), dim3(kResolveThreads), smem, s, p, rb, ids, out_attn);
     if (e != cudaSuccess) return e;
     if (!c->resident) {
-        static int prio = 1;
-        if (prio == 1) {
-            int lo = 0, hi = 0;
-            cudaDeviceGetStreamPriorityRange(&lo, &hi);
-            prio = hi;                                   // greatest priority (numerically lowest)
-        }
-        e = launch_pdl_prio(prio, gather_kernel, dim3(148), dim3(kGatherThreads), 0, s, p, (const int32_t*)c->miss,
-                       (const int32_t*)c->miss_count, (int)c->kmax, (const uint8_t*)c->host_store, c->slots);
+        e = launch_gather(c, p, s);
         if (e != cudaSuccess) return e;
     }
     return cudaGetLastError();

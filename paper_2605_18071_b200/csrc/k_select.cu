@@ -700,12 +700,19 @@ cudaError_t launch_select_resolve(kvd_cache* c, const StepParams& p, const uint1
     FuseArgs fa;
     fa.rb = resolve_bufs(c);
     fa.out_attn = out_attn;
-    fa.host_store = c->resident ? nullptr : c->host_store;
+    static int inner = -1;                        // misses copied inside the fused kernel (default)
+    if (inner < 0) {
+        const char* env = getenv("KVD_FUSED_GATHER");   // experiments only: 0 = separate gather kernel
+        inner = env && atoi(env) == 0 ? 0 : 1;
+    }
+    fa.host_store = (c->resident || !inner) ? nullptr : c->host_store;
     fa.slots = c->slots;
     const int nt = topk_threads();
     e = nt == 256 ? launch_topk_nt<256, true>(c, p, out_ids, out_scores, fa, s)
       : nt == 512 ? launch_topk_nt<512, true>(c, p, out_ids, out_scores, fa, s)
                   : launch_topk_nt<1024, true>(c, p, out_ids, out_scores, fa, s);
+    if (e != cudaSuccess) return e;
+    if (!c->resident && !inner) e = launch_gather(c, p, s);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }

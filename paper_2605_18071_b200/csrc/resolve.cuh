@@ -272,30 +272,34 @@ __device__ inline int resolve_main(const StepParams& p, const ResolveBufs& rb, i
 }
 
 
-// (a4) inside a segment's CTA: warps copy the nm missed 8 KiB records host -> slot
-// (zero-copy 16-byte loads over the host link, 8 in flight per lane).
+// (a4) inside a segment's CTA: all threads copy the nm missed 8 KiB records host -> slot.
+// The (record, 16-byte chunk) space is flattened over the CTA and every thread keeps up to 8
+// zero-copy loads in flight, so the whole miss set is requested in one host-link round trip.
 __device__ __forceinline__ void gather_segment(const StepParams& p, int bi, int h, const int32_t* M, const int32_t* dest,
                                                int nm, const uint8_t* __restrict__ host_store,
                                                uint8_t* __restrict__ slots) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const int r = p.req[bi];
-    const int chunks = p.rec_bytes / 16;
+    const int cpr = p.rec_bytes / 16;                       // 16-byte chunks per record (power of two)
+    const int lcpr = __ffs(cpr) - 1;
+    const int total = nm << lcpr;
     const uint8_t* hbase = host_store + (((int64_t)p.host_layer * p.R + r) * p.Hkv + h) * p.nb_max * (int64_t)p.rec_bytes;
     uint8_t* sbase = slots + (((int64_t)p.layer * p.R + r) * p.Hkv + h) * p.C * (int64_t)p.rec_bytes;
-    for (int i = warp; i < nm; i += nwarps) {
-        const int4* src = reinterpret_cast<const int4*>(hbase + (int64_t)M[i] * p.rec_bytes);
-        int4* dst = reinterpret_cast<int4*>(sbase + (int64_t)dest[i] * p.rec_bytes);
-        for (int c0 = 0; c0 < chunks; c0 += 32 * 8) {
-            int4 v[8];
+    for (int x0 = threadIdx.x; x0 < total; x0 += 8 * blockDim.x) {
+        int4 v[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int c = c0 + u * 32 + lane;
-                if (c < chunks) v[u] = ld_host16(src + c);
+        for (int u = 0; u < 8; ++u) {
+            const int x = x0 + u * blockDim.x;
+            if (x < total) {
+                const int i = x >> lcpr, c = x & (cpr - 1);
+                v[u] = ld_host16(reinterpret_cast<const int4*>(hbase + (int64_t)M[i] * p.rec_bytes) + c);
             }
+        }
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int c = c0 + u * 32 + lane;
-                if (c < chunks) dst[c] = v[u];
+        for (int u = 0; u < 8; ++u) {
+            const int x = x0 + u * blockDim.x;
+            if (x < total) {
+                const int i = x >> lcpr, c = x & (cpr - 1);
+                reinterpret_cast<int4*>(sbase + (int64_t)dest[i] * p.rec_bytes)[c] = v[u];
             }
         }
     }
