@@ -33,6 +33,23 @@ import time
 import numpy as np
 
 
+def ncu_traffic(config, bound, dom):
+    """DRAM bytes per ABI call (scaled per segment) from the committed ncu capture, or None."""
+    if bound != "hbm":
+        return None
+    import glob
+    files = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "*_ncu_traffic.json")))
+    if not files:
+        return None
+    try:
+        d = json.load(open(files[-1]))
+        e = d[config][dom]
+        return {"bytes_per_call": e["dram_bytes_per_call"], "segments": e["segments"],
+                "source": f"{os.path.basename(files[-1])}: {e['kernels']}"}
+    except (KeyError, ValueError, OSError):
+        return None
+
+
 def kvd_launch_count():
     from paper_2605_18071_b200 import kvd
     return int(kvd.lib().kvd_launch_count())
@@ -435,6 +452,13 @@ def run_gpu(args):
         roof = {"kernel": {"select": "score+topk (a1+a2)", "attn": "sparse decode + merge (a5+a6)"}[dom],
                 "bound": "hbm", "achieved": kernels[dom]["gbs"], "peak": hbm_peak, "unit": "GB/s",
                 "frac": kernels[dom]["frac_hbm"], "peak_source": hbm_src, "traffic": None}
+    # traffic: DRAM bytes per launch of the dominant ABI call's kernels from one committed
+    # `ncu --set full` capture (profiles/*_ncu_traffic.json, written by tools/ncu_traffic.py);
+    # host-link-bound calls have no DRAM equivalent of their algorithmic bytes (null)
+    tr = ncu_traffic(args.config, roof["bound"], dom)
+    if tr:
+        roof["traffic"] = tr["bytes_per_call"] * (segs_per_layer / tr["segments"])
+        roof["traffic_source"] = tr["source"]
     # the attention kernel's roofline is always reported (north_star: sparse-attn HBM GB/s % peak)
     roof_attn = {"achieved": kernels["attn"]["gbs"], "peak": hbm_peak, "unit": "GB/s",
                  "frac": kernels["attn"]["frac_hbm"]}

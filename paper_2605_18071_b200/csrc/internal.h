@@ -97,14 +97,18 @@ cudaError_t launch_select_resolve(kvd_cache* c, const StepParams& p, const uint1
 cudaError_t launch_attention(kvd_cache* c, const StepParams& p, const uint16_t* q, const int32_t* attn, float* out,
                              float* out_lse, cudaStream_t s);
 
-__host__ __device__ inline SegGeom seg_geom(int64_t n, int P, int sink, int local) {
+__host__ __device__ inline SegGeom seg_geom(int64_t n64, int P, int sink, int local) {
+    // 32-bit, shift-only (P in {1, 2, 4, 8, 16}; n < 2^27): every thread of the step kernels
+    // evaluates this, so no 64-bit integer divisions
+    const int lp = P >= 16 ? 4 : P >= 8 ? 3 : P >= 4 ? 2 : P >= 2 ? 1 : 0;
+    const int32_t n = (int32_t)n64;
     SegGeom g;
-    g.n = (int32_t)n;
-    g.nb = (int32_t)((n + P - 1) / P);
-    int32_t se = (int32_t)((sink + P - 1) / P);
-    int64_t ft = n - local;
+    g.n = n;
+    g.nb = (n + P - 1) >> lp;
+    int32_t se = (sink + P - 1) >> lp;
+    int32_t ft = n - local;
     if (ft < 0) ft = 0;
-    int32_t lb = local > 0 ? (int32_t)(ft / P) : g.nb;
+    int32_t lb = local > 0 ? (ft >> lp) : g.nb;
     if (lb > g.nb) lb = g.nb;
     if (se > lb) se = lb;                  // overlapping sink/local: all blocks pinned
     g.sink_end = se;

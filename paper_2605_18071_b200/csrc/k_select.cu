@@ -137,6 +137,7 @@ __global__ void __launch_bounds__(kScoreThreads, 4) score_kernel(StepParams p, c
 
 // ------------------------------------------------------------------ (a2) top-k
 constexpr int kListCap = 4096;                // compacted threshold-bin members per CTA
+constexpr int kTakeMax = 512;                 // list emission for k up to this
 
 struct TopkShared {
     int hist[2][256];                 // per-pass digit histograms (double-buffered: read remotely)
@@ -150,6 +151,8 @@ struct TopkShared {
     int ctot[2];                      // CTA totals of the emission counts (read remotely)
     int ncomp;                        // compacted members of the first threshold bin (this CTA)
     int lcount;                       // threshold-bin members of this CTA (LIST mode)
+    int ntake;                        // taken ids of this CTA (list emission)
+    int32_t take[kTakeMax];
     uint32_t lkey[kTieList];
     int32_t lid[kTieList];
 };
@@ -349,29 +352,29 @@ __global__ void __launch_bounds__(NT, 1) topk_kernel(FuseArgs fa, StepParams p, 
         kk -= sm.above;
         cnt = sm.cnt;
     }
-    // ---- threshold-bin members: compact them (when they fit) and take their key range
-    bool compacted = false;
+    // ---- compact the threshold bin's members and the keys above it (when they fit; bit 31 of
+    // the index marks "above") and take the members' key range
     kmn = 0xFFFFFFFFu;
     kmx = 0u;
-    if (kk != cnt && cnt > kTieList) {
-        for (int i0 = (c_lo & ~31) + warp * 32; i0 < c_hi; i0 += NT) {
-            const int i = i0 + lane;
-            const uint32_t key = skey[i];
-            const bool in = i >= c_lo && i < c_hi && bin_at(i) == bstar;
-            if (in) {
-                kmn = min(kmn, key);
-                kmx = max(kmx, key);
-            }
-            const uint32_t bal = __ballot_sync(0xffffffffu, in);
-            int wbase = 0;
-            if (lane == 0 && bal) wbase = atomicAdd(&sm.ncomp, __popc(bal));
-            wbase = __shfl_sync(0xffffffffu, wbase, 0);
-            const int slot = wbase + __popc(bal & ((1u << lane) - 1u));
-            if (in && slot < kListCap) comp[slot] = make_uint2(key, (uint32_t)i);
+    for (int i0 = (c_lo & ~31) + warp * 32; i0 < c_hi; i0 += NT) {
+        const int i = i0 + lane;
+        const bool inr = i >= c_lo && i < c_hi;
+        const uint32_t key = inr ? skey[i] : 0u;
+        const int b = inr ? bin_at(i) : -1;
+        const bool in = inr && b >= bstar;
+        if (inr && b == bstar) {
+            kmn = min(kmn, key);
+            kmx = max(kmx, key);
         }
-        cta_minmax<CL>(kmn, kmx, sm);             // contains the barriers that publish ncomp
-        compacted = sm.ncomp <= kListCap;         // uniform over the CTA
+        const uint32_t bal = __ballot_sync(0xffffffffu, in);
+        int wbase = 0;
+        if (lane == 0 && bal) wbase = atomicAdd(&sm.ncomp, __popc(bal));
+        wbase = __shfl_sync(0xffffffffu, wbase, 0);
+        const int slot = wbase + __popc(bal & ((1u << lane) - 1u));
+        if (in && slot < kListCap) comp[slot] = make_uint2(key, (uint32_t)i | (b > bstar ? 0x80000000u : 0u));
     }
+    cta_minmax<CL>(kmn, kmx, sm);                 // contains the barriers that publish ncomp
+    const bool compacted = sm.ncomp <= kListCap;  // uniform over the CTA
     const uint32_t diff = kmn ^ kmx;
     int lo = (kk != cnt && cnt > kTieList && diff) ? 32 - __clz(diff) : 0;   // bits [0, lo) still to resolve
     uint32_t mask = lo == 32 ? 0u : ~((1u << lo) - 1u);
@@ -395,8 +398,8 @@ __global__ void __launch_bounds__(NT, 1) topk_kernel(FuseArgs fa, StepParams p, 
             const int nc = sm.ncomp;
             for (int j0 = warp * 32; j0 < nc; j0 += NT) {
                 const int j = j0 + lane;
-                const uint32_t key = j < nc ? comp[j].x : 0u;
-                warp_hist_add(hb, (key >> shift) & (uint32_t)(nbins - 1), j < nc && (key & mask) == prefix);
+                const uint2 e = j < nc ? comp[j] : make_uint2(0u, 0x80000000u);
+                warp_hist_add(hb, (e.x >> shift) & (uint32_t)(nbins - 1), !(e.y >> 31) && (e.x & mask) == prefix);
             }
         } else {
             for (int i0 = (c_lo & ~31) + warp * 32; i0 < c_hi; i0 += NT) {
@@ -432,7 +435,7 @@ __global__ void __launch_bounds__(NT, 1) topk_kernel(FuseArgs fa, StepParams p, 
         };
         if (compacted) {
             for (int j = tid; j < sm.ncomp; j += NT)
-                if ((comp[j].x & mask) == prefix) add(comp[j].x, (int)comp[j].y);
+                if (!(comp[j].y >> 31) && (comp[j].x & mask) == prefix) add(comp[j].x, (int)comp[j].y);
         } else {
             for (int i = c_lo + tid; i < c_hi; i += NT)
                 if (bin_at(i) == bstar && (skey[i] & mask) == prefix) add(skey[i], i);
@@ -452,6 +455,53 @@ __global__ void __launch_bounds__(NT, 1) topk_kernel(FuseArgs fa, StepParams p, 
         }
         return rank;
     };
+    int32_t* ids_out = out_ids + ((int64_t)bi * p.Hkv + h) * p.k;
+    float* sc_out = out_scores ? out_scores + ((int64_t)bi * p.Hkv + h) * p.k : nullptr;
+    if (compacted && mode != kModeEqual && p.k <= kTakeMax) {
+        // ---- emission from the compacted list: every taken id is in it (above the bin, or a
+        // taken member); its output position = number of taken ids (cluster-wide) below it
+        if (tid == 0) sm.ntake = 0;
+        __syncthreads();
+        const int nc = sm.ncomp;
+        for (int j = tid; j < nc; j += NT) {
+            const uint2 e = comp[j];
+            const int i = (int)(e.y & 0x7FFFFFFFu);
+            bool take = e.y >> 31;
+            if (!take) {
+                const uint32_t km = e.x & mask;
+                take = km > prefix || (km == prefix && (mode == kModeWhole || bin_rank(e.x, (int32_t)(base + i)) < kk));
+            }
+            if (take) sm.take[atomicAdd(&sm.ntake, 1)] = (int32_t)(base + i);
+        }
+        cl_sync<CL>();
+        // gather the cluster's taken ids locally (p.k of them), then rank by id
+        int off = 0, tot = 0;
+#pragma unroll
+        for (int c = 0; c < CL; ++c) {
+            const int m = *cl_remote<CL>(&sm.ntake, c);
+            off += c < crank ? m : 0;
+            tot += m;
+        }
+        int32_t* all = reinterpret_cast<int32_t*>(comp);   // comp is no longer needed
+        __syncthreads();
+        {
+            int o = 0;
+            for (int c = 0; c < CL; ++c) {
+                const TopkShared* rs = cl_remote<CL>(&sm, c);
+                const int m = rs->ntake;
+                for (int j = tid; j < m; j += NT) all[o + j] = rs->take[j];
+                o += m;
+            }
+        }
+        __syncthreads();
+        for (int j = tid; j < sm.ntake; j += NT) {
+            const int32_t id = all[off + j];
+            int pos = 0;
+            for (int u = 0; u < tot; ++u) pos += all[u] < id ? 1 : 0;
+            ids_out[pos] = id;
+            if (sc_out) sc_out[pos] = __ldcg(sc + (id - base));
+        }
+    } else {
     // ---- emission.  Warp w owns positions [w0, w1) and walks them in 32-wide strips: pre-pass
     // counts (above, bin members), cluster-wide exclusive offsets in position order, then
     // ballots place every taken id at its ascending output position.
@@ -515,8 +565,6 @@ __global__ void __launch_bounds__(NT, 1) topk_kernel(FuseArgs fa, StepParams p, 
         for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
         taken_eq_before = t;
     }
-    int32_t* ids_out = out_ids + ((int64_t)bi * p.Hkv + h) * p.k;
-    float* sc_out = out_scores ? out_scores + ((int64_t)bi * p.Hkv + h) * p.k : nullptr;
     for (int i0 = warp * per_w; i0 < w1; i0 += 32) {
         const int i = i0 + lane;
         bool gt, eq;
@@ -539,6 +587,7 @@ __global__ void __launch_bounds__(NT, 1) topk_kernel(FuseArgs fa, StepParams p, 
         gt_before += __popc(bgt);
         eq_before += __popc(beq);
         taken_eq_before += __popc(btk);
+    }
     }
     stamp(5);
     stamp(6, 1000ull * mode + (32 - lo) + (compacted ? 100 : 0));

@@ -143,12 +143,14 @@ def _bf16(x):
     return (np.asarray(x, np.float32).view(np.uint32) >> 16).astype(np.uint16)
 
 
-@pytest.mark.parametrize("mode", ["zero", "one_dim"])
-def test_topk_ties_lowest_id(mode):
+@pytest.mark.parametrize("mode,n,P", [("zero", 16384, 16), ("one_dim", 16384, 16), ("zero", 40000, 1),
+                                      ("one_dim", 40000, 1)])
+def test_topk_ties_lowest_id(mode, n, P):
     """R10 ties: a zero query makes every score +0 (all keys equal: the k lowest candidate ids);
     a query on one dim makes scores = one bf16 summary coordinate (many exact ties inside the
-    threshold bin)."""
-    c = Case(L=1, B=2, Hq=8, Hkv=2, n=16384, P=16, k=128, C=300, policy="la", seed=22)
+    threshold bin).  P = 1 at n = 40,000: a 4-CTA cluster whose threshold bin overflows the
+    compacted list (full-scan digits and emission)."""
+    c = Case(L=1, B=2, Hq=8, Hkv=2, n=n, P=P, k=128, C=300 if P == 16 else 2000, policy="la", seed=22)
 
     def queries(l, t):
         q = np.zeros((c.B, c.Hq, 128), np.float32)
@@ -159,7 +161,8 @@ def test_topk_ties_lowest_id(mode):
     c.run(steps=3)
     if mode == "zero":
         ids = c.ids.cpu().numpy()
-        assert (ids[:, :, :c.k] == np.arange(1, 1 + c.k)).all()   # block 0 is pinned (sink)
+        first = -(-4 // P)                                        # sink blocks are pinned
+        assert (ids[:, :, :c.k] == np.arange(first, first + c.k)).all()
 
 
 # ---- the fused select + resolve + fetch call (kvd_select_resolve_fetch) against the oracle:
