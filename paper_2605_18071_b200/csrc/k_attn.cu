@@ -407,42 +407,62 @@ __global__ void __launch_bounds__(WARPS * 32, 1) attn_kernel(StepParams p, AttnB
 }
 
 
-// (a6) grid (S), 32*G threads: warp hh merges query head hh of segment s; lane jj holds piece
-// jj's (m, l); lane owns dims 4 lane .. 4 lane + 3 and sums the pieces with independent loads.
-__global__ void __launch_bounds__(256) merge_kernel(StepParams p, AttnBufs ab, Work wk, float* __restrict__ out,
-                                                    float* __restrict__ out_lse) {
+// (a6) grid (S), 32*G*NG threads: warp (grp, hh) merges pieces [32 grp, 32 grp + 32) of query
+// head hh of segment s; lane owns dims 4 lane .. 4 lane + 3.  All 32 partial rows of a warp
+// are requested before anything else (one memory round trip); groups combine through smem.
+template <int NG>   // groups of 32 pieces: 1 (np <= 32) or 2 (np <= 64)
+__global__ void __launch_bounds__(256 * NG) merge_kernel(StepParams p, AttnBufs ab, Work wk, float* __restrict__ out,
+                                                         float* __restrict__ out_lse) {
+    __shared__ float s_m[NG][8], s_l[NG][8];
+    __shared__ float4 s_acc[NG > 1 ? 8 : 1][32];
     const int cs = blockIdx.x;
-    const int lane = threadIdx.x & 31, hh = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int hh = NG > 1 ? warp % p.G : warp, grp = NG > 1 ? warp / p.G : 0;
     const int s0 = cs * wk.TS;
     const int fw = worker_of(s0, wk), lw = worker_of(s0 + wk.TS - 1, wk);
     const int np = lw - fw + 1;
     griddep_wait();                               // partials come from attn_kernel
-    if (np == 1) return;                          // finalised by its only worker
+    if (np == 1) return;                          // finalised by its only worker (uniform over the CTA)
     const int bi = cs / p.Hkv, h = cs - bi * p.Hkv;
     const int64_t rs = (int64_t)p.req[bi] * p.Hkv + h;
     const float* po0 = ab.part_o + (rs * kMaxPieces * 8) * (int64_t)kHeadDim;
     const float* pml0 = ab.part_ml + (rs * kMaxPieces * 8) * 2;
-    // every load of the segment up front (one memory round trip): the np <= 32 partial rows of
-    // this head and this lane's piece statistics
+    const int j0 = 32 * grp;
     const float4* src = reinterpret_cast<const float4*>(po0 + hh * kHeadDim) + lane;
-    float4 x[kMaxPieces];
+    float4 x[32];
 #pragma unroll
-    for (int u = 0; u < kMaxPieces; ++u)
-        x[u] = u < np ? __ldcg(src + u * 8 * (kHeadDim / 4)) : make_float4(0.f, 0.f, 0.f, 0.f);
-    const float mj = lane < np ? __ldcg(&pml0[(lane * 8 + hh) * 2]) : -INFINITY;
-    const float lj = lane < np ? __ldcg(&pml0[(lane * 8 + hh) * 2 + 1]) : 0.f;
+    for (int u = 0; u < 32; ++u)
+        x[u] = j0 + u < np ? __ldcg(src + (j0 + u) * 8 * (kHeadDim / 4)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const int j = j0 + lane;
+    const float mj = j < np ? __ldcg(&pml0[(j * 8 + hh) * 2]) : -INFINITY;
+    const float lj = j < np ? __ldcg(&pml0[(j * 8 + hh) * 2 + 1]) : 0.f;
     float M = mj;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-    const float scj = (lane < np && M != -INFINITY) ? fast_exp2(mj - M) : 0.f;
+    if (NG > 1) {
+        if (lane == 0) s_m[grp][hh] = M;
+        __syncthreads();
+#pragma unroll
+        for (int g2 = 0; g2 < NG; ++g2) M = fmaxf(M, s_m[g2][hh]);
+    }
+    const float scj = (j < np && M != -INFINITY) ? fast_exp2(mj - M) : 0.f;
     float l = scj * lj;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-    for (int u = 0; u < kMaxPieces; ++u) {
-        const float sc = __shfl_sync(0xffffffffu, scj, u);   // 0 for u >= np
+    for (int u = 0; u < 32; ++u) {
+        const float sc = __shfl_sync(0xffffffffu, scj, u);   // 0 past np
         acc.x += sc * x[u].x; acc.y += sc * x[u].y; acc.z += sc * x[u].z; acc.w += sc * x[u].w;
+    }
+    if (NG > 1) {
+        if (grp == 1) s_acc[hh][lane] = acc;
+        if (lane == 0) s_l[grp][hh] = l;
+        __syncthreads();
+        if (grp != 0) return;
+        const float4 o1 = s_acc[hh][lane];
+        acc.x += o1.x; acc.y += o1.y; acc.z += o1.z; acc.w += o1.w;
+        l += s_l[1][hh];
     }
     const float il = l > 0.f ? 1.f / l : 0.f;
     const int64_t oh = (int64_t)bi * p.Hq + (int64_t)h * p.G + hh;
@@ -469,10 +489,15 @@ static cudaError_t launch_attn_s(kvd_cache* c, const StepParams& p, const uint16
     Work wk;
     wk.TS = (p.W + p.E - 1) / p.E;
     wk.T = S * wk.TS;
-    // workers: enough to fill every SM, but at most kMaxPieces - 1 per segment so a
-    // segment never has more than kMaxPieces pieces (<= ceil(NW/S) + 1), and at most T
+    // workers: enough to fill every SM, but at most maxp - 1 per segment so a segment never
+    // has more than maxp <= kMaxPieces pieces (<= ceil(NW/S) + 1), and at most T
+    static int maxp = 0;
+    if (!maxp) {
+        const char* env = getenv("KVD_ATTN_MAXP");   // experiments only
+        maxp = env ? std::max(2, std::min(atoi(env), kMaxPieces)) : 32;   // default: one merge group
+    }
     int nw = max_ctas * WARPS;
-    nw = std::min(nw, S * (kMaxPieces - 1));
+    nw = std::min(nw, S * (maxp - 1));
     nw = std::min(nw, wk.T);
     wk.NW = std::max(nw, 1);
     static int xflags = -1;
@@ -500,7 +525,10 @@ static cudaError_t launch_attn_s(kvd_cache* c, const StepParams& p, const uint16
         split = ((a + 1) * wk.NW - 1) / wk.T != ((b + 1) * wk.NW - 1) / wk.T;
     }
     if (split) {
-        e = launch_pdl(merge_kernel, dim3(S), dim3(32 * p.G), 0, s, p, ab, wk, out, out_lse);
+        const int maxnp = (wk.NW + S - 1) / S + 1;   // pieces of a segment <= ceil(NW/S) + 1
+        e = maxnp <= 32 ? launch_pdl(merge_kernel<1>, dim3(S), dim3(32 * p.G), 0, s, p, ab, wk, out, out_lse)
+                        : launch_pdl(merge_kernel<2>, dim3(S), dim3(64 * p.G), 0, s, p, ab, wk, out, out_lse);
+        // (merge_kernel<2> keeps fewer loads in flight: the register file cannot hold 64 rows)
         if (e != cudaSuccess) return e;
     }
     if (trace) {   // experiments only: synchronous dump of per-warp phase times (us from first stamp)
