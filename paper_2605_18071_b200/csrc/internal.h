@@ -25,7 +25,7 @@ constexpr int kAttnStages = 3;        // smem stages per warp
 constexpr int kTileBytes = 8192;      // one 16-token K||V tile
 constexpr int kSplitTiles = 16;       // (legacy split size; StepParams.nsplit)
 constexpr int kMaxSelectBlocks = 8 * 1024 * 32;   // top-k cluster capacity: 8 CTAs x 1024 threads x 32 keys
-constexpr int kMaxPieces = 64;        // attention partials per (request, KV head) (k_attn.cu)
+constexpr int kMaxPieces = 32;        // attention partials per (request, KV head) (k_attn.cu)
 constexpr int64_t kSlotOfBytes = 64ll << 20;   // setup scratch for per-block slot targets
 
 struct SegGeom {                      // per-request pinned geometry (device copy in params)

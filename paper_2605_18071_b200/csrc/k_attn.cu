@@ -489,15 +489,10 @@ static cudaError_t launch_attn_s(kvd_cache* c, const StepParams& p, const uint16
     Work wk;
     wk.TS = (p.W + p.E - 1) / p.E;
     wk.T = S * wk.TS;
-    // workers: enough to fill every SM, but at most maxp - 1 per segment so a segment never
-    // has more than maxp <= kMaxPieces pieces (<= ceil(NW/S) + 1), and at most T
-    static int maxp = 0;
-    if (!maxp) {
-        const char* env = getenv("KVD_ATTN_MAXP");   // experiments only
-        maxp = env ? std::max(2, std::min(atoi(env), kMaxPieces)) : 32;   // default: one merge group
-    }
+    // workers: enough to fill every SM, but at most kMaxPieces - 1 per segment so a segment
+    // never has more than kMaxPieces pieces (<= ceil(NW/S) + 1), and at most T
     int nw = max_ctas * WARPS;
-    nw = std::min(nw, S * (maxp - 1));
+    nw = std::min(nw, S * (kMaxPieces - 1));
     nw = std::min(nw, wk.T);
     wk.NW = std::max(nw, 1);
     static int xflags = -1;
@@ -525,10 +520,9 @@ static cudaError_t launch_attn_s(kvd_cache* c, const StepParams& p, const uint16
         split = ((a + 1) * wk.NW - 1) / wk.T != ((b + 1) * wk.NW - 1) / wk.T;
     }
     if (split) {
-        const int maxnp = (wk.NW + S - 1) / S + 1;   // pieces of a segment <= ceil(NW/S) + 1
-        e = maxnp <= 32 ? launch_pdl(merge_kernel<1>, dim3(S), dim3(32 * p.G), 0, s, p, ab, wk, out, out_lse)
-                        : launch_pdl(merge_kernel<2>, dim3(S), dim3(64 * p.G), 0, s, p, ab, wk, out, out_lse);
-        // (merge_kernel<2> keeps fewer loads in flight: the register file cannot hold 64 rows)
+        // pieces of a segment <= ceil(NW/S) + 1 <= kMaxPieces = 32: one group of rows per warp.
+        // (64 pieces measured slower at c2 and c4: merge_kernel<2> cannot keep 64 rows in flight)
+        e = launch_pdl(merge_kernel<1>, dim3(S), dim3(32 * p.G), 0, s, p, ab, wk, out, out_lse);
         if (e != cudaSuccess) return e;
     }
     if (trace) {   // experiments only: synchronous dump of per-warp phase times (us from first stamp)
