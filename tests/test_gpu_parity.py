@@ -182,3 +182,21 @@ def test_fused_ragged_and_cluster_spans(n, P, C):
 def test_fused_k_zero_and_group_of_seven():
     Case(L=1, B=1, Hq=8, Hkv=2, n=1000, P=16, k=0, C=10, seed=33, fused=True).run(steps=2)
     Case(L=1, B=2, Hq=14, Hkv=2, n=2048, P=16, k=24, C=48, policy="lfu", seed=34, fused=True).run(steps=4)
+
+
+# ---- degenerate and maximum shapes
+@pytest.mark.parametrize("n,k", [(1, 0), (40, 0), (68, 0), (69, 0), (100, 1), (129, 2)])
+def test_tiny_contexts_all_or_mostly_pinned(n, k):
+    """n <= sink + local pins every block (no candidates, k = 0); slightly longer contexts leave
+    one or two candidates; partial last blocks everywhere."""
+    for fused in (False, True):
+        c = Case(L=1, B=2, Hq=8, Hkv=2, n=n, P=16, k=k, C=None, seed=41, ragged=False, fused=fused)
+        c.run(steps=2)
+
+
+@pytest.mark.parametrize("fused", [False, True])
+def test_max_batch_many_segments(fused):
+    """KVD_MAX_BATCH requests x 8 KV heads = 2048 segments per call: more segments than attention
+    workers, so most workers finalise whole segments in place; host-backed with evictions."""
+    c = Case(L=1, B=256, Hq=32, Hkv=8, n=600, P=16, k=8, C=20, policy="lru", seed=42, fused=fused)
+    c.run(steps=2, check_state=True)
