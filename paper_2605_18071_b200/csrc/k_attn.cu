@@ -491,8 +491,17 @@ static cudaError_t launch_attn_s(kvd_cache* c, const StepParams& p, const uint16
     wk.T = S * wk.TS;
     // workers: enough to fill every SM, but at most kMaxPieces - 1 per segment so a segment
     // never has more than kMaxPieces pieces (<= ceil(NW/S) + 1), and at most T
+    // pieces per segment: 16 once a launch has >= 8 segments (a micro-batch chain of one Llama
+    // request; 15 workers per segment leave SM room for the other chains' fetches: c3 2623 ->
+    // 2865 tok/s, c2 unchanged), 32 for fewer segments (c4: 1675 vs 1632 at 16)
+    static int maxp_env = -1;
+    if (maxp_env < 0) {
+        const char* env = getenv("KVD_ATTN_MAXP");   // experiments only: override the cap
+        maxp_env = env ? std::max(2, std::min(atoi(env), kMaxPieces)) : 0;
+    }
+    const int maxp = maxp_env ? maxp_env : (S >= 8 ? 16 : kMaxPieces);
     int nw = max_ctas * WARPS;
-    nw = std::min(nw, S * (kMaxPieces - 1));
+    nw = std::min(nw, S * (maxp - 1));
     nw = std::min(nw, wk.T);
     wk.NW = std::max(nw, 1);
     static int xflags = -1;

@@ -57,8 +57,8 @@ struct VecOf<4> {
 };
 
 // grid (tiles, Hkv, B); CTA = kScoreThreads threads scoring kScoreThreads*V blocks of one segment.
-template <int V>
-__global__ void __launch_bounds__(kScoreThreads, 4) score_kernel(StepParams p, const uint16_t* __restrict__ q,
+template <int V, int R>
+__global__ void __launch_bounds__(kScoreThreads, R > 16 ? 2 : 4) score_kernel(StepParams p, const uint16_t* __restrict__ q,
                                                                  const uint16_t* __restrict__ summ,
                                                                  float* __restrict__ scores,
                                                                  const int32_t* __restrict__ ntok) {
@@ -78,7 +78,6 @@ __global__ void __launch_bounds__(kScoreThreads, 4) score_kernel(StepParams p, c
     const int64_t rstride = p.nb_pad / V;         // Vec elements per dim row
     // two register batches of R rows (ping-pong): while one batch is consumed the
     // other is in flight, so 2R rows of this thread's blocks are always requested
-    constexpr int R = V == 2 ? 16 : 8;
     Vec bufA[R], bufB[R];
 #pragma unroll
     for (int u = 0; u < R; ++u)
@@ -457,6 +456,7 @@ __global__ void __launch_bounds__(NT, 1) topk_kernel(FuseArgs fa, StepParams p, 
     };
     int32_t* ids_out = out_ids + ((int64_t)bi * p.Hkv + h) * p.k;
     float* sc_out = out_scores ? out_scores + ((int64_t)bi * p.Hkv + h) * p.k : nullptr;
+    bool s_ready = false;                         // fused: S[] of the resolve already in smem
     if (compacted && mode != kModeEqual && p.k <= kTakeMax) {
         // ---- emission from the compacted list: every taken id is in it (above the bin, or a
         // taken member); its output position = number of taken ids (cluster-wide) below it
@@ -500,6 +500,18 @@ __global__ void __launch_bounds__(NT, 1) topk_kernel(FuseArgs fa, StepParams p, 
             for (int u = 0; u < tot; ++u) pos += all[u] < id ? 1 : 0;
             ids_out[pos] = id;
             if (sc_out) sc_out[pos] = __ldcg(sc + (id - base));
+        }
+        if (RESOLVE && crank == 0 && 2 * (int)fa.rb.nkeys + p.k <= span) {
+            // hand the sorted selection to the resolve in shared memory (its S[] slot; the
+            // keys are dead, `all` lies beyond it): no global re-read, no validation needed
+            int32_t* S = reinterpret_cast<int32_t*>(skey) + 2 * fa.rb.nkeys;
+            for (int j = tid; j < tot; j += NT) {
+                const int32_t id = all[j];
+                int pos = 0;
+                for (int u = 0; u < tot; ++u) pos += all[u] < id ? 1 : 0;
+                S[pos] = id;
+            }
+            s_ready = true;
         }
     } else {
     // ---- emission.  Warp w owns positions [w0, w1) and walks them in 32-wide strips: pre-pass
@@ -600,7 +612,7 @@ __global__ void __launch_bounds__(NT, 1) topk_kernel(FuseArgs fa, StepParams p, 
         cl_sync<CL>();
         if (crank != 0) return;
         uint8_t* smraw = reinterpret_cast<uint8_t*>(skey);
-        const int nm = resolve_main(p, fa.rb, bi, h, out_ids, fa.out_attn, smraw, rsm, true);
+        const int nm = resolve_main(p, fa.rb, bi, h, out_ids, fa.out_attn, smraw, rsm, true, s_ready);
         if (nm > 0 && fa.host_store) {
             const int32_t* S = reinterpret_cast<const int32_t*>(reinterpret_cast<uint64_t*>(smraw) + fa.rb.nkeys);
             gather_segment(p, bi, h, S + 2 * fa.rb.kmax, S + 3 * fa.rb.kmax, nm, fa.host_store, fa.slots);
@@ -608,10 +620,10 @@ __global__ void __launch_bounds__(NT, 1) topk_kernel(FuseArgs fa, StepParams p, 
     }
 }
 
-template <int V>
+template <int V, int R>
 static cudaError_t launch_score(kvd_cache* c, const StepParams& p, const uint16_t* q, cudaStream_t s) {
     const unsigned tiles = (unsigned)((c->nb_pad + kScoreThreads * V - 1) / (kScoreThreads * V));
-    return launch_pdl(score_kernel<V>, dim3(tiles, p.Hkv, p.B), dim3(kScoreThreads), 0, s, p, q,
+    return launch_pdl(score_kernel<V, R>, dim3(tiles, p.Hkv, p.B), dim3(kScoreThreads), 0, s, p, q,
                       (const uint16_t*)c->summ, c->scores, (const int32_t*)c->ntok_dev);
 }
 
@@ -682,6 +694,18 @@ static cudaError_t launch_topk(kvd_cache* c, const StepParams& p, int kpt, int32
     return e;
 }
 
+// score kernel variant: V = 2 blocks per thread with R = 16 rows per register batch (default);
+// KVD_SEL_V = 4 selects V = 4, R = 8 (experiments only; R = 32 spills)
+static cudaError_t launch_score_cfg(kvd_cache* c, const StepParams& p, const uint16_t* q, cudaStream_t s) {
+    static int var = -1;
+    if (var < 0) {
+        const char* v = getenv("KVD_SEL_V");
+        var = (v && atoi(v) == 4) ? 1 : 0;
+    }
+    if (var == 1) return launch_score<4, 8>(c, p, q, s);
+    return launch_score<2, 16>(c, p, q, s);
+}
+
 // Cluster size and keys per thread for a segment span of nb_pad blocks with nt threads per
 // CTA: at most 16 keys per thread while the cluster is small (clusters of whole-SM CTAs do not
 // all fit at once), at most 8 CTAs per cluster (portable), kpt a multiple of 4 (float4 staging).
@@ -719,12 +743,7 @@ static int topk_threads() {
 
 cudaError_t launch_select(kvd_cache* c, const StepParams& p, const uint16_t* q, int32_t* out_ids, float* out_scores,
                           cudaStream_t s) {
-    static int V = 0;
-    if (!V) {
-        const char* env = getenv("KVD_SEL_V");   // experiments only: blocks per scoring thread (2 or 4)
-        V = env && atoi(env) == 4 ? 4 : 2;
-    }
-    cudaError_t e = V == 4 ? launch_score<4>(c, p, q, s) : launch_score<2>(c, p, q, s);
+    cudaError_t e = launch_score_cfg(c, p, q, s);
     if (e != cudaSuccess || p.k == 0) return e != cudaSuccess ? e : cudaGetLastError();
     const FuseArgs fa{};
     const int nt = topk_threads();
@@ -738,12 +757,7 @@ cudaError_t launch_select(kvd_cache* c, const StepParams& p, const uint16_t* q, 
 // kvd_select_resolve_fetch: score_kernel, then the fused top-k + resolve + fetch kernel.
 cudaError_t launch_select_resolve(kvd_cache* c, const StepParams& p, const uint16_t* q, int32_t* out_ids,
                                   float* out_scores, int32_t* out_attn, cudaStream_t s) {
-    static int V = 0;
-    if (!V) {
-        const char* env = getenv("KVD_SEL_V");
-        V = env && atoi(env) == 4 ? 4 : 2;
-    }
-    cudaError_t e = V == 4 ? launch_score<4>(c, p, q, s) : launch_score<2>(c, p, q, s);
+    cudaError_t e = launch_score_cfg(c, p, q, s);
     if (e != cudaSuccess) return e;
     if (p.k == 0) return launch_resolve(c, p, out_ids, out_attn, s);   // nothing to select
     FuseArgs fa;

@@ -64,7 +64,7 @@ __device__ __forceinline__ void resolve_pre(const StepParams& p, const ResolveBu
 // griddepcontrol.wait.  Returns the miss count; M[] / dest[] (blocks / slots) stay in smraw.
 __device__ inline int resolve_main(const StepParams& p, const ResolveBufs& rb, int bi, int h,
                             const int32_t* __restrict__ ids, int32_t* __restrict__ out_attn, uint8_t* smraw,
-                            ResolveShared& rsm, bool launch_dependents) {
+                            ResolveShared& rsm, bool launch_dependents, bool s_ready = false) {
     const int r = p.req[bi];
     const int tid = threadIdx.x;
     const SegGeom g = seg_geom(rb.ntok[r], p.P, p.sink_tokens, p.local_tokens);
@@ -90,10 +90,11 @@ __device__ inline int resolve_main(const StepParams& p, const ResolveBufs& rb, i
     uint32_t* inS = reinterpret_cast<uint32_t*>(vtmp + rb.kmax);
 
     const int ns = g.sink_end, nl = g.nb - g.local_begin;
-    // ---- 1. load + validate the selection (ascending, in range, not pinned)
+    // ---- 1. load + validate the selection (ascending, in range, not pinned); s_ready: the
+    //         fused kernel already placed its own (valid by construction) ids in S[]
     if (tid == 0) rsm.bad = 0;
     __syncthreads();
-    for (int i = tid; i < k; i += blockDim.x) {
+    for (int i = s_ready ? k : tid; i < k; i += blockDim.x) {
         const int32_t b = __ldcg(&S_in[i]);
         S[i] = b;
         bool bad = b < g.sink_end || b >= g.local_begin || (i > 0 && __ldcg(&S_in[i - 1]) >= b);
@@ -112,7 +113,7 @@ __device__ inline int resolve_main(const StepParams& p, const ResolveBufs& rb, i
         const int i = base + tid;
         int hs = -1;
         if (i < k) {
-            hs = table[S[i]];
+            hs = rb.nkeys == 0 ? S[i] : table[S[i]];   // fully resident: block b lives in slot b (R14)
             hitslot[i] = hs;
         }
         const int is_miss = (i < k && hs < 0) ? 1 : 0;
