@@ -77,3 +77,29 @@ def test_no_gpu_create_fails_loudly():
         pytest.skip("GPU present")
     with pytest.raises(KVDError):
         KVCache(**dict(BASE, num_layers=1, max_requests=1, max_context=4096, slots_per_segment=256, max_select=32))
+
+
+def test_config_limits_of_this_build():
+    """Host-backed caches rank victims on chip (C <= ~27,000 at max_select 128) and the top-k
+    cluster holds <= 262,144 blocks per request; both are rejected up front (include/kvd.h)."""
+    with pytest.raises(KVDError):
+        KVCache.required_bytes(**dict(BASE, max_context=1 << 20, slots_per_segment=40000))
+    KVCache.required_bytes(**dict(BASE, max_context=1 << 20, slots_per_segment=16384))   # c4 fits
+    KVCache.required_bytes(**dict(BASE, max_context=1 << 20, slots_per_segment=1 << 16))  # resident
+    with pytest.raises(KVDError):
+        KVCache.required_bytes(**dict(BASE, block_tokens=1, max_context=300000, slots_per_segment=1 << 20))
+
+
+def test_step_calls_validate_before_launch():
+    """Every step call rejects a NULL cache synchronously (nothing launched) and the launch
+    counter does not move."""
+    L = lib()
+    n0 = L.kvd_launch_count()
+    q = ctypes.c_void_p(0)
+    reqs = (ctypes.c_int32 * 1)(0)
+    assert L.kvd_select_topk(None, 0, q, reqs, 1, 8, q, q, q) == 1
+    assert L.kvd_resolve_and_fetch(None, 0, reqs, 1, q, 8, 1, q, q) == 1
+    assert L.kvd_select_resolve_fetch(None, 0, q, reqs, 1, 8, 1, q, q, q, q) == 1
+    assert L.kvd_sparse_decode(None, 0, q, reqs, 1, q, 13, q, q, q) == 1
+    assert L.kvd_launch_count() == n0
+    assert b"NULL" in L.kvd_last_error() or b"null" in L.kvd_last_error()
