@@ -710,8 +710,13 @@ static cudaError_t launch_score_cfg(kvd_cache* c, const StepParams& p, const uin
 // CTA: at most 16 keys per thread while the cluster is small (clusters of whole-SM CTAs do not
 // all fit at once), at most 8 CTAs per cluster (portable), kpt a multiple of 4 (float4 staging).
 void topk_geometry(int64_t nb_pad, int nt, int* cl, int* kpt) {
+    static int kmax = 0;
+    if (!kmax) {
+        const char* env = getenv("KVD_TOPK_KPT");   // experiments only: keys per thread before growing the cluster
+        kmax = env && atoi(env) == 8 ? 8 : 16;
+    }
     int c = 1;
-    while (c < 8 && (int64_t)c * nt * 16 < nb_pad) c <<= 1;
+    while (c < 8 && (int64_t)c * nt * kmax < nb_pad) c <<= 1;
     int64_t per = (nb_pad + (int64_t)c * nt - 1) / ((int64_t)c * nt);
     per = (per + 3) / 4 * 4;
     *cl = c;
