@@ -474,6 +474,7 @@ __global__ void __launch_bounds__(NT, 1) topk_kernel(FuseArgs fa, StepParams p, 
             if (take) sm.take[atomicAdd(&sm.ntake, 1)] = (int32_t)(base + i);
         }
         cl_sync<CL>();
+        stamp(4);
         // gather the cluster's taken ids locally (p.k of them), then rank by id
         int off = 0, tot = 0;
 #pragma unroll
