@@ -4,7 +4,7 @@
 tag=${1:-p}; shift
 cfgs=${@:-c2 c3}
 mkdir -p gpurun_out
-K="regex:select_kernel|resolve_kernel|gather_kernel|attn_kernel"
+K="regex:score_kernel|topk_kernel|resolve_kernel|gather_kernel|attn_kernel"
 for c in $cfgs; do
   if [ $c = c2 ]; then skip=12; else skip=$((4*4*32)); fi
   timeout 600 /usr/local/cuda/bin/ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k "$K" -s $skip -c 60 --csv \
