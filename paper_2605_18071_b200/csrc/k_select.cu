@@ -373,7 +373,49 @@ __global__ void __launch_bounds__(NT, 1) topk_kernel(FuseArgs fa, StepParams p, 
         if (in && slot < kListCap) comp[slot] = make_uint2(key, (uint32_t)i | (b > bstar ? 0x80000000u : 0u));
     }
     cta_minmax<CL>(kmn, kmx, sm);                 // contains the barriers that publish ncomp
-    const bool compacted = sm.ncomp <= kListCap;  // uniform over the CTA
+    bool compacted = sm.ncomp <= kListCap;        // uniform over the CTA
+    // ---- clusters: when the cluster's compacted lists fit one list, rank 0 gathers them (ids
+    // made cluster-global) and finishes alone, with no further cluster barriers
+    bool local = false;
+    int64_t gbase = base;                         // id of local position 0 in the current lists
+    if constexpr (CL > 1) {
+        int tot_c = 0;
+        bool fit = true;
+#pragma unroll
+        for (int c = 0; c < CL; ++c) {
+            const int m = *cl_remote<CL>(&sm.ncomp, c);
+            tot_c += m;
+            fit = fit && m <= kListCap;
+        }
+        if (fit && tot_c <= kListCap && p.k <= kTakeMax) {   // uniform over the cluster
+            if (crank == 0) {
+                int o = sm.ncomp;                 // rank 0's own entries stay (its base is 0)
+                for (int c = 1; c < CL; ++c) {
+                    const uint2* rc = cg::this_cluster().map_shared_rank(comp, c);
+                    const int m = *cl_remote<CL>(&sm.ncomp, c);
+                    const uint32_t add = (uint32_t)c * (uint32_t)span;   // ids < 2^31: flag bit kept
+                    for (int j = tid; j < m; j += NT) {
+                        uint2 e = rc[j];
+                        e.y += add;
+                        comp[o + j] = e;
+                    }
+                    o += m;
+                }
+            }
+            cl_sync<CL>();                        // remote lists read: the other ranks are done
+            if (crank != 0) return;
+            if (tid == 0) sm.ncomp = tot_c;
+            __syncthreads();
+            local = true;
+            compacted = true;
+            gbase = 0;
+        }
+    }
+    const int ncl = local ? 1 : CL;               // CTAs whose shared memory is still consulted
+    auto csync = [&]() {
+        if (local) __syncthreads();
+        else cl_sync<CL>();
+    };
     const uint32_t diff = kmn ^ kmx;
     int lo = (kk != cnt && cnt > kTieList && diff) ? 32 - __clz(diff) : 0;   // bits [0, lo) still to resolve
     uint32_t mask = lo == 32 ? 0u : ~((1u << lo) - 1u);
@@ -408,11 +450,11 @@ __global__ void __launch_bounds__(NT, 1) topk_kernel(FuseArgs fa, StepParams p, 
                               i >= c_lo && i < c_hi && bin_at(i) == bstar && (key & mask) == prefix);
             }
         }
-        cl_sync<CL>();
+        csync();
         if (tid < nbins) {
             int t = 0;
 #pragma unroll
-            for (int c = 0; c < CL; ++c) t += cl_remote<CL>(hb, c)[tid];
+            for (int c = 0; c < ncl; ++c) t += cl_remote<CL>(hb, c)[tid];
             sm.tot[tid] = t;
         }
         __syncthreads();
@@ -430,7 +472,7 @@ __global__ void __launch_bounds__(NT, 1) topk_kernel(FuseArgs fa, StepParams p, 
         auto add = [&](uint32_t key, int i) {
             const int slot = atomicAdd(&sm.lcount, 1);
             sm.lkey[slot] = key;
-            sm.lid[slot] = (int32_t)(base + i);
+            sm.lid[slot] = (int32_t)(gbase + i);
         };
         if (compacted) {
             for (int j = tid; j < sm.ncomp; j += NT)
@@ -439,12 +481,12 @@ __global__ void __launch_bounds__(NT, 1) topk_kernel(FuseArgs fa, StepParams p, 
             for (int i = c_lo + tid; i < c_hi; i += NT)
                 if (bin_at(i) == bstar && (skey[i] & mask) == prefix) add(skey[i], i);
         }
-        cl_sync<CL>();
+        csync();
     }
     auto bin_rank = [&](uint32_t key, int32_t id) {   // members beating (key, id)
         int rank = 0;
 #pragma unroll 1
-        for (int c = 0; c < CL; ++c) {
+        for (int c = 0; c < ncl; ++c) {
             TopkShared* rs = cl_remote<CL>(&sm, c);
             const int m = rs->lcount;
             for (int j = 0; j < m; ++j) {
@@ -457,7 +499,7 @@ __global__ void __launch_bounds__(NT, 1) topk_kernel(FuseArgs fa, StepParams p, 
     int32_t* ids_out = out_ids + ((int64_t)bi * p.Hkv + h) * p.k;
     float* sc_out = out_scores ? out_scores + ((int64_t)bi * p.Hkv + h) * p.k : nullptr;
     bool s_ready = false;                         // fused: S[] of the resolve already in smem
-    if (compacted && mode != kModeEqual && p.k <= kTakeMax) {
+    if (compacted && (mode != kModeEqual || local) && p.k <= kTakeMax) {
         // ---- emission from the compacted list: every taken id is in it (above the bin, or a
         // taken member); its output position = number of taken ids (cluster-wide) below it
         if (tid == 0) sm.ntake = 0;
@@ -469,16 +511,27 @@ __global__ void __launch_bounds__(NT, 1) topk_kernel(FuseArgs fa, StepParams p, 
             bool take = e.y >> 31;
             if (!take) {
                 const uint32_t km = e.x & mask;
-                take = km > prefix || (km == prefix && (mode == kModeWhole || bin_rank(e.x, (int32_t)(base + i)) < kk));
+                if (km > prefix || (km == prefix && mode == kModeWhole)) {
+                    take = true;
+                } else if (km == prefix && mode == kModeList) {
+                    take = bin_rank(e.x, (int32_t)(gbase + i)) < kk;
+                } else if (km == prefix) {        // kModeEqual (local finish only): lowest ids first
+                    int r = 0;
+                    for (int u = 0; u < nc; ++u) {
+                        const uint2 f = comp[u];
+                        r += (!(f.y >> 31) && (f.x & mask) == prefix && (int)(f.y & 0x7FFFFFFFu) < i) ? 1 : 0;
+                    }
+                    take = r < kk;
+                }
             }
-            if (take) sm.take[atomicAdd(&sm.ntake, 1)] = (int32_t)(base + i);
+            if (take) sm.take[atomicAdd(&sm.ntake, 1)] = (int32_t)(gbase + i);
         }
-        cl_sync<CL>();
+        csync();
         stamp(4);
         // gather the cluster's taken ids locally (p.k of them), then rank by id
         int off = 0, tot = 0;
 #pragma unroll
-        for (int c = 0; c < CL; ++c) {
+        for (int c = 0; c < ncl; ++c) {
             const int m = *cl_remote<CL>(&sm.ntake, c);
             off += c < crank ? m : 0;
             tot += m;
@@ -487,7 +540,7 @@ __global__ void __launch_bounds__(NT, 1) topk_kernel(FuseArgs fa, StepParams p, 
         __syncthreads();
         {
             int o = 0;
-            for (int c = 0; c < CL; ++c) {
+            for (int c = 0; c < ncl; ++c) {
                 const TopkShared* rs = cl_remote<CL>(&sm, c);
                 const int m = rs->ntake;
                 for (int j = tid; j < m; j += NT) all[o + j] = rs->take[j];
@@ -550,10 +603,10 @@ __global__ void __launch_bounds__(NT, 1) topk_kernel(FuseArgs fa, StepParams p, 
         sm.woff[warp][lane] = incl - v;
         if (lane == 31) sm.ctot[warp] = incl;
     }
-    cl_sync<CL>();
+    csync();
     int before_gt = 0, before_eq = 0;
 #pragma unroll
-    for (int c = 0; c < CL; ++c) {
+    for (int c = 0; c < ncl; ++c) {
         if (c < crank) {
             before_gt += *cl_remote<CL>(&sm.ctot[0], c);
             before_eq += *cl_remote<CL>(&sm.ctot[1], c);
@@ -567,7 +620,7 @@ __global__ void __launch_bounds__(NT, 1) topk_kernel(FuseArgs fa, StepParams p, 
     if (mode == kModeList) {
         // taken bin members at positions before this warp's range (ids ascend with positions)
         int t = 0;
-        for (int c = 0; c < CL; ++c) {
+        for (int c = 0; c < ncl; ++c) {
             TopkShared* rs = cl_remote<CL>(&sm, c);
             for (int j = lane; j < rs->lcount; j += 32) {
                 const int32_t id = rs->lid[j];
@@ -587,14 +640,14 @@ __global__ void __launch_bounds__(NT, 1) topk_kernel(FuseArgs fa, StepParams p, 
         bool take_eq = false;
         if (mode == kModeWhole) take_eq = eq;
         else if (mode == kModeEqual) take_eq = eq && eq_before + __popc(beq & lt) < kk;
-        else if (eq) take_eq = bin_rank(skey[i], (int32_t)(base + i)) < kk;
+        else if (eq) take_eq = bin_rank(skey[i], (int32_t)(gbase + i)) < kk;
         const uint32_t btk = __ballot_sync(0xffffffffu, take_eq);
         const int eq_taken_before = mode == kModeWhole ? eq_before
                                   : mode == kModeEqual ? min(eq_before, kk)
                                                        : taken_eq_before;
         if (gt || take_eq) {
             const int pos = gt_before + eq_taken_before + __popc((bgt | btk) & lt);
-            ids_out[pos] = (int32_t)(base + i);
+            ids_out[pos] = (int32_t)(gbase + i);
             if (sc_out) sc_out[pos] = __ldcg(sc + i);
         }
         gt_before += __popc(bgt);
@@ -606,11 +659,11 @@ __global__ void __launch_bounds__(NT, 1) topk_kernel(FuseArgs fa, StepParams p, 
     stamp(6, 1000ull * mode + (32 - lo) + (compacted ? 100 : 0));
     if constexpr (!RESOLVE) {
         griddep_launch();
-        if (CL > 1) cl_sync<CL>();               // remote readers of this CTA's shared memory are done
+        if (CL > 1 && !local) cl_sync<CL>();     // remote readers of this CTA's shared memory are done
     } else {
         // every CTA's ids are written (cluster barrier: release / acquire) and no CTA reads
         // another's shared memory any more; rank 0 resolves and fetches
-        cl_sync<CL>();
+        csync();
         if (crank != 0) return;
         uint8_t* smraw = reinterpret_cast<uint8_t*>(skey);
         const int nm = resolve_main(p, fa.rb, bi, h, out_ids, fa.out_attn, smraw, rsm, true, s_ready);
