@@ -174,12 +174,16 @@ kvd_status kvd_resolve_and_fetch(kvd_cache* c, int32_t layer, const int32_t* req
                                  int32_t B, const int32_t* ids, int32_t k_blocks,
                                  uint32_t step, int32_t* out_attn, kvd_stream stream);
 
-/* (1)+(2) fused: exactly kvd_select_topk followed by kvd_resolve_and_fetch (same
- * arguments, same results, same cache state, bit for bit), but the top-k, the
- * resolve and the miss fetch of a segment run in one kernel (one thread-block
- * cluster per segment; rank 0 resolves and copies the misses), so the step has
- * no kernel boundary between selection and fetch.  out_ids is still written.
- * Errors as for the two calls. */
+/* (1)+(2) fused -- "identifying critical KV entries via the index" then "fetching
+ * the selected entries from DRAM".  Exactly kvd_select_topk
+ * followed by kvd_resolve_and_fetch: same arguments (q, req_ids, B, k_blocks as for
+ * select; step as for resolve), same results, same cache state, bit for bit.  The
+ * top-k, the resolve and the miss fetch of a segment run in one kernel (one
+ * thread-block cluster per segment; rank 0 resolves and copies the misses), so the
+ * step has no kernel boundary between selection and fetch.  out_ids (device int32
+ * [B][Hkv][k_blocks]) and out_scores (or NULL) are written as by select; out_attn
+ * as by resolve.  Caller owns every buffer; asynchronous on `stream`.  Errors as for
+ * the two calls (validated synchronously; nothing launched on error). */
 kvd_status kvd_select_resolve_fetch(kvd_cache* c, int32_t layer, const uint16_t* q,
                                     const int32_t* req_ids, int32_t B, int32_t k_blocks,
                                     uint32_t step, int32_t* out_ids, float* out_scores,
