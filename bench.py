@@ -1,26 +1,38 @@
 """bench.py — decode-step throughput of the KVDrive hot path on B200 (libkvd).
 
 One "step" = one decode token for every request of the batch through all L
-layers: per layer, kvd_select_resolve_fetch (a1+a2+a3+a4: score kernel, then
-one fused top-k + resolve + fetch kernel; --unfused: kvd_select_topk then
-kvd_resolve_and_fetch) -> kvd_sparse_decode (a5+a6), layers serially
-(DESIGN.md §2).  The per-kernel roofline pass times the three separate calls.  The whole step
+layers: per layer, kvd_select_resolve_fetch (a1+a2+a3+a4: one kernel scores the
+block summaries, selects the top-k, resolves them against the GPU cache and
+copies the misses from pinned host DRAM; --unfused: kvd_select_topk then
+kvd_resolve_and_fetch) -> kvd_sparse_decode (a5+a6: split-K attention with the
+LSE merge in the same kernel), layers serially.  The whole step
 is captured once as a CUDA graph and replayed; the decode-step index lives in
 device memory (kvd_set_device_step) so every replay is a new step.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3]
     python bench.py --impl reference ...   # the CPU oracle on a bounded sample
 
-Multi-GPU (torchrun, one process per GPU): (request, KV-head) units are
-independent through every row, so every rank serves its own
-B requests (global batch N*B, weak scaling) with no collective on the decode
-path; the only collectives are the timing barrier and the max-over-ranks.
+Multi-GPU: one process per GPU (self-launched through torch.distributed.run when
+--gpus N > 1 and WORLD_SIZE is unset).  (request, KV-head) units are independent
+through every row: "weak" sharding gives every rank its own B
+requests; "strong" partitions the config's B*Hkv units over the ranks (whole
+requests when N divides B: no collective at all; otherwise head ranges, and one
+NCCL all-gather of the step's fp32 outputs).  c4 / c5 default to strong.
 
 Inputs are seeded synthetic Llama-3.1-8B / Qwen2.5-1M-shaped K/V/queries
 (synth/), resident in HBM (or in the pinned host store for the
 host-backed configs) before the timed region.  Every step touches far more
 than the 126 MB L2 (3.3 GB at c2, 13 GB + host fetches at c3), so no flush is
 needed ("l2": "inputs larger than L2").
+
+Measurement: the timed region replays the step graph K times
+between CUDA events on the launching stream (max over ranks).  The graph's
+kernels carry libkvd's device-side kernel timer (kvd_enable_kernel_timer), so
+every kernel's launch duration is measured on the path that is timed; the same
+graph without the timer is replayed right after as a check.  The roofline is
+reported for the resource that binds the step (algorithmic bytes per step of
+that resource / ms_per_step) and per kernel (algorithmic bytes per launch /
+average launch duration).
 """
 import argparse
 import json
@@ -32,48 +44,32 @@ import time
 
 import numpy as np
 
-
-def ncu_traffic(config, bound, dom):
-    """DRAM bytes per ABI call (scaled per segment) from the committed ncu capture, or None."""
-    if bound != "hbm":
-        return None
-    import glob
-    files = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "*_ncu_traffic.json")))
-    if not files:
-        return None
-    try:
-        d = json.load(open(files[-1]))
-        e = d[config][dom]
-        return {"bytes_per_call": e["dram_bytes_per_call"], "segments": e["segments"],
-                "source": f"{os.path.basename(files[-1])}: {e['kernels']}"}
-    except (KeyError, ValueError, OSError):
-        return None
-
-
-def kvd_launch_count():
-    from paper_2605_18071_b200 import kvd
-    return int(kvd.lib().kvd_launch_count())
-
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-# BASELINE.json configs (DESIGN.md §4): per-rank shapes.
+# BASELINE.json configs.  B is the config's batch (per rank for weak scaling).
 CONFIGS = {
-    "c1": dict(chains=1, L=1, B=1, Hq=8, Hkv=2, n=4096, P=16, k=32, C=None, alias=0,
+    "c1": dict(chains=1, L=1, B=1, Hq=8, Hkv=2, n=4096, P=16, k=32, C=None, alias=0, shard="weak",
                desc="1 req, 1 layer, 8q/2kv, d128, 4k ctx, block 16, top-k 32, resident"),
-    "c2": dict(chains=8, L=32, B=8, Hq=32, Hkv=8, n=32768, P=16, k=128, C=None, alias=0,
+    "c2": dict(chains=8, L=32, B=8, Hq=32, Hkv=8, n=32768, P=16, k=128, C=None, alias=0, shard="weak",
                desc="Llama-3.1-8B shapes (32 layers, 32q/8kv, d128) bf16, 32k ctx, batch 8, top-k 2048 tokens, resident"),
-    "c3": dict(chains=16, L=32, B=16, Hq=32, Hkv=8, n=131072, P=16, k=128, C=2048, alias=4,
+    "c3": dict(chains=16, L=32, B=16, Hq=32, Hkv=8, n=131072, P=16, k=128, C=2048, alias=4, shard="weak",
                desc="Llama-3.1-8B shapes, 128k ctx, batch 16, GPU cache 25% of KV (2048 slots/segment), misses "
                     "gathered from pinned host DRAM, top-k 2048 tokens"),
-    "c4": dict(chains=4, L=28, B=4, Hq=28, Hkv=4, n=1 << 20, P=16, k=128, C=16384, alias=2,
+    "c4": dict(chains=4, L=28, B=4, Hq=28, Hkv=4, n=1 << 20, P=16, k=128, C=16384, alias=2, shard="strong",
                desc="Qwen2.5-7B-1M shapes (28 layers, 28q/4kv, d128), 1M ctx, batch 4, GPU cache 25%, host-backed"),
-    "c5": dict(chains=16, L=32, B=64, Hq=32, Hkv=8, n=131072, P=16, k=128, C=768, alias=2,
-               desc="Llama-3.1-8B shapes, 128k ctx, batch 64, GPU cache 768 slots/segment (9.4%), host-backed"),
+    "c4k": dict(chains=4, L=28, B=4, Hq=28, Hkv=4, n=1 << 20, P=16, k=1024, C=16384, alias=2, shard="strong",
+                desc="c4 with top-k 1024 blocks (16384 tokens = 1.56% of 1M, SURVEY 8.2)"),
+    "c5": dict(chains=16, L=32, B=64, Hq=32, Hkv=8, n=131072, P=16, k=128, C=768, alias=2, shard="strong",
+               desc="Llama-3.1-8B shapes, 128k ctx, batch 64 partitioned over the GPUs, GPU cache 768 "
+                    "slots/segment (9.4%), host-backed"),
 }
 METRIC = "decode tokens/s at 128k ctx; sparse-attn HBM GB/s % peak; fetch GB/s, 1-8 GPU"
 RECORD = 8192           # bytes of one 16-token K||V block record (bf16)
 SUMMARY = 256           # bytes of one block summary (128 bf16)
+KINDS = ("select", "resolve", "gather", "attn")
+KIND_NAMES = {"select": "select_kernel (a1+a2; fused: +a3+a4)", "resolve": "resolve_kernel (a3)",
+              "gather": "gather_kernel (a4)", "attn": "attn_kernel (a5+a6)"}
 
 
 def parse(argv=None):
@@ -85,7 +81,7 @@ def parse(argv=None):
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--policy", default="la", choices=["lru", "lfu", "la"])
     ap.add_argument("--alpha", type=float, default=0.9)
-    ap.add_argument("--alias", type=int, default=None, help="host-layer alias A (layer l uses synthetic layer l %% A)")
+    ap.add_argument("--alias", type=int, default=None, help="host-layer alias A (layer l uses the K/V of layer l %% A)")
     ap.add_argument("--fill", type=int, default=None, help="untimed cache-fill steps before warm-up")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
@@ -94,15 +90,15 @@ def parse(argv=None):
     ap.add_argument("--chains", type=int, default=None,
                     help="micro-batch chains (SFC overlap): the batch is split into this many request groups, "
                          "each run through all layers on its own stream inside the graph")
-    ap.add_argument("--shard", default="requests", choices=["requests", "heads"],
-                    help="multi-GPU unit assignment: 'requests' = every rank serves its own B requests (weak "
-                         "scaling, no collective); 'heads' = the config's B*Hkv units are partitioned over the "
-                         "ranks (strong scaling; SURVEY 8.6) and the fp32 outputs are all-gathered each step")
+    ap.add_argument("--shard", default=None, choices=["weak", "strong"],
+                    help="multi-GPU unit assignment (default per config): 'weak' = every rank serves its own B "
+                         "requests; 'strong' = the config's B*Hkv units are partitioned over the ranks")
     ap.add_argument("--unfused", action="store_true",
                     help="step through kvd_select_topk + kvd_resolve_and_fetch instead of the fused "
                          "kvd_select_resolve_fetch (same results)")
     ap.add_argument("--layers", type=int, default=None, help="override L (profiling only; not a bench number)")
-    ap.add_argument("--cpu-sample-s", type=float, default=12.0, help="target seconds of oracle work")
+    ap.add_argument("--cpu-sample-s", type=float, default=6.0, help="target seconds per oracle sample")
+    ap.add_argument("--master-port", type=int, default=29531, help="self-launch rendezvous port (N > 1)")
     return ap.parse_args(argv)
 
 
@@ -113,17 +109,52 @@ def dist_env():
     return rank, world, local
 
 
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
 # ---------------------------------------------------------------- algorithmic bytes
-def per_segment_bytes(cfg, misses_per_seg=0.0):
+def per_segment_bytes(cfg, misses_per_seg=0.0, victims=True):
+    """Algorithmic bytes per segment per step, by row."""
     nb = (cfg["n"] + cfg["P"] - 1) // cfg["P"]
     G = cfg["Hq"] // cfg["Hkv"]
     k = cfg["k"]
+    C = cfg["C"] if cfg["C"] is not None else nb
     p = 1 + (64 + cfg["P"] - 1) // cfg["P"]          # sink block + local blocks (n % P == 0)
+    resident = C >= nb
     return dict(
         select=SUMMARY * nb + 2 * G * 128 + 8 * k,          # summaries + q + (ids, scores)
+        resolve=4 * k + (0 if resident or not victims else 13 * C + 4 * C),   # table probes + victim scan (LA)
         attn=RECORD * (k + p) + 2 * G * 128 + 4 * G * 128 + 4 * G,   # K/V pages + q + o + lse
         fetch=RECORD * misses_per_seg,                     # host link read (and HBM write)
     )
+
+
+def load_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def ncu_traffic(config, kind):
+    """Per-launch DRAM / PCIe bytes of one kernel kind from the committed ncu capture
+    (profiles/*_ncu_traffic.json, written by tools/ncu_traffic.py), per segment."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_traffic.json")))
+    if not files:
+        return None
+    try:
+        d = json.load(open(files[-1]))
+        e = d[config][kind]
+        e = dict(e)
+        e["source"] = os.path.basename(files[-1])
+        return e
+    except (KeyError, ValueError, OSError):
+        return None
 
 
 # ---------------------------------------------------------------- clocks
@@ -172,40 +203,43 @@ class ClockSampler:
 
 # ---------------------------------------------------------------- the GPU arm
 class Runner:
-    def __init__(self, args, cfg, rank, dev):
+    def __init__(self, args, cfg, rank, dev, world=None):
         import torch
         import synth
         from paper_2605_18071_b200 import KVCache
+        from paper_2605_18071_b200 import dist as kdist
         self.torch, self.args, self.cfg, self.rank, self.dev = torch, args, cfg, rank, dev
+        world = world if world is not None else int(os.environ.get("WORLD_SIZE", "1"))
         L, B, Hq, Hkv, n, P, k = (cfg[x] for x in ("L", "B", "Hq", "Hkv", "n", "P", "k"))
         self.G = G = Hq // Hkv
         nb = (n + P - 1) // P
         C = cfg["C"] if cfg["C"] is not None else nb
-        A = args.alias if args.alias is not None else cfg["alias"]
-        A = A if (A and A < L) else L
-        if C < nb and args.alias is None:
-            # keep every rank's pinned host store under ~40 % of the box's RAM (all ranks share it)
-            world_ = int(os.environ.get("WORLD_SIZE", "1"))
-            per_layer = cfg["B"] * cfg["Hkv"] * nb * RECORD
-            ram = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
-            A = max(1, min(A, int(0.4 * ram / world_ // per_layer)))
-        self.A = A
         self.resident = C >= nb
-        from paper_2605_18071_b200 import dist as kdist
-        world = int(os.environ.get("WORLD_SIZE", "1"))
-        self.mode = getattr(args, "shard", "requests")
+        # ---- this rank's units
+        self.shard = args.shard or cfg.get("shard", "weak")
         self.h0 = 0
-        if self.mode == "heads":
-            # strong scaling: this rank owns heads h0..h1-1 of some of the config's B requests
+        self.gather = False                       # heads split: all-gather the step's outputs
+        if self.shard == "strong" and world > 1:
             self.all_parts = kdist.unit_partition(B, Hkv, world)
             self.greqs, self.h0, h1 = kdist.rank_heads(self.all_parts[rank])
+            self.gather = not kdist.whole_requests(self.all_parts, Hkv)
             Hkv = h1 - self.h0
             Hq = Hkv * G
             B = len(self.greqs)
         else:
-            self.greqs = kdist.rank_requests(rank, world, B)   # synthetic identity of this rank's requests
+            self.greqs = kdist.rank_requests(rank, world, B) if world > 1 else list(range(B))
         self.B, self.Hkv, self.Hq = B, Hkv, Hq                  # this rank's (local) shapes
         self.reqs = list(range(B))
+        # ---- host-layer alias A: the pinned host store holds A layers; layer l's K/V are the
+        # synthetic layer l % A's (queries stay per layer: own random streams)
+        A = args.alias if args.alias is not None else cfg["alias"]
+        A = A if (A and A < L) else L
+        if not self.resident and args.alias is None:
+            # keep every rank's pinned host store under ~40 % of the box's RAM (all ranks share it)
+            per_layer = B * Hkv * nb * RECORD
+            ram = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
+            A = max(1, min(A, int(0.4 * ram / world // per_layer)))
+        self.A = A
         self.cache = KVCache(num_layers=L, num_q_heads=Hq, num_kv_heads=Hkv, block_tokens=P, max_requests=B,
                              max_context=n, slots_per_segment=C, max_select=k, sink_tokens=4, local_tokens=64,
                              policy=args.policy, host_layer_alias=(0 if self.A == L else self.A), device=dev.index)
@@ -221,14 +255,14 @@ class Runner:
         del Kd, Vd
         torch.cuda.synchronize(dev)
         self.setup_s = time.time() - t0
-        # queries for every step of the run, per synthetic layer: [T][L][B][Hq][128]
+        # queries for every step of the run: [T][L][B][Hq][128]; layer l follows the key topics
+        # of its K/V (synthetic layer l % A) with its own random streams (stream layer l)
         self.fill = max(1, args.fill if args.fill is not None else (1 if self.resident else max(4, 2 * C // k)))
-        self.T = self.fill + args.warmup + 3 * args.steps + 2
+        self.T = min(self.fill + args.warmup + 3 * args.steps + 2, 256)
         Hkv_all = cfg["Hkv"]
-        qs = [synth.batch_queries(args.seed, sl, self.greqs, Hkv_all, G, t0=0, nsteps=self.T,
-                                  alpha=args.alpha)[:, :, self.h0 * G:(self.h0 + Hkv) * G]
-              for sl in range(self.A)]
-        qh = np.stack([qs[l % self.A] for l in range(L)], axis=1)        # [T][L][B][Hq][128]
+        qh = np.stack([synth.batch_queries(args.seed, l % self.A, self.greqs, Hkv_all, G, t0=0, nsteps=self.T,
+                                           alpha=args.alpha, stream_layer=l)[:, :, self.h0 * G:(self.h0 + Hkv) * G]
+                       for l in range(L)], axis=1)
         self.q_host = torch.from_numpy(qh.view(np.int16)).pin_memory()
         self.q_dev = self.q_host.to(dev)
         self.q_cur = torch.empty_like(self.q_dev[0])
@@ -247,13 +281,16 @@ class Runner:
         self.fused = not args.unfused
         self.launches_per_step = None  # counted by libkvd (kvd_launch_count) over one eager step / the capture
 
-    # one layer of one chain (requests b0..b1-1) through the three ABI calls
+    def row(self):
+        return self.t % self.T
+
+    # one layer of one chain (requests b0..b1-1) through the ABI calls
     def layer(self, l, s, step=0, chain=None):
         c, k = self.cache, self.cfg["k"]
         b0, b1 = chain if chain else (0, len(self.reqs))
         reqs = self.reqs[b0:b1]
         q = self.q_cur[l, b0:b1]
-        if self.fused:   # kvd_select_resolve_fetch: top-k, resolve and fetch with no kernel boundary
+        if self.fused:   # kvd_select_resolve_fetch: score, top-k, resolve and fetch in one kernel
             c.select_resolve_fetch(l, q, reqs, k, step, self.ids[l, b0:b1], self.attn[l, b0:b1], stream=s)
         else:
             c.select_topk(l, q, reqs, k, self.ids[l, b0:b1], None, stream=s)
@@ -263,12 +300,13 @@ class Runner:
     def eager_step(self, s):
         torch = self.torch
         with torch.cuda.stream(s):
-            self.q_cur.copy_(self.q_dev[self.t], non_blocking=True)
+            self.q_cur.copy_(self.q_dev[self.row()], non_blocking=True)
         self.t += 1
         self.cache.set_device_step(None)
         n0 = kvd_launch_count()
         for l in range(self.cfg["L"]):
-            self.layer(l, s, step=self.t)
+            for ch in self.chains:                # the graph's launches, serialised on one stream
+                self.layer(l, s, step=self.t, chain=ch)
         self.launches_per_step = kvd_launch_count() - n0
 
     def capture(self, s):
@@ -288,33 +326,39 @@ class Runner:
             for cs in self.chain_streams:
                 s.wait_stream(cs)
         self.launches_per_step = kvd_launch_count() - n0
-        self.graph = g
+        return g
 
     def prepare_graph(self, s):
         """Capture the step graph; the device step counter continues from the eager steps."""
         torch = self.torch
         self.step_dev.fill_(self.t)
         torch.cuda.synchronize(self.dev)
-        self.capture(s)
+        self.graph = self.capture(s)
 
     def graph_step(self, s, source="dev"):
         torch = self.torch
         with torch.cuda.stream(s):
             if source == "dev":
-                self.q_cur.copy_(self.q_dev[self.t], non_blocking=True)
+                self.q_cur.copy_(self.q_dev[self.row()], non_blocking=True)
             else:
-                self.q_cur.copy_(self.q_host[self.t], non_blocking=True)
+                self.q_cur.copy_(self.q_host[self.row()], non_blocking=True)
             self.graph.replay()
             if source != "dev":
                 self.out_host.copy_(self.out, non_blocking=True)
         self.t += 1
 
 
+def kvd_launch_count():
+    from paper_2605_18071_b200 import kvd
+    return int(kvd.lib().kvd_launch_count())
+
+
 def run_gpu(args):
     import torch
     import torch.distributed as dist
     rank, world, local = dist_env()
-    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -322,33 +366,26 @@ def run_gpu(args):
     from paper_2605_18071_b200 import build as kb
     if rank == 0 or not os.path.exists(kb.SO):
         kb.build()
+    if world > 1:
+        dist.barrier()
     import synth
     synth.build_gpu()
     cfg = dict(CONFIGS[args.config])
     if args.layers:
         cfg["L"] = args.layers
+    from paper_2605_18071_b200 import dist as kdist
 
     def barrier():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize(dev)
 
-    from paper_2605_18071_b200 import dist as kdist
-
-    def max_over_ranks(x):
-        return kdist.max_over_ranks(x, dev)
-
-    def sum_over_ranks(x):
-        return kdist.sum_over_ranks(x, dev)
-
-    R = Runner(args, cfg, rank, dev)
+    R = Runner(args, cfg, rank, dev, world)
     s = torch.cuda.Stream(device=dev)
     L, B, Hkv = cfg["L"], R.B, R.Hkv                          # this rank's shapes
     segs_per_layer = B * Hkv
-    heads_mode = R.mode == "heads" and world > 1
-    # all_gather_into_tensor output: per-rank outputs concatenated along dim 0 ([world*L][B_r][Hq_r][128])
     gathered = (torch.empty((world * R.out.shape[0],) + tuple(R.out.shape[1:]), dtype=R.out.dtype, device=dev)
-                if heads_mode else None)
+                if R.gather else None)
 
     def gather_outputs():
         # head sharding: the step's per-rank fp32 outputs -> every rank (NCCL over NVLink)
@@ -358,15 +395,26 @@ def run_gpu(args):
     for _ in range(R.fill):
         R.eager_step(s)
     s.synchronize()
-    # capture one step as a CUDA graph (the step index is read on the device)
-    if not args.no_graph:
-        R.prepare_graph(s)
     step_fn = (lambda: R.eager_step(s)) if args.no_graph else (lambda: R.graph_step(s))
 
     def run():
         step_fn()
-        if heads_mode:
+        if R.gather:
             gather_outputs()
+
+    def timed_steps(k):
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for _ in range(k):
+            run()
+        e1.record(s)
+        e1.synchronize()
+        barrier()
+        return e0.elapsed_time(e1) / k
+    # capture the step (the step index is read on the device)
+    if not args.no_graph:
+        R.prepare_graph(s)
     clk = ClockSampler(local)          # sampled from warm-up through the e2e pass (GPU busy throughout)
     clk.start()
     for _ in range(args.warmup):
@@ -374,94 +422,105 @@ def run_gpu(args):
     s.synchronize()
     R.cache.reset_stats()
     # ---- timed region: K steps, device-timed on the launching stream
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    barrier()
-    ev0.record(s)
-    for _ in range(args.steps):
-        run()
-    ev1.record(s)
-    ev1.synchronize()
-    barrier()
-    ms = ev0.elapsed_time(ev1) / args.steps
+    ms = timed_steps(args.steps)
     st = R.cache.stats()
-    ms_max = max_over_ranks(ms)
-    # whole-job tokens: requests mode sums every rank's requests; heads mode counts each
-    # of the config's requests once (its heads are spread over the ranks)
-    tokens = cfg["B"] * args.steps if heads_mode else sum_over_ranks(B * args.steps)
-    value = tokens / (ms_max * args.steps * 1e-3)
+    ms_max = kdist.max_over_ranks(ms, dev)
+    # whole-job tokens: every rank's requests once (strong mode: a request split over head
+    # ranges is counted once)
+    tokens_per_step = cfg["B"] if (R.shard == "strong" and world > 1) else kdist.sum_over_ranks(B, dev)
+    value = tokens_per_step / (ms_max * 1e-3)
     hit_rate = st["hits"] / max(1, st["selected"])
     misses_per_seg = st["misses"] / max(1, args.steps * L * segs_per_layer)
 
-    # ---- per-kernel pass: the same steps, each ABI call bracketed by CUDA events on the
-    # launching stream.  A GPU spin (torch.cuda._sleep) gates each step so the host has
-    # queued every launch before the device starts: the events then see device time only.
-    kt = {"select": 0.0, "resolve_fetch": 0.0, "attn": 0.0}
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(L)]
-    npk = args.steps
-    R.cache.set_device_step(None)
-    for _ in range(npk):
-        with torch.cuda.stream(s):
-            torch.cuda._sleep(20_000_000)            # ~10 ms at 1.965 GHz: covers the host enqueue
-            R.q_cur.copy_(R.q_dev[R.t], non_blocking=True)
-        R.t += 1
-        c = R.cache
-        for l in range(L):
-            e = evs[l]
-            e[0].record(s)
-            c.select_topk(l, R.q_cur[l], R.reqs, cfg["k"], R.ids[l], None, stream=s)
-            e[1].record(s)
-            c.resolve_and_fetch(l, R.reqs, R.ids[l], cfg["k"], R.t, R.attn[l], stream=s)
-            e[2].record(s)
-            c.sparse_decode(l, R.q_cur[l], R.reqs, R.attn[l], R.W, R.out[l], R.lse[l], stream=s)
-            e[3].record(s)
-        s.synchronize()
-        for l in range(L):
-            e = evs[l]
-            kt["select"] += e[0].elapsed_time(e[1])
-            kt["resolve_fetch"] += e[1].elapsed_time(e[2])
-            kt["attn"] += e[2].elapsed_time(e[3])
-    nl = npk * L
-    per_launch_ms = {key: v / nl for key, v in kt.items()}
+    # ---- per-kernel launch durations: the same step graph re-captured with libkvd's device-side
+    # kernel timer on (kvd_enable_kernel_timer: no event node between the kernels), K steps
+    R.cache.enable_kernel_timer(True)
+    if not args.no_graph:
+        R.prepare_graph(s)
+    for _ in range(2):
+        run()
+    R.cache.enable_kernel_timer(True)             # zero the accumulators (synchronises)
+    ms_timer = kdist.max_over_ranks(timed_steps(args.steps), dev)
+    kt = R.cache.read_kernel_timer()
+    R.cache.enable_kernel_timer(False)
+    if not args.no_graph:
+        R.prepare_graph(s)                        # the plain graph again (e2e pass)
+
+    # ---- rooflines
     b = per_segment_bytes(cfg, misses_per_seg)
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except Exception:
-        pass
+    peaks = load_peaks()
     hbm_peak = peaks.get("hbm_gbs") or 6650.0
     hbm_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if peaks.get("hbm_gbs") else "fallback (B200_PROFILING.md)"
-    link = host_link_probe(torch, dev) if not R.resident else None
-    kernels = {}
-    for key, by in (("select", b["select"]), ("attn", b["attn"])):
-        gbs = by * segs_per_layer / (per_launch_ms[key] * 1e-3) / 1e9
-        kernels[key] = {"ms_per_launch": per_launch_ms[key], "bytes_per_launch": by * segs_per_layer,
-                        "gbs": gbs, "frac_hbm": gbs / hbm_peak}
-    fetch_bytes = b["fetch"] * segs_per_layer
-    kernels["resolve_fetch"] = {"ms_per_launch": per_launch_ms["resolve_fetch"], "host_bytes_per_launch": fetch_bytes,
-                                "host_gbs": fetch_bytes / (per_launch_ms["resolve_fetch"] * 1e-3) / 1e9}
+    link = None if R.resident else host_link_probes(torch, dev)
+    misses_per_step = misses_per_seg * L * segs_per_layer
+    hbm_bytes_step = L * segs_per_layer * (b["select"] + b["resolve"] + b["attn"]) + RECORD * misses_per_step
+    link_bytes_step = RECORD * misses_per_step
+    hbm_step = {"achieved": hbm_bytes_step / (ms * 1e-3) / 1e9, "bytes_per_step": hbm_bytes_step}
+    hbm_step["frac"] = hbm_step["achieved"] / hbm_peak
+    link_step = None
     if link:
-        kernels["resolve_fetch"]["frac_host_link"] = kernels["resolve_fetch"]["host_gbs"] / link["gbs"]
-    dom = max(per_launch_ms, key=per_launch_ms.get)
-    if dom == "resolve_fetch" and link:
-        roof = {"kernel": "resolve+gather (a3+a4)", "bound": "host-link", "achieved": kernels[dom]["host_gbs"],
-                "peak": link["gbs"], "unit": "GB/s", "frac": kernels[dom]["frac_host_link"],
-                "peak_source": "pinned H2D cudaMemcpy probe in this run", "traffic": None}
+        link_step = {"achieved": link_bytes_step / (ms * 1e-3) / 1e9, "bytes_per_step": link_bytes_step,
+                     "peak": link["gbs"]}
+        link_step["frac"] = link_step["achieved"] / link["gbs"]
+    # per kernel (device-timed launches of the timed graph)
+    chains = len(R.chains)
+    kernels = {}
+    for kind in KINDS:
+        ns, nl = kt[kind]
+        if nl == 0:
+            continue
+        avg_ms = ns / nl * 1e-6
+        segs_per_launch = segs_per_layer * L * args.steps / nl
+        e = {"kernel": KIND_NAMES[kind], "launches_per_step": nl / args.steps, "avg_launch_us": avg_ms * 1e3,
+             "busy_ms_per_step": ns * 1e-6 / args.steps, "segments_per_launch": segs_per_launch}
+        e["busy_share"] = e["busy_ms_per_step"] / ms_timer         # > 1 when launches of chains overlap
+        if kind == "select":
+            by = b["select"] + (b["resolve"] if R.fused else 0)
+            e["hbm_bytes_per_launch"] = by * segs_per_launch
+            if R.fused and link:
+                e["host_bytes_per_launch"] = RECORD * misses_per_seg * segs_per_launch
+        elif kind == "attn":
+            e["hbm_bytes_per_launch"] = b["attn"] * segs_per_launch
+        elif kind == "resolve":
+            e["hbm_bytes_per_launch"] = b["resolve"] * segs_per_launch
+        elif kind == "gather":
+            e["host_bytes_per_launch"] = RECORD * misses_per_seg * segs_per_launch
+        if "hbm_bytes_per_launch" in e:
+            e["hbm_gbs_per_launch"] = e["hbm_bytes_per_launch"] / (avg_ms * 1e-3) / 1e9
+            e["frac_hbm_per_launch"] = e["hbm_gbs_per_launch"] / hbm_peak
+        if "host_bytes_per_launch" in e and link:
+            e["host_gbs_per_launch"] = e["host_bytes_per_launch"] / (avg_ms * 1e-3) / 1e9
+        kernels[kind] = e
+    dom = max(kernels, key=lambda k_: kernels[k_]["busy_ms_per_step"]) if kernels else None
+    # the binding resource of the step: host link when its step fraction is the larger one
+    if link_step and link_step["frac"] >= hbm_step["frac"]:
+        roof = {"bound": "host-link", "achieved": link_step["achieved"], "peak": link["gbs"], "unit": "GB/s",
+                "frac": link_step["frac"], "scope": "step: host-link bytes of the missed blocks / ms_per_step",
+                "peak_source": link["how"]}
+        tr = ncu_traffic(args.config, "select")
+        roof["traffic"] = (tr["pcie_read_bytes_per_segment"] * segs_per_layer * L
+                           if tr and tr.get("pcie_read_bytes_per_segment") is not None else None)
     else:
-        if dom == "resolve_fetch":
-            dom = "attn"
-        roof = {"kernel": {"select": "score+topk (a1+a2)", "attn": "sparse decode + merge (a5+a6)"}[dom],
-                "bound": "hbm", "achieved": kernels[dom]["gbs"], "peak": hbm_peak, "unit": "GB/s",
-                "frac": kernels[dom]["frac_hbm"], "peak_source": hbm_src, "traffic": None}
-    # traffic: DRAM bytes per launch of the dominant ABI call's kernels from one committed
-    # `ncu --set full` capture (profiles/*_ncu_traffic.json, written by tools/ncu_traffic.py);
-    # host-link-bound calls have no DRAM equivalent of their algorithmic bytes (null)
-    tr = ncu_traffic(args.config, roof["bound"], dom)
-    if tr:
-        roof["traffic"] = tr["bytes_per_call"] * (segs_per_layer / tr["segments"])
-        roof["traffic_source"] = tr["source"]
-    # the attention kernel's roofline is always reported (north_star: sparse-attn HBM GB/s % peak)
-    roof_attn = {"achieved": kernels["attn"]["gbs"], "peak": hbm_peak, "unit": "GB/s",
-                 "frac": kernels["attn"]["frac_hbm"]}
+        roof = {"bound": "hbm", "achieved": hbm_step["achieved"], "peak": hbm_peak, "unit": "GB/s",
+                "frac": hbm_step["frac"], "scope": "step: algorithmic HBM bytes (SURVEY 8.5) / ms_per_step",
+                "peak_source": hbm_src}
+        trs = [ncu_traffic(args.config, kd) for kd in ("select", "attn")]
+        roof["traffic"] = (sum(t["dram_bytes_per_segment"] for t in trs) * segs_per_layer * L
+                           if all(t and t.get("dram_bytes_per_segment") is not None for t in trs) else None)
+    roof["traffic_unit"] = "bytes per step (ncu --set full DRAM/PCIe bytes per segment x segments)"
+    if dom:
+        dk = kernels[dom]
+        roof["dominant_kernel"] = {"kind": dom, "name": dk["kernel"], "avg_launch_us": dk["avg_launch_us"],
+                                   "busy_share": dk["busy_share"]}
+        if "hbm_gbs_per_launch" in dk:
+            roof["dominant_kernel"].update(achieved_gbs=dk["hbm_gbs_per_launch"],
+                                           frac_hbm=dk["frac_hbm_per_launch"])
+    # north_star's named figure: sparse-attention HBM GB/s as a fraction of peak
+    roof_attn = None
+    if "attn" in kernels:
+        ka = kernels["attn"]
+        roof_attn = {"achieved": ka["hbm_gbs_per_launch"], "peak": hbm_peak, "unit": "GB/s",
+                     "frac": ka["frac_hbm_per_launch"], "scope": "per launch (device-timed in the timed graph)"}
 
     # ---- e2e: queries H2D from pinned host + result D2H inside the timed region
     e2e = None
@@ -474,13 +533,13 @@ def run_gpu(args):
         e0.record(s)
         for _ in range(args.steps):
             R.graph_step(s, source="host")
-            if heads_mode:
+            if R.gather:
                 gather_outputs()
         e1.record(s)
         e1.synchronize()
         barrier()
-        ems = max_over_ranks(e0.elapsed_time(e1) / args.steps)
-        e2e = {"value": tokens / (ems * args.steps * 1e-3), "unit": "tokens/s", "ms_per_step": ems,
+        ems = kdist.max_over_ranks(e0.elapsed_time(e1) / args.steps, dev)
+        e2e = {"value": tokens_per_step / (ems * 1e-3), "unit": "tokens/s", "ms_per_step": ems,
                "h2d_bytes_per_step": int(R.q_cur.numel() * 2), "d2h_bytes_per_step": int(R.out.numel() * 4)}
     R.cache.check()
     clocks = clk.stop()
@@ -488,17 +547,23 @@ def run_gpu(args):
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
-        "scaling": "strong" if heads_mode else "weak",
+        "scaling": "strong" if (R.shard == "strong" and world > 1) else "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded; DESIGN.md §4)",
-        "config": {"workload": args.config, "desc": cfg["desc"], "global_batch": cfg["B"] if heads_mode else B * world, "seq_len": cfg["n"],
+        "config": {"workload": args.config, "desc": cfg["desc"],
+                   "global_batch": tokens_per_step if world > 1 else B, "seq_len": cfg["n"],
                    "layers": L, "q_heads": cfg["Hq"], "kv_heads": cfg["Hkv"], "block_tokens": cfg["P"],
                    "top_k_blocks": cfg["k"], "slots_per_segment": cfg["C"] or (cfg["n"] // cfg["P"]),
                    "policy": args.policy, "alpha": args.alpha, "host_layer_alias": R.A if not R.resident else None,
-                   "fill_steps": R.fill, "graph": not args.no_graph, "chains": len(R.chains), "fused_select_resolve": R.fused, "parallelism": (f"head-shard x{world} + NCCL all-gather" if heads_mode else f"request-shard x{world}"),
+                   "fill_steps": R.fill, "graph": not args.no_graph, "chains": chains,
+                   "fused_select_resolve": R.fused,
+                   "parallelism": (f"{R.shard}-shard x{world}" + (" + NCCL all-gather of head outputs" if R.gather
+                                                                else ", no collective on the decode path")),
                    "l2": "inputs larger than L2 (no flush)"},
         "hit_rate": hit_rate, "misses_per_segment": misses_per_seg,
-        "roofline": roof, "roofline_attn": roof_attn, "kernels": kernels,
-        "host_link": link, "e2e": e2e, "gpu_launches": R.launches_per_step * args.steps,
+        "roofline": roof, "roofline_attn": roof_attn, "hbm_step": hbm_step, "host_link_step": link_step,
+        "kernels": kernels, "host_link": link, "e2e": e2e,
+        "ms_per_step_with_kernel_timer": ms_timer,
+        "gpu_launches": R.launches_per_step * args.steps,
         "clocks": clocks, "setup_s": R.setup_s,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -510,86 +575,159 @@ def run_gpu(args):
         dist.destroy_process_group()
 
 
-def host_link_probe(torch, dev, nbytes=1 << 30):
-    """Pinned host -> HBM cudaMemcpy bandwidth (the host-link denominator)."""
+def host_link_probes(torch, dev, nbytes=1 << 30):
+    """The host-link denominator: max of a pinned H2D DMA copy and a zero-copy
+    read with the miss gather's own access pattern (kvd_probe_zero_copy), 1 GiB each."""
+    from paper_2605_18071_b200 import kvd
     h = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
     d = torch.empty(nbytes, dtype=torch.uint8, device=dev)
-    for _ in range(2):
-        d.copy_(h, non_blocking=True)
-    torch.cuda.synchronize(dev)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(4):
-        d.copy_(h, non_blocking=True)
-    e1.record()
-    e1.synchronize()
-    gbs = 4 * nbytes / (e0.elapsed_time(e1) * 1e-3) / 1e9
+    s = torch.cuda.current_stream(dev)
+
+    def timed(fn, reps=4):
+        fn()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        e1.synchronize()
+        return reps * nbytes / (e0.elapsed_time(e1) * 1e-3) / 1e9
+
+    dma = timed(lambda: d.copy_(h, non_blocking=True))
+    zc = {}
+    for ctas in (148, 296, 592):
+        zc[ctas] = timed(lambda: kvd.probe_zero_copy(h, d, nbytes, ctas, s))
+    best = max(zc.values())
     del h, d
-    return {"gbs": gbs, "how": "pinned H2D cudaMemcpyAsync, 1 GiB x4"}
+    return {"gbs": max(dma, best), "dma_gbs": dma, "zero_copy_gbs": best,
+            "zero_copy_by_ctas": {str(k): v for k, v in zc.items()},
+            "how": "max(pinned H2D cudaMemcpyAsync, zero-copy 16-B loads kvd_probe_zero_copy), 1 GiB x4 each"}
 
 
 # ---------------------------------------------------------------- the CPU oracle (baseline / reference arm)
+class OracleSample:
+    """A bounded sample of the workload for the oracle as it stands: `ntasks` whole segment-
+    steps runs (select O2-O5 + resolve O6 + attention O8 of one segment of layer 0 for 3 steps
+    from a cold cache).  Inputs and summaries (setup, a0) are prepared outside the timed part
+    for at most `max_bytes` of K/V; tasks cycle over the prepared segments."""
+
+    def __init__(self, args, cfg, ntasks, max_bytes=3 << 30):
+        import oracle
+        import synth
+        self.oracle = oracle
+        L, B, Hq, Hkv, n, P, k = (cfg[x] for x in ("L", "B", "Hq", "Hkv", "n", "P", "k"))
+        self.G = Hq // Hkv
+        nb = (n + P - 1) // P
+        self.C = cfg["C"] if cfg["C"] is not None else nb
+        self.W = k + 1 + (64 + P - 1) // P + 1
+        self.cfg, self.args, self.k, self.P = cfg, args, k, P
+        nseg = max(1, min(ntasks, B * Hkv, max_bytes // (4 * n * 128)))
+        self.ntasks = ntasks
+        self.segs = []
+        for seg in range(nseg):
+            r, h = divmod(seg, Hkv)
+            K, V = synth.segment_kv(args.seed, 0, r, h, n)
+            S = oracle.block_summaries(K, P)
+            q = synth.queries(args.seed, 0, r, h, self.G, t0=0, nsteps=3, alpha=args.alpha)
+            self.segs.append((K, V, S, q, oracle.pinned_blocks(n, P), nb))
+
+    def run(self, threads):
+        """All tasks on `threads` host threads; returns (wall seconds, segment-steps).  The
+        oracle's C functions release the GIL (ctypes), so threads run them in parallel."""
+        from concurrent.futures import ThreadPoolExecutor
+        oracle, pol = self.oracle, self.oracle.POLICIES[self.args.policy]
+
+        def one(i):
+            K, V, S, q, pinned, nb = self.segs[i % len(self.segs)]
+            oc = oracle.SegmentCache(nb, self.C, pinned)
+            for t in range(3):
+                oracle.segment_step(oc, q[t], S, K, V, self.P, self.k, t + 1, pol, self.W)
+            return 3
+        t0 = time.perf_counter()
+        if threads <= 1:
+            done = sum(one(i) for i in range(self.ntasks))
+        else:
+            with ThreadPoolExecutor(threads) as ex:
+                done = sum(ex.map(one, range(self.ntasks)))
+        return time.perf_counter() - t0, done
+
+
 def cpu_baseline(args, cfg, target_s):
-    """Time the oracle (as it stands) on a bounded sample of the same workload:
-    whole segments (select O2-O5 + resolve O6 + fetch O7 + attention O8) of one
-    layer's decode step, scaled to tokens/s = B / (per-segment time x B*Hkv*L)."""
-    import oracle
-    import synth
-    L, B, Hq, Hkv, n, P, k = (cfg[x] for x in ("L", "B", "Hq", "Hkv", "n", "P", "k"))
-    G = Hq // Hkv
-    nb = (n + P - 1) // P
-    C = cfg["C"] if cfg["C"] is not None else nb
-    W = k + 1 + (64 + P - 1) // P + 1
-    done, spent, t_all = 0, 0.0, time.time()
-    seg = 0
-    while spent < target_s and time.time() - t_all < 3 * target_s and seg < B * Hkv:
-        r, h = divmod(seg, Hkv)
-        K, V = synth.segment_kv(args.seed, 0, r, h, n)
-        S = oracle.block_summaries(K, P)          # setup (a0), not timed
-        pinned = oracle.pinned_blocks(n, P)
-        oc = oracle.SegmentCache(nb, C, pinned)
-        q = synth.queries(args.seed, 0, r, h, G, t0=0, nsteps=3, alpha=args.alpha)
-        for t in range(3):
-            t0 = time.perf_counter()
-            oracle.segment_step(oc, q[t], S, K, V, P, k, t + 1, oracle.POLICIES[args.policy], W)
-            spent += time.perf_counter() - t0
-            done += 1
-        seg += 1
-    per_seg = spent / max(1, done)
-    step_s = per_seg * B * Hkv * L
-    return {"value": B / step_s, "unit": "tokens/s", "cores": 1, "kind": "oracle",
-            "sample": f"{done} segment-steps ({seg} segments x 3 steps) of layer 0, {spent:.1f} s of oracle work; "
-                      f"scaled x{B * Hkv * L} segments/step"}
+    """The oracle timed on this host's cores: 1 thread and all cores (threads over segments)."""
+    cores = cpu_cores()
+    L, B, Hkv = cfg["L"], cfg["B"], cfg["Hkv"]
+    seg_steps_per_step = B * Hkv * L
+    probe = OracleSample(args, cfg, 1)
+    w1, n1 = probe.run(1)
+    per1 = w1 / n1                                # seconds per segment-step, 1 thread
+    n_one = max(1, int(target_s / (3 * per1)))
+    n_all = max(cores, int(target_s * cores / (3 * per1)))
+    w_one, d_one = OracleSample(args, cfg, n_one).run(1)
+    allc = OracleSample(args, cfg, n_all)
+    w_all, d_all = allc.run(cores)
+    v1 = B / (w_one / d_one * seg_steps_per_step)
+    va = B / (w_all / d_all * seg_steps_per_step)
+    return {"value": va, "unit": "tokens/s", "cores": cores, "kind": "oracle",
+            "value_1_thread": v1, "speedup_all_cores": va / v1,
+            "sample": f"all cores: {d_all} segment-steps ({n_all} runs of 3 steps over {len(allc.segs)} layer-0 "
+                      f"segments) on {cores} threads in {w_all:.1f} s; 1 thread: {d_one} segment-steps in "
+                      f"{w_one:.1f} s; each scaled to the {seg_steps_per_step} segment-steps of one decode step "
+                      f"(B x Hkv x L)"}
 
 
 def run_reference(args):
+    """--impl reference: the oracle as it stands, on this host's cores.  Each step is one
+    bounded sample of the workload (whole segment-steps, threads over segments); ms_per_step
+    is that sample's wall time, value extrapolates it to the config's decode tokens/s."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
     cfg = dict(CONFIGS[args.config])
     import oracle
     oracle.build()
-    # K steps of a bounded per-step sample, after W warm-up samples
-    per = max(1.0, min(10.0, 60.0 / max(1, args.steps)))
-    for _ in range(min(args.warmup, 1)):
-        cpu_baseline(args, cfg, 0.5)
-    vals = [cpu_baseline(args, cfg, per) for _ in range(args.steps)]
-    # one host runs the oracle for the whole job (N*B requests): tokens/s is the per-host rate
-    v = float(np.mean([x["value"] for x in vals]))
-    B = cfg["B"] * world
-    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": B / v * 1e3,
+    cores = cpu_cores()
+    L, B, Hkv = cfg["L"], cfg["B"], cfg["Hkv"]
+    w1, n1 = OracleSample(args, cfg, 1).run(1)
+    per_wall = w1 / n1 / cores                    # ~ seconds per segment-step on all cores
+    budget = min(8.0, 150.0 / max(1, args.steps + args.warmup))   # whole run within a few minutes
+    ntasks = max(cores, int(budget / (3 * per_wall)))
+    sample = OracleSample(args, cfg, ntasks)
+    for _ in range(args.warmup):
+        sample.run(cores)
+    walls, done = [], 0
+    for _ in range(args.steps):
+        w, done = sample.run(cores)
+        walls.append(w)
+    wall = float(np.mean(walls))
+    seg_steps_per_step = B * Hkv * L
+    v = B / (wall / done * seg_steps_per_step)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64/f32 (oracle)",
             "data": "synthetic (seeded; DESIGN.md §4)",
             "config": {"workload": args.config, "desc": cfg["desc"], "global_batch": B, "seq_len": cfg["n"]},
-            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": 1, "kind": "oracle",
-                             "sample": vals[0]["sample"]},
+            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": cores, "kind": "oracle",
+                             "sample": f"each step: {done} segment-steps ({ntasks} runs of 3 steps over "
+                                       f"{len(sample.segs)} layer-0 segments) on {cores} threads, {wall:.2f} s "
+                                       f"wall (= ms_per_step); value scales it to the {seg_steps_per_step} "
+                                       f"segment-steps of one decode step"},
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
+def self_launch(args):
+    """--gpus N > 1 without a torch.distributed environment: launch N ranks (one per GPU)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(args.master_port), os.path.abspath(__file__),
+           *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -228,6 +228,26 @@ kvd_status kvd_read_summaries(kvd_cache* c, int32_t layer, int32_t req, int32_t 
 kvd_status kvd_read_scores(kvd_cache* c, int32_t layer, int32_t req, int32_t head, float* out);
 
 kvd_status kvd_get_stats(kvd_cache* c, kvd_stats* out);   /* synchronises the device */
+
+/* Kernel timer (measurement; bench.py).  While enabled, every step kernel records its own
+ * launch duration on the device: from the earliest start of any of its CTAs / warps after
+ * griddepcontrol.wait to the end of the last one (%globaltimer), accumulated per kind:
+ * [0] select (score + top-k, fused: + resolve + fetch), [1] resolve (kvd_resolve_and_fetch),
+ * [2] gather (kvd_resolve_and_fetch, host-backed), [3] attention (split-K + merge).  This
+ * times the kernels of a CUDA-graph / multi-stream step exactly as it runs, with no event node
+ * between kernels (which would break their programmatic overlap).  Costs two device-scope
+ * atomics per CTA (per warp for attention).  kvd_enable_kernel_timer synchronises and zeroes
+ * the accumulators (allocating on first use); enable = 0 stops recording.  Step calls capture
+ * the on/off state when they are issued (or captured into a graph).
+ * kvd_read_kernel_timer synchronises and copies ns[4] (summed launch durations) and
+ * launches[4] (counts). */
+kvd_status kvd_enable_kernel_timer(kvd_cache* c, int32_t enable);
+/* Host-link probe (measurement; the gather's denominator): copy `bytes` (a
+ * multiple of 16) from pinned host memory `host` to device memory `dev` with the miss gather's
+ * own access pattern (16-byte zero-copy loads, 8 in flight per thread) on `ctas` CTAs of 256
+ * threads.  Asynchronous on `stream`; KVD_EINVAL if `host` is not pinned host memory. */
+kvd_status kvd_probe_zero_copy(const void* host, void* dev, size_t bytes, int32_t ctas, kvd_stream stream);
+kvd_status kvd_read_kernel_timer(kvd_cache* c, uint64_t* ns, uint64_t* launches);
 kvd_status kvd_reset_stats(kvd_cache* c);                 /* synchronises the device */
 
 /* Synchronise the device and report KVD_EDEVICE if any kernel flagged bad input

@@ -58,6 +58,9 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
     uint32_t ok;
     asm volatile(
@@ -154,6 +157,48 @@ __device__ __forceinline__ int4 ld_stream16(const void* p) {
 // and griddep_launch() once its main loop is done.
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// ------------------------------------------------ in-kernel launch timing
+// kvd_enable_kernel_timer: every step kernel records its launch's duration on the device, so
+// the benchmark can time the kernels of the exact (graph-captured, PDL-chained, multi-stream)
+// path it times, with no event node between kernels.  A launch's units (CTAs or warps) take
+// the min of their start stamps (after griddepcontrol.wait) in the launch's slot; the unit that
+// completes the slot's count adds end - start to the per-kind accumulator and resets the slot.
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void kt_begin(unsigned long long* slots, int slot) {
+    if (slots) atomicMin(&slots[2 * slot], global_ns());
+}
+__device__ __forceinline__ void kt_end(unsigned long long* slots, unsigned long long* acc, int slot, int kind,
+                                       unsigned long long units) {
+    if (!slots) return;
+    unsigned long long* sl = slots + 2 * slot;
+    if (atomicAdd(&sl[1], 1ull) == units - 1) {
+        const unsigned long long t1 = global_ns();
+        const unsigned long long t0 = atomicExch(&sl[0], ~0ull);
+        atomicExch(&sl[1], 0ull);
+        atomicAdd(&acc[2 * kind], t1 > t0 ? t1 - t0 : 0ull);
+        atomicAdd(&acc[2 * kind + 1], 1ull);
+    }
+}
+// Phase stamps for tuning (experiment builds only: -DKVD_EXPERIMENTS; compiled out of the
+// product).  EXP_STAMP(buf, unit, i) records %globaltimer for unit (CTA / warp index) and
+// phase i into the device buffer StepParams::exp_trace, read back by kvd_exp_read_trace.
+constexpr int kExpUnits = 16384, kExpPhases = 8;
+#ifdef KVD_EXPERIMENTS
+#define EXP_STAMP(buf, unit, i)                                                             \
+    do {                                                                                   \
+        if ((buf) && (unit) < kExpUnits) (buf)[(unit) * kExpPhases + (i)] = global_ns();    \
+    } while (0)
+#else
+#define EXP_STAMP(buf, unit, i) \
+    do {                        \
+    } while (0)
+#endif
+enum { kKtSelect = 0, kKtResolve = 1, kKtGather = 2, kKtAttn = 3, kKtMerge = 4, kKtKinds = 5 };
 
 // Process-wide count of step-kernel launches issued by libkvd (kvd_launch_count;
 // a launch recorded into a CUDA graph counts once, at capture).

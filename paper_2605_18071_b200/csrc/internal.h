@@ -19,13 +19,14 @@
 
 namespace kvd {
 
-constexpr int kScoreCols = 128;       // blocks per score-kernel tile (nb_pad multiple)
+constexpr int kScoreCols = 128;       // nb_pad is a multiple of this (summary / table rows)
+
 constexpr int kAttnWarps = 4;         // warps per attention CTA
 constexpr int kAttnStages = 3;        // smem stages per warp
 constexpr int kTileBytes = 8192;      // one 16-token K||V tile
-constexpr int kSplitTiles = 16;       // (legacy split size; StepParams.nsplit)
-constexpr int kMaxSelectBlocks = 8 * 1024 * 32;   // top-k cluster capacity: 8 CTAs x 1024 threads x 32 keys
-constexpr int kMaxPieces = 32;        // attention partials per (request, KV head) (k_attn.cu)
+constexpr int kMaxSelectBlocks = 8 * 1024 * 32;   // select cluster capacity: 8 CTAs x 1024 threads x 32 keys
+constexpr int kMaxPieces = 32;        // attention pieces (partials) per (request, KV head) (k_attn.cu)
+constexpr int kPieceTiles = 8;        // 16-token tiles per attention piece (at least)
 constexpr int64_t kSlotOfBytes = 64ll << 20;   // setup scratch for per-block slot targets
 
 struct SegGeom {                      // per-request pinned geometry (device copy in params)
@@ -42,8 +43,11 @@ struct StepParams {
     const uint32_t* step_dev;         // non-null: read the step on the device (graph replay)
     int32_t host_layer;
     int32_t rec_bytes;
-    int32_t nsplit;
     float scale_log2;
+    unsigned long long* kt_slots;     // kvd_enable_kernel_timer: [L*R*kKtKinds][2], or NULL
+    unsigned long long* kt_acc;       // [kKtKinds][2] (ns, launches)
+    int32_t kt_base;                  // slot of (layer, first request): (layer*R + req[0]) * kKtKinds
+    unsigned long long* exp_trace;    // experiment builds: phase stamps (NULL otherwise)
     int32_t req[KVD_MAX_BATCH];
 };
 
@@ -56,6 +60,7 @@ struct kvd_cache {
     bool resident;
     int64_t rec_bytes;
     int max_splits;
+    int prio_hi = 0;                      // greatest stream priority of the device (host-link kernels)
     // device
     uint8_t* slots = nullptr;
     uint16_t* summ = nullptr;
@@ -69,6 +74,9 @@ struct kvd_cache {
     int32_t* miss_count = nullptr;
     float* part_o = nullptr;
     float* part_ml = nullptr;
+    unsigned long long* kt_slots = nullptr;  // kernel timer (bench instrumentation)
+    unsigned long long* kt_acc = nullptr;
+    bool kt_on = false;
     unsigned long long* stats = nullptr;   // [5] kvd_stats fields
     int32_t* err = nullptr;
     int32_t* ntok_dev = nullptr;
@@ -89,13 +97,29 @@ cudaError_t launch_prefix(kvd_cache* c, int layer, int req, const uint16_t* dk, 
 cudaError_t launch_select(kvd_cache* c, const StepParams& p, const uint16_t* q, int32_t* out_ids, float* out_scores,
                           cudaStream_t s);
 size_t resolve_smem_bytes(int64_t nkeys, int64_t kmax, int64_t nb_pad);   // k_resolve.cu
+size_t resolve_static_smem();                                               // k_resolve.cu
+void select_geometry(int64_t nb_pad, int segs, bool resident, int* nt, int* cl, int* kpt, int* v);   // k_select.cu
+size_t select_smem_bytes(int nt, int kpt);                                  // k_select.cu (dynamic)
+size_t select_static_smem();                                                // k_select.cu
 constexpr size_t kMaxSmemBytes = 227 * 1024;
 cudaError_t launch_resolve(kvd_cache* c, const StepParams& p, const int32_t* ids, int32_t* out_attn, cudaStream_t s);
 cudaError_t launch_gather(kvd_cache* c, const StepParams& p, cudaStream_t s);
+cudaError_t launch_zero_copy(const void* host, void* dev, size_t bytes, int ctas, cudaStream_t s);
 cudaError_t launch_select_resolve(kvd_cache* c, const StepParams& p, const uint16_t* q, int32_t* out_ids,
                                   float* out_scores, int32_t* out_attn, cudaStream_t s);
 cudaError_t launch_attention(kvd_cache* c, const StepParams& p, const uint16_t* q, const int32_t* attn, float* out,
                              float* out_lse, cudaStream_t s);
+
+// Split-K plan of one segment's attention: its TS tiles are cut into NP pieces of
+// kPieceTiles tiles or more (at most kMaxPieces), piece i = tiles [i*TS/NP, (i+1)*TS/NP).
+// A function of TS (i.e. of k) only -- not of how many segments share a launch or a GPU -- so
+// every output is bit-identical however the requests are batched, chained or sharded.
+__host__ __device__ inline int attn_pieces(int TS) {
+    const int pt0 = (TS + kMaxPieces - 1) / kMaxPieces;
+    const int pt = pt0 > kPieceTiles ? pt0 : kPieceTiles;
+    const int np = (TS + pt - 1) / pt;
+    return np > 0 ? np : 1;
+}
 
 __host__ __device__ inline SegGeom seg_geom(int64_t n64, int P, int sink, int local) {
     // 32-bit, shift-only (P in {1, 2, 4, 8, 16}; n < 2^27): every thread of the step kernels

@@ -1,19 +1,24 @@
-// k_attn.cu — rows (a5) split-K sparse decode attention and (a6) LSE merge.
+// k_attn.cu — rows (a5) split-K sparse decode attention and (a6) LSE merge, one kernel.
 //
 // "executing attention ... over the union of the newly fetched and resident KV
 // entries".  The attention lists from resolve (selected +
 // pinned blocks, ascending) are cut into 16-token tiles (E = 16/P list
-// entries, 8 KiB).  The call's S = B*Hkv segments give T = S*TS tiles (TS =
-// ceil(W/E) per segment, uniform; entries past a segment's valid length read a
-// zero record and are masked).  The tile sequence is split evenly over NW warp
-// workers (stream-K: worker w owns tiles [w*T/NW, (w+1)*T/NW)), so every SM
-// streams the same number of tiles whatever B, Hkv and k are; a worker whose
-// range crosses a segment boundary produces one partial per segment piece.
+// entries, 8 KiB).  Every segment has TS = ceil(W/E) tiles (uniform in a call;
+// entries past a segment's valid length read a zero record and are masked).
 //
-// Per worker (one warp; 8 per SM by default): a private STAGES-deep ring of 8 KiB tiles in shared
-// memory fed by bulk async copies (TMA engine) completing on mbarriers; the
-// (block, slot) entries are staged through shared memory 128 at a time so a
-// copy is never issued behind a dependent global load.  Per tile, on tensor
+// Split plan.  A segment's tiles are cut into NP = attn_pieces(TS) pieces of
+// >= 8 tiles (internal.h).  The plan depends on TS (i.e. on k) only, never on
+// how many segments share the launch, so outputs are bit-identical however the
+// requests are batched, chained or sharded over GPUs.  The call's S*NP pieces
+// are dealt to NW warp workers in contiguous ranges (stream-K over pieces:
+// worker w owns pieces [w*Ptot/NW, (w+1)*Ptot/NW)); consecutive pieces are
+// consecutive tiles, so a worker streams one contiguous tile range and its
+// copy pipeline runs across piece and segment boundaries without a break.
+//
+// Per worker (one warp; 8 per SM): a private STAGES-deep ring of 8 KiB tiles in
+// shared memory fed by bulk async copies (TMA engine) completing on mbarriers;
+// the (block, slot) entries are staged through shared memory 128 at a time so
+// a copy is never issued behind a dependent global load.  Per tile, on tensor
 // cores (mma.sync m16n8k16 bf16 -> fp32, swap-AB: 16 tokens fill M, heads N):
 //     S^T[16 tok][8] = K[16][128] . Q^T                   (8 MMAs)
 //     O^T[128][8]   += V^T[128][16] . P^T                  (8 or 16 MMAs)
@@ -25,18 +30,21 @@
 // parts take two MMAs.  The S^T accumulator becomes the P^T B-fragment with
 // movmatrix.trans.  Online softmax in the log2 domain (exp2).
 //
-// (a6) A segment handled by one worker is finalised in place; otherwise each
-// piece writes its unnormalised partial (o~_j, m_j, l_j) and merge_kernel,
-// launched behind attn_kernel (PDL, so no fences or arrival counters on the
-// streaming path), combines them with one warp per query head:
+// (a6) At the end of each piece the worker writes its unnormalised partial
+// (o~_j, m_j, l_j) with plain stores; merge_kernel, launched behind attn_kernel
+// with programmatic dependent launch (its CTAs are resident before the
+// attention grid drains, and griddepcontrol.wait orders the partials: no
+// fences or arrival counters on the streaming path), combines the NP partials
+// of every segment in piece order j = 0 .. NP-1:
 //     m = max_j m_j;  l = sum_j l_j 2^(m_j-m);  o = sum_j 2^(m_j-m) o~_j / l;
 //     lse = (m + log2 l) ln 2.
-// HBM-bound: 8 KiB per 16-token tile; 4*G flop per 4 B of K/V.
+// One CTA per segment, one warp per query head; each lane requests all NP of
+// its partial rows at once (one memory round trip).  A segment of one piece is
+// finalised in place by its worker.  HBM-bound: 8 KiB per 16-token tile; 4*G
+// flop per 4 B of K/V.
 #include <algorithm>
 #include <cstdlib>
 #include <type_traits>
-#include <vector>
-#include <cstdio>
 
 #include "common.cuh"
 #include "internal.h"
@@ -54,26 +62,16 @@ struct AttnBufs {
 constexpr int kEntChunk = 128;                      // list entries staged per chunk (>= STAGES * 16)
 
 struct Work {
-    int32_t T;          // total tiles of the call (< 2^31: B <= 256, Hkv * TS small)
     int32_t TS;         // tiles per segment
+    int32_t NP;         // pieces per segment (attn_pieces(TS))
+    int32_t Ptot;       // pieces of the call (S * NP)
     int32_t NW;         // workers
-    int32_t xflags;     // timing experiments only (KVD_ATTN_X): 1 = skip S MMAs, 2 = skip P.V MMAs
-    unsigned long long* trace;   // KVD_ATTN_TRACE: per-warp globaltimer stamps [NW][8] (experiments only)
 };
 
-__device__ __forceinline__ unsigned long long gtime() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
-#define ATTN_STAMP(i)                                                         \
-    do {                                                                      \
-        if (wk.trace && lane == 0 && w < wk.NW) wk.trace[(int64_t)w * 8 + (i)] = gtime(); \
-    } while (0)
-
-__device__ __forceinline__ int tile_begin(int w, const Work& wk) { return (int)((int64_t)w * wk.T / wk.NW); }
-__device__ __forceinline__ int worker_of(int t, const Work& wk) {
-    return (int)(((int64_t)(t + 1) * wk.NW - 1) / wk.T);
+// first tile of global piece gp (pieces of a segment are balanced: i*TS/NP)
+__device__ __forceinline__ int piece_tile(int gp, const Work& wk) {
+    const int s = gp / wk.NP, i = gp - s * wk.NP;
+    return s * wk.TS + (i * wk.TS) / wk.NP;
 }
 
 template <int STAGES, int WARPS>
@@ -93,18 +91,34 @@ __global__ void __launch_bounds__(WARPS * 32, 1) attn_kernel(StepParams p, AttnB
         fence_mbar_init();
     }
     __syncwarp();
-    const int ta = w < wk.NW ? tile_begin(w, wk) : 0, tb = w < wk.NW ? tile_begin(w + 1, wk) : 0;
-    const int nt = tb - ta;
+    const int pa = w < wk.NW ? (int)((int64_t)w * wk.Ptot / wk.NW) : 0;
+    const int pb = w < wk.NW ? (int)((int64_t)(w + 1) * wk.Ptot / wk.NW) : 0;
+    const int ta = piece_tile(pa, wk);
+    const int nt = piece_tile(pb, wk) - ta;
     const int s_first = ta / wk.TS, i_first = ta - s_first * wk.TS;   // segment / tile-in-segment of tile ta
     // P, E = 16/P and CT = kEntChunk/E >= STAGES (tiles per entry chunk) are powers of two: shifts, no divisions
     const int logP = __ffs(p.P) - 1, logE = 4 - logP, logCT = 7 - logE;
     const int E = 1 << logE, rec = p.rec_bytes, CT = 1 << logCT;
     const uint64_t pol = l2_evict_first_policy();
     const bool packed = p.G <= 4;
-    ATTN_STAMP(0);
+    if (lane == 0) EXP_STAMP(p.exp_trace, w, 0);
     griddep_wait();                                // lists / slots / q come from earlier kernels
-    ATTN_STAMP(1);
-    if (nt <= 0) return;
+    if (lane == 0) EXP_STAMP(p.exp_trace, w, 1);
+    // kernel timer (kvd.h): one start / end per CTA; the CTA's last warp to finish ends it
+    __shared__ int kt_warps_done;
+    if (threadIdx.x == 0) {
+        kt_warps_done = 0;
+        kt_begin(p.kt_slots, p.kt_base + kKtAttn);
+    }
+    __syncthreads();
+    auto kt_warp_exit = [&]() {
+        if (p.kt_slots && lane == 0 && atomicAdd(&kt_warps_done, 1) == WARPS - 1)
+            kt_end(p.kt_slots, p.kt_acc, p.kt_base + kKtAttn, kKtAttn, gridDim.x);
+    };
+    if (nt <= 0) {
+        kt_warp_exit();
+        return;
+    }
 
     // stage entry chunk c (tiles ta + c*CT ..) into buffer c & 1: (block, slot), or (-1, -1).
     // resolve pads each list past its valid length with (-1, -1); entries j >= W are tile padding.
@@ -169,9 +183,10 @@ __global__ void __launch_bounds__(WARPS * 32, 1) attn_kernel(StepParams p, AttnB
     float oacc[8][4];
     float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
     int cs = -1;                                            // current segment
+    int cp = pa - 1;                                        // current piece (global index)
     int n_cur = 0;
 
-    // flush the running piece of segment cs: partial or (single piece) final output
+    // flush piece cp of segment cs: final output (one-piece segment) or partial + arrival
     auto flush = [&]() {
 #pragma unroll
         for (int o = 4; o < 32; o <<= 1) {
@@ -186,12 +201,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1) attn_kernel(StepParams p, AttnB
         }
         const int bi = cs / p.Hkv, h = cs - bi * p.Hkv;
         const int64_t rs = (int64_t)p.req[bi] * p.Hkv + h;
-        const int s0 = cs * wk.TS;
-        const int fw = worker_of(s0, wk), lw = worker_of(s0 + wk.TS - 1, wk);
-        const int np = lw - fw + 1;
         const int h0 = 2 * quad, h1 = h0 + 1, d = lane >> 2;
         const bool own = !packed || quad < 2;               // lanes holding real head columns
-        if (np == 1) {
+        if (wk.NP == 1) {
             if (own) {
                 const float i0 = l0 > 0.f ? 1.f / l0 : 0.f, i1 = l1 > 0.f ? 1.f / l1 : 0.f;
 #pragma unroll
@@ -215,31 +227,31 @@ __global__ void __launch_bounds__(WARPS * 32, 1) attn_kernel(StepParams p, AttnB
             }
             return;
         }
-        const int j = w - fw;
+        const int j = cp - cs * wk.NP;                      // piece index within the segment
         float* po = ab.part_o + ((rs * kMaxPieces + j) * 8) * (int64_t)kHeadDim;
         float* pml = ab.part_ml + ((rs * kMaxPieces + j) * 8) * 2;
         if (own) {
 #pragma unroll
             for (int mt = 0; mt < 8; ++mt) {
-                po[h0 * kHeadDim + 16 * mt + d] = oacc[mt][0];
-                po[h1 * kHeadDim + 16 * mt + d] = oacc[mt][1];
-                po[h0 * kHeadDim + 16 * mt + 8 + d] = oacc[mt][2];
-                po[h1 * kHeadDim + 16 * mt + 8 + d] = oacc[mt][3];
+                __stcg(&po[h0 * kHeadDim + 16 * mt + d], oacc[mt][0]);
+                __stcg(&po[h1 * kHeadDim + 16 * mt + d], oacc[mt][1]);
+                __stcg(&po[h0 * kHeadDim + 16 * mt + 8 + d], oacc[mt][2]);
+                __stcg(&po[h1 * kHeadDim + 16 * mt + 8 + d], oacc[mt][3]);
             }
             if (d == 0) {
-                pml[h0 * 2] = m0;
-                pml[h0 * 2 + 1] = l0;
-                pml[h1 * 2] = m1;
-                pml[h1 * 2 + 1] = l1;
+                __stcg(&pml[h0 * 2], m0);
+                __stcg(&pml[h0 * 2 + 1], l0);
+                __stcg(&pml[h1 * 2], m1);
+                __stcg(&pml[h1 * 2 + 1], l1);
             }
         }
     };
 
-    int seg_left = 0;                                       // tiles left in the current segment
+    int piece_left = 0;                                     // tiles left in the current piece
     int st = 0;                                             // stage of the next tile to consume
     uint32_t ph = 0;                                        // its mbarrier phase
 
-    // Consume NT (1 or 2) tiles of the current segment: the two tiles' S chains, one softmax
+    // Consume NT (1 or 2) tiles of the current piece: the two tiles' S chains, one softmax
     // update over their 16 NT tokens and their P.V products are interleaved for ILP.
     auto step = [&](auto nt_tag, int k) {
         constexpr int NT = decltype(nt_tag)::value;
@@ -255,7 +267,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) attn_kernel(StepParams p, AttnB
             vlo[t] = elo.x >= 0 && (elo.x << logP) + (row_lo & pm) < n_cur;
             vhi[t] = ehi.x >= 0 && (ehi.x << logP) + (row_hi & pm) < n_cur;
             mbar_wait(&my_bar[st_t], ph_t);
-            if (kt == 0) ATTN_STAMP(2);
+            if (kt == 0 && lane == 0) EXP_STAMP(p.exp_trace, w, 2);
             sb[t] = smem_u32(my_stage + (size_t)st_t * kTileBytes);
             st_t = st_t + 1 == STAGES ? 0 : st_t + 1;
             ph_t ^= st_t == 0 ? 1u : 0u;
@@ -276,12 +288,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1) attn_kernel(StepParams p, AttnB
                 const uint32_t c = (uint32_t)(2 * kk + kchunk_hi), c2 = c + 2;
                 ldsm_x4(sb[t] + koff + ((c ^ kswz) << 4), a0, a1, a2, a3);
                 ldsm_x4(sb[t] + koff + ((c2 ^ kswz) << 4), b0, b1, b2, b3);
-                if (!(wk.xflags & 1)) {
-                    mma_bf16_16816(sacc[t], a0, a1, a2, a3, qf[kk][0], qf[kk][1]);
-                    mma_bf16_16816(sacc2[t], b0, b1, b2, b3, qf[kk + 1][0], qf[kk + 1][1]);
-                } else {
-                    sacc[t][0] += __uint_as_float(a0 & b0); sacc2[t][1] += __uint_as_float(a1 & b3);
-                }
+                mma_bf16_16816(sacc[t], a0, a1, a2, a3, qf[kk][0], qf[kk][1]);
+                mma_bf16_16816(sacc2[t], b0, b1, b2, b3, qf[kk + 1][0], qf[kk + 1][1]);
             }
         }
         // online softmax (log2 domain) over the NT tiles
@@ -341,8 +349,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) attn_kernel(StepParams p, AttnB
                     uint32_t a0, a1, a2, a3;
                     const uint32_t c = (uint32_t)(2 * mt + vchunk_hi);
                     ldsm_x4_t(sb[t] + voff + ((c ^ vswz) << 4), a0, a1, a2, a3);
-                    if (!(wk.xflags & 2)) mma_bf16_16816(oacc[mt], a0, a1, a2, a3, b0, b1);
-                    else oacc[mt][0] += __uint_as_float(a0 ^ a3 ^ b0);
+                    mma_bf16_16816(oacc[mt], a0, a1, a2, a3, b0, b1);
                 }
             } else {
                 const uint32_t bh0 = movmatrix_t(hlo), bh1 = movmatrix_t(hhi);
@@ -370,204 +377,161 @@ __global__ void __launch_bounds__(WARPS * 32, 1) attn_kernel(StepParams p, AttnB
 
     int k = 0;
     while (k < nt) {
-        if (seg_left == 0) {                                // new segment piece
-            if (cs >= 0) flush();
-            cs = cs < 0 ? s_first : cs + 1;
-            seg_left = cs == s_first ? wk.TS - i_first : wk.TS;
-            const int bi = cs / p.Hkv, h = cs - bi * p.Hkv;
-            n_cur = ab.ntok[p.req[bi]];
-            // Q^T B-fragments: column n = lane/4 -> head n (packed: n & 3), dims 16 kk + 2 quad + {0,1} (+8)
-            const int hd = packed ? (lane >> 2) & 3 : lane >> 2;
-            const uint16_t* qh = q + ((int64_t)bi * p.Hq + (int64_t)h * p.G + hd) * kHeadDim + 2 * quad;
+        if (piece_left == 0) {                              // next piece
+            if (cp >= pa) flush();
+            ++cp;
+            const int s = cp / wk.NP, i = cp - s * wk.NP;
+            piece_left = ((i + 1) * wk.TS) / wk.NP - (i * wk.TS) / wk.NP;
+            if (s != cs) {                                  // new segment: its query fragments
+                cs = s;
+                const int bi = cs / p.Hkv, h = cs - bi * p.Hkv;
+                n_cur = ab.ntok[p.req[bi]];
+                // Q^T B-fragments: column n = lane/4 -> head n (packed: n & 3), dims 16 kk + 2 quad + {0,1} (+8)
+                const int hd = packed ? (lane >> 2) & 3 : lane >> 2;
+                const uint16_t* qh = q + ((int64_t)bi * p.Hq + (int64_t)h * p.G + hd) * kHeadDim + 2 * quad;
 #pragma unroll
-            for (int kk = 0; kk < 8; ++kk) {
-                qf[kk][0] = hd < p.G ? *reinterpret_cast<const uint32_t*>(qh + 16 * kk) : 0u;
-                qf[kk][1] = hd < p.G ? *reinterpret_cast<const uint32_t*>(qh + 16 * kk + 8) : 0u;
+                for (int kk = 0; kk < 8; ++kk) {
+                    qf[kk][0] = hd < p.G ? *reinterpret_cast<const uint32_t*>(qh + 16 * kk) : 0u;
+                    qf[kk][1] = hd < p.G ? *reinterpret_cast<const uint32_t*>(qh + 16 * kk + 8) : 0u;
+                }
             }
 #pragma unroll
             for (int mt = 0; mt < 8; ++mt) oacc[mt][0] = oacc[mt][1] = oacc[mt][2] = oacc[mt][3] = 0.f;
             m0 = m1 = -INFINITY;
             l0 = l1 = 0.f;
         }
-        const int left = min(seg_left, nt - k);
+        const int left = min(piece_left, nt - k);
         if (left >= 2) {
             step(std::integral_constant<int, 2>{}, k);
             k += 2;
-            seg_left -= 2;
+            piece_left -= 2;
         } else {
             step(std::integral_constant<int, 1>{}, k);
             k += 1;
-            seg_left -= 1;
+            piece_left -= 1;
         }
     }
-    ATTN_STAMP(3);
+    if (lane == 0) EXP_STAMP(p.exp_trace, w, 3);
     griddep_launch();
     flush();
-    ATTN_STAMP(6);
+    __syncwarp();
+    if (lane == 0) EXP_STAMP(p.exp_trace, w, 4);
+    kt_warp_exit();
 }
 
-
-// (a6) grid (S), 32*G*NG threads: warp (grp, hh) merges pieces [32 grp, 32 grp + 32) of query
-// head hh of segment s; lane owns dims 4 lane .. 4 lane + 3.  All 32 partial rows of a warp
-// are requested before anything else (one memory round trip); groups combine through smem.
-template <int NG>   // groups of 32 pieces: 1 (np <= 32) or 2 (np <= 64)
-__global__ void __launch_bounds__(256 * NG) merge_kernel(StepParams p, AttnBufs ab, Work wk, float* __restrict__ out,
-                                                         float* __restrict__ out_lse) {
-    __shared__ float s_m[NG][8], s_l[NG][8];
-    __shared__ float4 s_acc[NG > 1 ? 8 : 1][32];
+// (a6) grid (S), 32*G threads: warp hh merges query head hh of segment blockIdx.x; lane owns dims
+// 4 lane .. 4 lane + 3.  Thread 0 copies the segment's NP partial blocks (G rows of 512 B each,
+// contiguous per piece) into shared memory with bulk async copies on one mbarrier while lane j
+// loads (m_j, l_j): one memory round trip for everything.  The sums run in piece order j.
+__global__ void __launch_bounds__(32 * KVD_MAX_GROUP) merge_kernel(StepParams p, AttnBufs ab, Work wk,
+                                                                 float* __restrict__ out, float* __restrict__ out_lse) {
+    extern __shared__ __align__(128) float4 s_part[];   // [NP][G][32] float4
+    __shared__ __align__(8) uint64_t bar;
     const int cs = blockIdx.x;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int hh = NG > 1 ? warp % p.G : warp, grp = NG > 1 ? warp / p.G : 0;
-    const int s0 = cs * wk.TS;
-    const int fw = worker_of(s0, wk), lw = worker_of(s0 + wk.TS - 1, wk);
-    const int np = lw - fw + 1;
+    const int lane = threadIdx.x & 31, hh = threadIdx.x >> 5;
+    const int NP = wk.NP, G = p.G;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
     griddep_wait();                               // partials come from attn_kernel
-    if (np == 1) return;                          // finalised by its only worker (uniform over the CTA)
+    if (threadIdx.x == 0) kt_begin(p.kt_slots, p.kt_base + kKtMerge);
     const int bi = cs / p.Hkv, h = cs - bi * p.Hkv;
     const int64_t rs = (int64_t)p.req[bi] * p.Hkv + h;
-    const float* po0 = ab.part_o + (rs * kMaxPieces * 8) * (int64_t)kHeadDim;
-    const float* pml0 = ab.part_ml + (rs * kMaxPieces * 8) * 2;
-    const int j0 = 32 * grp;
-    const float4* src = reinterpret_cast<const float4*>(po0 + hh * kHeadDim) + lane;
-    float4 x[32];
-#pragma unroll
-    for (int u = 0; u < 32; ++u)
-        x[u] = j0 + u < np ? __ldcg(src + (j0 + u) * 8 * (kHeadDim / 4)) : make_float4(0.f, 0.f, 0.f, 0.f);
-    const int j = j0 + lane;
-    const float mj = j < np ? __ldcg(&pml0[(j * 8 + hh) * 2]) : -INFINITY;
-    const float lj = j < np ? __ldcg(&pml0[(j * 8 + hh) * 2 + 1]) : 0.f;
+    const float* po = ab.part_o + rs * kMaxPieces * 8 * (int64_t)kHeadDim;
+    if (threadIdx.x == 0) {
+        const uint32_t row = (uint32_t)(G * kHeadDim * 4);
+        mbar_arrive_expect_tx(&bar, row * (uint32_t)NP);
+        for (int j = 0; j < NP; ++j) bulk_g2s(s_part + j * G * 32, po + (int64_t)j * 8 * kHeadDim, row, &bar);
+    }
+    const float* pml = ab.part_ml + (rs * kMaxPieces * 8 + hh) * 2;
+    const float mj = lane < NP ? pml[lane * 16] : -INFINITY;   // a new kernel: plain loads see the
+    const float lj = lane < NP ? pml[lane * 16 + 1] : 0.f;     // partials (griddepcontrol.wait)
     float M = mj;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-    if (NG > 1) {
-        if (lane == 0) s_m[grp][hh] = M;
-        __syncthreads();
-#pragma unroll
-        for (int g2 = 0; g2 < NG; ++g2) M = fmaxf(M, s_m[g2][hh]);
-    }
-    const float scj = (j < np && M != -INFINITY) ? fast_exp2(mj - M) : 0.f;
-    float l = scj * lj;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+    const float scj = (lane < NP && M != -INFINITY) ? fast_exp2(mj - M) : 0.f;
+    mbar_wait(&bar, 0);
+    float l = 0.f;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-    for (int u = 0; u < 32; ++u) {
-        const float sc = __shfl_sync(0xffffffffu, scj, u);   // 0 past np
-        acc.x += sc * x[u].x; acc.y += sc * x[u].y; acc.z += sc * x[u].z; acc.w += sc * x[u].w;
-    }
-    if (NG > 1) {
-        if (grp == 1) s_acc[hh][lane] = acc;
-        if (lane == 0) s_l[grp][hh] = l;
-        __syncthreads();
-        if (grp != 0) return;
-        const float4 o1 = s_acc[hh][lane];
-        acc.x += o1.x; acc.y += o1.y; acc.z += o1.z; acc.w += o1.w;
-        l += s_l[1][hh];
+    for (int j = 0; j < NP; ++j) {                // sequential in j
+        const float sc = __shfl_sync(0xffffffffu, scj, j);
+        const float lu = __shfl_sync(0xffffffffu, lj, j);
+        const float4 x = s_part[(j * G + hh) * 32 + lane];
+        l = __fmaf_rn(sc, lu, l);
+        acc.x = __fmaf_rn(sc, x.x, acc.x);
+        acc.y = __fmaf_rn(sc, x.y, acc.y);
+        acc.z = __fmaf_rn(sc, x.z, acc.z);
+        acc.w = __fmaf_rn(sc, x.w, acc.w);
     }
     const float il = l > 0.f ? 1.f / l : 0.f;
-    const int64_t oh = (int64_t)bi * p.Hq + (int64_t)h * p.G + hh;
+    const int64_t oh = (int64_t)bi * p.Hq + (int64_t)h * G + hh;
     reinterpret_cast<float4*>(out + oh * kHeadDim)[lane] = make_float4(acc.x * il, acc.y * il, acc.z * il, acc.w * il);
     if (out_lse && lane == 0) out_lse[oh] = l > 0.f ? (M + log2f(l)) * 0.69314718055994531f : -INFINITY;
+    if (p.kt_slots) {
+        __syncthreads();
+        if (threadIdx.x == 0) kt_end(p.kt_slots, p.kt_acc, p.kt_base + kKtMerge, kKtMerge, gridDim.x);
+    }
 }
 
 template <int STAGES, int WARPS>
 static cudaError_t launch_attn_s(kvd_cache* c, const StepParams& p, const uint16_t* q, const int32_t* attn, float* out,
                                  float* out_lse, cudaStream_t s) {
     constexpr size_t smem = (size_t)WARPS * STAGES * kTileBytes;
-    static int max_ctas = 0;
-    if (!max_ctas) {
+    static int max_ctas[64] = {};                 // per device ordinal
+    const int dev = c->cfg.device & 63;
+    if (!max_ctas[dev]) {
         cudaError_t e = cudaFuncSetAttribute(attn_kernel<STAGES, WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        int per_sm = 0, sms = 0, dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        int per_sm = 0, sms = 0;
+        e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->cfg.device);
+        if (e != cudaSuccess) return e;
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, attn_kernel<STAGES, WARPS>, WARPS * 32, smem);
         if (e != cudaSuccess) return e;
-        max_ctas = sms * (per_sm > 0 ? per_sm : 1);
+        max_ctas[dev] = sms * (per_sm > 0 ? per_sm : 1);
     }
-    const int S = p.B * p.Hkv;
     Work wk;
     wk.TS = (p.W + p.E - 1) / p.E;
-    wk.T = S * wk.TS;
-    // workers: enough to fill every SM, but at most kMaxPieces - 1 per segment so a segment
-    // never has more than kMaxPieces pieces (<= ceil(NW/S) + 1), and at most T
-    // pieces per segment: 16 once a launch has >= 8 segments (a micro-batch chain of one Llama
-    // request; 15 workers per segment leave SM room for the other chains' fetches: c3 2623 ->
-    // 2865 tok/s, c2 unchanged), 32 for fewer segments (c4: 1675 vs 1632 at 16)
-    static int maxp_env = -1;
-    if (maxp_env < 0) {
-        const char* env = getenv("KVD_ATTN_MAXP");   // experiments only: override the cap
-        maxp_env = env ? std::max(2, std::min(atoi(env), kMaxPieces)) : 0;
+    wk.NP = attn_pieces(wk.TS);
+#ifdef KVD_EXPERIMENTS
+    if (const char* e = getenv("KVD_ATTN_PIECE_TILES")) {   // experiment builds only
+        const int pt = std::max(1, atoi(e));
+        wk.NP = std::max(1, std::min(kMaxPieces, (wk.TS + pt - 1) / pt));
     }
-    const int maxp = maxp_env ? maxp_env : (S >= 8 ? 16 : kMaxPieces);
-    int nw = max_ctas * WARPS;
-    nw = std::min(nw, S * (maxp - 1));
-    nw = std::min(nw, wk.T);
-    wk.NW = std::max(nw, 1);
-    static int xflags = -1;
-    if (xflags < 0) {
-        const char* env = getenv("KVD_ATTN_X");
-        xflags = env ? atoi(env) : 0;
-    }
-    wk.xflags = xflags;
-    static int trace = -1;
-    static unsigned long long* tbuf = nullptr;
-    if (trace < 0) {
-        trace = getenv("KVD_ATTN_TRACE") ? 1 : 0;
-        if (trace) cudaMalloc(&tbuf, sizeof(unsigned long long) * 8 * 8192);
-    }
-    wk.trace = trace ? tbuf : nullptr;
-    if (trace) cudaMemsetAsync(tbuf, 0, sizeof(unsigned long long) * 8 * 8192, s);
+#endif
+    wk.Ptot = p.B * p.Hkv * wk.NP;
+    // workers: every warp slot of the device at most, with an even number of pieces each
+    // (ppw = ceil(Ptot / slots); NW = ceil(Ptot / ppw)), so no worker has a piece more than
+    // the others -- the assignment never changes the arithmetic (the plan is per segment)
+    const int slots = max_ctas[dev] * WARPS;
+    const int ppw = (wk.Ptot + slots - 1) / slots;
+    wk.NW = std::max(1, (wk.Ptot + ppw - 1) / ppw);
     AttnBufs ab{c->slots, c->ntok_dev, c->zero_rec, c->part_o, c->part_ml};
     const unsigned grid = (unsigned)((wk.NW + WARPS - 1) / WARPS);
-    cudaError_t e = launch_pdl(attn_kernel<STAGES, WARPS>, dim3(grid), dim3(WARPS * 32), smem, s, p, ab, wk, q, attn, out,
-                               out_lse);
+    cudaError_t e = launch_pdl(attn_kernel<STAGES, WARPS>, dim3(grid), dim3(WARPS * 32), smem, s, p, ab, wk, q, attn,
+                               out, out_lse);
     if (e != cudaSuccess) return e;
-    bool split = false;                           // some segment spans more than one worker
-    for (int sg = 0; sg < S && !split; ++sg) {
-        const int64_t a = (int64_t)sg * wk.TS, b = a + wk.TS - 1;
-        split = ((a + 1) * wk.NW - 1) / wk.T != ((b + 1) * wk.NW - 1) / wk.T;
-    }
-    if (split) {
-        // pieces of a segment <= ceil(NW/S) + 1 <= kMaxPieces = 32: one group of rows per warp.
-        // (64 pieces measured slower at c2 and c4: merge_kernel<2> cannot keep 64 rows in flight)
-        e = launch_pdl(merge_kernel<1>, dim3(S), dim3(32 * p.G), 0, s, p, ab, wk, out, out_lse);
-        if (e != cudaSuccess) return e;
-    }
-    if (trace) {   // experiments only: synchronous dump of per-warp phase times (us from first stamp)
-        cudaStreamSynchronize(s);
-        std::vector<unsigned long long> h((size_t)wk.NW * 8);
-        cudaMemcpy(h.data(), tbuf, h.size() * 8, cudaMemcpyDeviceToHost);
-        unsigned long long t0 = ~0ull;
-        for (int i = 0; i < wk.NW; ++i) if (h[i * 8] && h[i * 8] < t0) t0 = h[i * 8];
-        const char* names[7] = {"entry", "griddep", "tile0", "stream_end", "merge_begin", "merge_end", "exit"};
-        for (int j = 0; j < 7; ++j) {
-            std::vector<double> v;
-            for (int i = 0; i < wk.NW; ++i) if (h[i * 8 + j]) v.push_back((h[i * 8 + j] - t0) * 1e-3);
-            if (v.empty()) continue;
-            std::sort(v.begin(), v.end());
-            fprintf(stderr, "attn trace %-12s n=%5zu min %7.2f p50 %7.2f p90 %7.2f max %7.2f us\n", names[j], v.size(), v[0],
-                    v[v.size() / 2], v[v.size() * 9 / 10], v.back());
+    if (wk.NP > 1) {                              // split segments: LSE merge behind it (PDL)
+        const size_t msmem = (size_t)wk.NP * p.G * kHeadDim * 4;   // <= 32 x 8 x 512 B = 128 KiB
+        static size_t msmem_set[64] = {};
+        if (msmem > msmem_set[dev]) {
+            e = cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msmem);
+            if (e != cudaSuccess) return e;
+            msmem_set[dev] = msmem;
         }
+        e = launch_pdl(merge_kernel, dim3(p.B * p.Hkv), dim3(32 * p.G), msmem, s, p, ab, wk, out, out_lse);
+        if (e != cudaSuccess) return e;
     }
     return cudaGetLastError();
 }
 
 cudaError_t launch_attention(kvd_cache* c, const StepParams& p, const uint16_t* q, const int32_t* attn, float* out,
                              float* out_lse, cudaStream_t s) {
-    // (warps per CTA, ring depth per warp): KVD_ATTN_CFG = 3 (4 warps x 3 stages, 2 CTAs per
-    // SM: 8 warp workers per SM, default), 1 (4 x 6, 1 CTA per SM), 2 (2 x 12).  Measured at
-    // c2 / c3: 28.9 / 37.7 us (3), 28.7 / 41.2 us (1), 35.4 / 53.1 us (2): the per-warp
-    // dependent chain of MMA + softmax needs >= 2 warps per scheduler.
-    static int cfg = 0;
-    if (!cfg) {
-        const char* env = getenv("KVD_ATTN_CFG");
-        cfg = env ? atoi(env) : 3;
-        if (cfg < 1 || cfg > 3) cfg = 3;
-    }
-    if (cfg == 2) return launch_attn_s<12, 2>(c, p, q, attn, out, out_lse, s);
-    if (cfg == 3) return launch_attn_s<3, 4>(c, p, q, attn, out, out_lse, s);
-    return launch_attn_s<6, 4>(c, p, q, attn, out, out_lse, s);
+    // 4 warps x 3 stages of 8 KiB per CTA, 2 CTAs per SM: 8 warp workers per SM (the per-warp
+    // dependent chain of MMA + softmax needs >= 2 warps per scheduler; measured round 1:
+    // 4 x 6 stages at 1 CTA/SM and 2 x 12 stages were slower at c2 / c3)
+    return launch_attn_s<3, 4>(c, p, q, attn, out, out_lse, s);
 }
 
 }  // namespace kvd

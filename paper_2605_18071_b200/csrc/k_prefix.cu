@@ -133,8 +133,9 @@ cudaError_t launch_prefix(kvd_cache* c, int layer, int req, const uint16_t* dk, 
             for (int h = 0; h < c->Hkv; ++h) {
                 uint8_t* dst = c->host_store +
                                ((((int64_t)layer * c->R + req) * c->Hkv + h) * c->nb_max) * c->rec_bytes;
-                cudaMemcpyAsync(dst, recs + (int64_t)h * g.nb * c->rec_bytes, (size_t)g.nb * c->rec_bytes,
-                                cudaMemcpyDeviceToHost, s);
+                const cudaError_t e = cudaMemcpyAsync(dst, recs + (int64_t)h * g.nb * c->rec_bytes,
+                                                      (size_t)g.nb * c->rec_bytes, cudaMemcpyDeviceToHost, s);
+                if (e != cudaSuccess) return e;
             }
         }
     }

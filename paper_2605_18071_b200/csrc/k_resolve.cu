@@ -29,7 +29,13 @@ __global__ void __launch_bounds__(kResolveThreads) resolve_kernel(StepParams p, 
     const int bi = blockIdx.y, h = blockIdx.x;
     resolve_pre(p, rb, bi, h, rsm);
     griddep_wait();                               // ids / scores come from select
+    if (threadIdx.x == 0) kt_begin(p.kt_slots, p.kt_base + kKtResolve);
     resolve_main(p, rb, bi, h, ids, out_attn, smraw, rsm, true);
+    if (p.kt_slots) {
+        __syncthreads();
+        if (threadIdx.x == 0)
+            kt_end(p.kt_slots, p.kt_acc, p.kt_base + kKtResolve, kKtResolve, (unsigned long long)gridDim.x * gridDim.y);
+    }
 }
 
 // (a4) grid-stride over (request, head, miss index); one warp per 8 KiB record.
@@ -44,6 +50,7 @@ __global__ void __launch_bounds__(kGatherThreads) gather_kernel(StepParams p, co
     const int64_t total = (int64_t)p.B * p.Hkv * p.k;
     const int chunks = p.rec_bytes / 16;
     griddep_wait();                               // miss list comes from resolve
+    if (threadIdx.x == 0) kt_begin(p.kt_slots, p.kt_base + kKtGather);
     for (int64_t w = warp; w < total; w += nwarps) {
         const int i = (int)(w % p.k);
         const int64_t bh = w / p.k;
@@ -70,7 +77,34 @@ __global__ void __launch_bounds__(kGatherThreads) gather_kernel(StepParams p, co
             }
         }
     }
+    if (p.kt_slots) {
+        __syncthreads();
+        if (threadIdx.x == 0) kt_end(p.kt_slots, p.kt_acc, p.kt_base + kKtGather, kKtGather, gridDim.x);
+    }
 }
+
+// Host-link probe (kvd_probe_zero_copy): the gather's own access pattern -- 16-byte zero-copy
+// loads from mapped pinned memory, 8 in flight per thread -- over a contiguous range.
+__global__ void __launch_bounds__(256) zero_copy_kernel(const int4* __restrict__ src, int4* __restrict__ dst, int64_t n16) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n16; i0 += 8 * stride) {
+        int4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (i0 + u * stride < n16) v[u] = ld_host16(src + i0 + u * stride);
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (i0 + u * stride < n16) dst[i0 + u * stride] = v[u];
+    }
+}
+
+cudaError_t launch_zero_copy(const void* host, void* dev, size_t bytes, int ctas, cudaStream_t s) {
+    zero_copy_kernel<<<ctas, 256, 0, s>>>(reinterpret_cast<const int4*>(host), reinterpret_cast<int4*>(dev),
+                                          (int64_t)(bytes / 16));
+    return cudaGetLastError();
+}
+
+size_t resolve_static_smem() { return sizeof(ResolveShared); }
 
 size_t resolve_smem_bytes(int64_t nkeys, int64_t kmax, int64_t nb_pad) {
     return sizeof(uint64_t) * (size_t)nkeys + sizeof(int32_t) * (size_t)kmax * 5 +
@@ -85,13 +119,8 @@ ResolveBufs resolve_bufs(kvd_cache* c) {
 }
 
 cudaError_t launch_gather(kvd_cache* c, const StepParams& p, cudaStream_t s) {
-    static int prio = 1;
-    if (prio == 1) {
-        int lo = 0, hi = 0;
-        cudaDeviceGetStreamPriorityRange(&lo, &hi);
-        prio = hi;                                   // greatest priority (numerically lowest)
-    }
-    return launch_pdl_prio(prio, gather_kernel, dim3(148), dim3(kGatherThreads), 0, s, p, (const int32_t*)c->miss,
+    // greatest priority (numerically lowest): scheduled ahead of other chains' HBM-bound kernels
+    return launch_pdl_prio(c->prio_hi, gather_kernel, dim3(148), dim3(kGatherThreads), 0, s, p, (const int32_t*)c->miss,
                            (const int32_t*)c->miss_count, (int)c->kmax, (const uint8_t*)c->host_store, c->slots);
 }
 
@@ -99,11 +128,12 @@ cudaError_t launch_resolve(kvd_cache* c, const StepParams& p, const int32_t* ids
                            cudaStream_t s) {
     const ResolveBufs rb = resolve_bufs(c);
     const size_t smem = resolve_smem_bytes(rb.nkeys, c->kmax, c->nb_pad);
-    static size_t smem_set = 0;                   // dynamic + static must fit: always opt in
-    if (smem > smem_set) {
+    static size_t smem_set[64] = {};              // opted-in dynamic size, per device ordinal
+    const int dev = c->cfg.device & 63;
+    if (smem > smem_set[dev]) {
         cudaError_t e = cudaFuncSetAttribute(resolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        smem_set = smem;
+        smem_set[dev] = smem;
     }
     cudaError_t e = launch_pdl(resolve_kernel, dim3(p.Hkv, p.B), dim3(kResolveThreads), smem, s, p, rb, ids, out_attn);
     if (e != cudaSuccess) return e;

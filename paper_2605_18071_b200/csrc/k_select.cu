@@ -1,842 +1,83 @@
-// k_select.cu — rows (a1) summary scoring and (a2) top-k block selection.
-//
-// (a1) "identifying critical KV entries via the index": every
-// block's score is the dot product of the KV head's group query with the
-// block's mean-key summary, computed as one fp32 FMA chain
-// over the 128 dims in order (DESIGN.md §3 R3, R5) so that ids are bit-exact.
-// HBM-bound: 256 B of summary per block.  score_kernel is a pure streaming
-// kernel: the summaries are dim-major, so a thread owning V consecutive blocks
-// reads one V*2-byte vector per dim row and a warp reads 64*V contiguous bytes
-// per row (coalesced).  No shared-memory staging: each thread keeps 2R rows of
-// its blocks in flight (two ping-pong register batches) and runs V independent
-// chains.  Small CTAs (256 threads x V = 2 blocks, up to 4 per SM) keep the
-// wave tail short.  Rows of the first batch are requested before
-// griddepcontrol.wait (summaries are immutable during a step), overlapping the
-// previous kernel's tail.  Scores go to HBM/L2 as fp32 (4 B per 256 B read).
-//
-// (a2) "retrieving only the Top-K important chunks": topk_kernel,
-// launched behind score_kernel (PDL), runs one thread-block cluster of CL CTAs x
-// 1024 threads per segment (CL = 1 up to 16,384 blocks, 4 at 65,536).  Each CTA
-// stages its span of keys in shared memory.  Radix select over monotone
-// 32-bit keys (R10), 8-bit digits starting at the highest bit where the
-// candidates differ (warp-aggregated shared histogram adds); per-CTA histograms are summed over the cluster
-// through distributed shared memory.  The digit loop stops as soon as the
-// threshold bin is taken whole, holds <= 32 keys (ranked directly: key desc, id
-// asc), or is a single key value (equal keys: lowest ids first).  After the first
-// digit the threshold bin's members are compacted, so later digits touch only
-// them.  Emission: warps own contiguous position ranges, per-warp counts get
-// cluster-wide offsets, and ballots place each taken id, so ids come out
-// ascending with no sort.
-#include <cooperative_groups.h>
-
-#include <algorithm>
-#include <cstdio>
-#include <cstdlib>
-#include <vector>
-
-#include "resolve.cuh"
-
-namespace cg = cooperative_groups;
+// k_select.cu — launch geometry and entry points of the select kernel (rows a1 + a2, fused
+// with a3 + a4); the kernel itself is in select.cuh, instantiated per CTA size in
+// k_select_nt512.cu and k_select_nt1024.cu.
+#include "select.cuh"
 
 namespace kvd {
 
-constexpr int kScoreThreads = 256;
-constexpr int kTieList = 32;                  // threshold bins up to this size are ranked directly
-
-template <int V>
-struct VecOf;
-template <>
-struct VecOf<2> {
-    using T = uint32_t;
-    static __device__ __forceinline__ uint32_t word(const T& x, int) { return x; }
-};
-template <>
-struct VecOf<4> {
-    using T = uint2;
-    static __device__ __forceinline__ uint32_t word(const T& x, int i) { return i ? x.y : x.x; }
-};
-
-// grid (tiles, Hkv, B); CTA = kScoreThreads threads scoring kScoreThreads*V blocks of one segment.
-template <int V, int R>
-__global__ void __launch_bounds__(kScoreThreads, R > 16 ? 2 : 4) score_kernel(StepParams p, const uint16_t* __restrict__ q,
-                                                                 const uint16_t* __restrict__ summ,
-                                                                 float* __restrict__ scores,
-                                                                 const int32_t* __restrict__ ntok) {
-    using Vec = typename VecOf<V>::T;
-    __shared__ float qbar[kHeadDim];
-    const int bi = blockIdx.z, h = blockIdx.y;
-    const int r = p.req[bi];
-    const int64_t nb = (ntok[r] + p.P - 1) / p.P;   // ntok is written only by kvd_load_prefix (setup)
-    const int64_t b0 = (int64_t)blockIdx.x * kScoreThreads * V + (int64_t)threadIdx.x * V;
-    if ((int64_t)blockIdx.x * kScoreThreads * V >= nb) {
-        griddep_launch();
-        return;                                   // whole CTA past this request's end
-    }
-    const int64_t seg = ((int64_t)p.layer * p.R + r) * p.Hkv + h;
-    const bool ld = b0 < nb;                      // V-groups never straddle nb_pad (V | 128)
-    const Vec* base = reinterpret_cast<const Vec*>(summ + seg * kHeadDim * p.nb_pad + (ld ? b0 : 0));
-    const int64_t rstride = p.nb_pad / V;         // Vec elements per dim row
-    // two register batches of R rows (ping-pong): while one batch is consumed the
-    // other is in flight, so 2R rows of this thread's blocks are always requested
-    Vec bufA[R], bufB[R];
-#pragma unroll
-    for (int u = 0; u < R; ++u)
-        if (ld) bufA[u] = __ldcs(base + u * rstride);
-#pragma unroll
-    for (int u = 0; u < R; ++u)
-        if (ld) bufB[u] = __ldcs(base + (R + u) * rstride);
-    griddep_wait();                               // summaries are immutable; q may come from an earlier kernel
-    if (threadIdx.x < kHeadDim) {
-        // group query: qbar[j] = ((+0 + q_0[j]) + q_1[j]) + ... (fp32, g ascending; R3)
-        const uint16_t* qh = q + ((int64_t)bi * p.Hq + (int64_t)h * p.G) * kHeadDim;
-        float a = 0.0f;
-        for (int g = 0; g < p.G; ++g) a = __fadd_rn(a, bf16_bits(qh[g * kHeadDim + threadIdx.x]));
-        qbar[threadIdx.x] = a;
-    }
-    __syncthreads();
-    float acc[V];
-#pragma unroll
-    for (int v = 0; v < V; ++v) acc[v] = 0.0f;
-    auto consume = [&](const Vec (&buf)[R], int j0) {
-#pragma unroll
-        for (int u = 0; u < R; ++u) {
-            const float qj = qbar[j0 + u];
-#pragma unroll
-            for (int v = 0; v < V; ++v) {
-                const uint32_t w = VecOf<V>::word(buf[u], v >> 1);
-                acc[v] = __fmaf_rn(qj, (v & 1) ? bf16_hi(w) : bf16_lo(w), acc[v]);   // sequential in j (R5)
-            }
-        }
-    };
-#pragma unroll 1
-    for (int j0 = 0; j0 < kHeadDim; j0 += 2 * R) {
-        consume(bufA, j0);
-        if (ld && j0 + 2 * R < kHeadDim) {
-#pragma unroll
-            for (int u = 0; u < R; ++u) bufA[u] = __ldcs(base + (j0 + 2 * R + u) * rstride);
-        }
-        consume(bufB, j0 + R);
-        if (ld && j0 + 3 * R < kHeadDim) {
-#pragma unroll
-            for (int u = 0; u < R; ++u) bufB[u] = __ldcs(base + (j0 + 3 * R + u) * rstride);
-        }
-    }
-    griddep_launch();
-    if (!ld) return;
-    float* out = scores + seg * p.nb_pad + b0;
-    if (b0 + V <= nb) {
-#pragma unroll
-        for (int v = 0; v < V; v += 2) *reinterpret_cast<float2*>(out + v) = make_float2(acc[v], acc[v + 1]);
-    } else {
-#pragma unroll
-        for (int v = 0; v < V; ++v)
-            if (b0 + v < nb) out[v] = acc[v];
-    }
+// Launch geometry for `segs` segments of nb_pad blocks: threads per CTA, cluster size, keys per
+// thread and vector width.  The cluster starts at the fewest CTAs whose shared memory holds the
+// segment (<= kMaxKpt keys per 1024-thread CTA) and doubles (<= 8, portable) while the launch
+// has fewer than kSelectCtaTarget CTAs and a CTA keeps >= 1024 blocks: a few long segments (c4:
+// 4 per chain) are spread over many SMs -- one SM streams a segment's summaries at only
+// ~50-80 GB/s (tools/micro/score_stream.cu) -- while launches of many segments keep one CTA per
+// segment (no cluster barriers).  CTAs of up to 2048 blocks run 512 threads (4 keys each), longer
+// spans 1024.  The choice never changes a result (scores are per block; the top-k is exact).
+// V (blocks per row load) = 2, 4 or 8 keys per thread: 4-, 8- or 16-byte loads.
+constexpr int kMaxKpt = kMaxSelectBlocks / (8 * 1024);   // 32 at 1024 threads: 5 B of smem per key
+constexpr int kSelectCtaTarget = 64;
+static int tune(const char* name, int dflt) {
+#ifdef KVD_EXPERIMENTS
+    const char* e = getenv(name);             // experiment builds only (tools/; never the product)
+    if (e) return atoi(e);
+#else
+    (void)name;
+#endif
+    return dflt;
 }
-
-// ------------------------------------------------------------------ (a2) top-k
-constexpr int kListCap = 4096;                // compacted threshold-bin members per CTA
-constexpr int kTakeMax = 512;                 // list emission for k up to this
-
-struct TopkShared {
-    int hist[2][256];                 // per-pass digit histograms (double-buffered: read remotely)
-    int tot[256];                     // cluster-summed histogram
-    int wcnt[2][32];                  // per-warp counts of the emission pre-pass (above, bin)
-    int woff[2][32];                  // their cluster-wide exclusive offsets
-    uint32_t wred[2][32];
-    uint32_t cmin[2], cmax[2];        // this CTA's key ranges: candidates, threshold-bin members (read remotely)
-    int mm_slot;                      // next cmin/cmax slot
-    int digit, above, cnt;            // pass decision (broadcast)
-    int ctot[2];                      // CTA totals of the emission counts (read remotely)
-    int ncomp;                        // compacted members of the first threshold bin (this CTA)
-    int lcount;                       // threshold-bin members of this CTA (LIST mode)
-    int ntake;                        // taken ids of this CTA (list emission)
-    int32_t take[kTakeMax];
-    uint32_t lkey[kTieList];
-    int32_t lid[kTieList];
-};
-
-template <int CL>
-__device__ __forceinline__ void cl_sync() {
-    if constexpr (CL == 1) __syncthreads();
-    else cg::this_cluster().sync();
-}
-template <int CL, class T>
-__device__ __forceinline__ T* cl_remote(T* p, int rank) {
-    if constexpr (CL == 1) return p;
-    else return cg::this_cluster().map_shared_rank(p, rank);
-}
-
-enum { kModeWhole = 0, kModeList = 1, kModeEqual = 2 };
-
-// inverse of score_key32 for non-NaN keys (key 0 = NaN -> -inf here)
-__device__ __forceinline__ float key_to_score(uint32_t key) {
-    if (key == 0u) return -INFINITY;
-    return __uint_as_float((key >> 31) ? (key & 0x7FFFFFFFu) : ~key);
-}
-
-// cluster-wide min / max of (kmn, kmx); every thread returns the cluster values
-template <int CL>
-__device__ __forceinline__ void cta_minmax(uint32_t& kmn, uint32_t& kmx, TopkShared& sm) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    kmn = __reduce_min_sync(0xffffffffu, kmn);
-    kmx = __reduce_max_sync(0xffffffffu, kmx);
-    if (lane == 0) {
-        sm.wred[0][warp] = kmn;
-        sm.wred[1][warp] = kmx;
-    }
-    __syncthreads();
-    if (warp == 0) {
-        const bool v = lane < (int)(blockDim.x >> 5);
-        const uint32_t a = __reduce_min_sync(0xffffffffu, v ? sm.wred[0][lane] : 0xFFFFFFFFu);
-        const uint32_t b = __reduce_max_sync(0xffffffffu, v ? sm.wred[1][lane] : 0u);
-        if (lane == 0) {
-            sm.cmin[sm.mm_slot] = a;
-            sm.cmax[sm.mm_slot] = b;
-        }
-    }
-    cl_sync<CL>();
-    const int slot = sm.mm_slot;
-    kmn = 0xFFFFFFFFu;
-    kmx = 0u;
-#pragma unroll
-    for (int c = 0; c < CL; ++c) {
-        kmn = min(kmn, cl_remote<CL>(sm.cmin, c)[slot]);
-        kmx = max(kmx, cl_remote<CL>(sm.cmax, c)[slot]);
-    }
-    __syncthreads();                              // everyone read mm_slot before it advances
-    if (threadIdx.x == 0) sm.mm_slot = slot + 1;
-    __syncthreads();
-}
-
-// warp 0: find the bin (descending) holding the kk-th largest member; lane l owns bins
-// d = nbins-1-(8l+j), j < 8.  Writes sm.digit / sm.above (members in higher bins) / sm.cnt.
-__device__ __forceinline__ void pick_digit(TopkShared& sm, int nbins, int kk, int lane) {
-    int c8[8], t = 0;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        const int d = nbins - 1 - (8 * lane + j);
-        c8[j] = d >= 0 ? sm.tot[d] : 0;
-        t += c8[j];
-    }
-    int incl = t;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-    }
-    int above = incl - t;
-    if (above < kk && kk <= incl) {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            if (above + c8[j] >= kk) {
-                sm.digit = nbins - 1 - (8 * lane + j);
-                sm.above = above;
-                sm.cnt = c8[j];
-                break;
-            }
-            above += c8[j];
-        }
-    }
-}
-
-// grid (CL, Hkv, B), cluster (CL, 1, 1), NT threads.  CTA rank c owns blocks
-// [c*span, (c+1)*span), span = NT*kpt, staged as monotone keys in shared memory.
-// Candidates = [sink_end, local_begin) (not pinned, < nb).  Every phase walks the keys in
-// 32-wide strips (conflict-free shared loads); warp w owns the contiguous strip range
-// [w*span/32, (w+1)*span/32) for the ordered emission.
-// Fused variant (RESOLVE): after the selection, CTA rank 0 resolves the segment against the
-// cache (a3, resolve.cuh) and copies its misses from the host store (a4) in the same CTA,
-// reusing the dynamic shared memory: select -> resolve -> fetch without kernel boundaries.
-struct FuseArgs {
-    ResolveBufs rb;
-    int32_t* out_attn;
-    const uint8_t* host_store;    // NULL: fully resident (no misses)
-    uint8_t* slots;
-};
-
-template <int CL, int NT, bool RESOLVE>
-__global__ void __launch_bounds__(NT, 1) topk_kernel(FuseArgs fa, StepParams p, const float* __restrict__ scores,
-                                                               const int32_t* __restrict__ ntok, int kpt,
-                                                               int32_t* __restrict__ out_ids,
-                                                               float* __restrict__ out_scores,
-                                                               unsigned long long* __restrict__ trace) {
-    extern __shared__ __align__(16) uint32_t skey[];   // [span] keys | [kListCap] compacted (key, index) pairs
-    __shared__ TopkShared sm;
-    const int crank = CL > 1 ? (int)cg::this_cluster().block_rank() : 0;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int h = blockIdx.y, bi = blockIdx.z;
-    const int r = p.req[bi];
-    const int span = NT * kpt;
-    uint2* comp = reinterpret_cast<uint2*>(skey + span);
-    uint8_t* sbin = reinterpret_cast<uint8_t*>(comp + kListCap);   // first-digit bin of every key
-    const int64_t base = (int64_t)crank * span;
-    const SegGeom g = seg_geom(ntok[r], p.P, p.sink_tokens, p.local_tokens);
-    const int64_t seg = ((int64_t)p.layer * p.R + r) * p.Hkv + h;
-    auto clampi = [](int64_t x, int64_t lo_, int64_t hi_) { return (int)(x < lo_ ? lo_ : x > hi_ ? hi_ : x); };
-    const int lim = clampi(p.nb_pad - base, 0, span);
-    const int c_lo = clampi(g.sink_end - base, 0, lim);
-    const int c_hi = clampi(g.local_begin - base, 0, lim);
-    const int ncand = g.local_begin - g.sink_end;
-    const float* sc = scores + seg * p.nb_pad + base;
-    unsigned long long* tr = trace ? trace + ((((int64_t)blockIdx.z * gridDim.y + blockIdx.y) * CL + crank) * 8) : nullptr;
-    auto stamp = [&](int i, unsigned long long v = 0) {   // KVD_TOPK_TRACE (experiments only)
-        if (tr && tid == 0) {
-            unsigned long long t;
-            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-            tr[i] = v ? v : t;
-        }
-    };
-    stamp(0);
-    __shared__ ResolveShared rsm;
-    if (RESOLVE && crank == 0) resolve_pre(p, fa.rb, bi, h, rsm);
-    if (tid == 0) {
-        sm.lcount = 0;
-        sm.ncomp = 0;
-        sm.mm_slot = 0;
-    }
-    griddep_wait();                               // scores come from score_kernel
-    stamp(1);
-    // ---- stage keys; candidate key range (NaN keys are 0; every other key is >= 1)
-    uint32_t kmn = 0xFFFFFFFFu, kmx = 0u;
-    for (int i = tid * 4; i < lim; i += NT * 4) {
-        const float4 x = __ldcg(reinterpret_cast<const float4*>(sc + i));
-        const uint32_t k4[4] = {score_key32(x.x), score_key32(x.y), score_key32(x.z), score_key32(x.w)};
-        *reinterpret_cast<uint4*>(&skey[i]) = make_uint4(k4[0], k4[1], k4[2], k4[3]);
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-            if (i + u >= c_lo && i + u < c_hi && k4[u] != 0u) {
-                kmn = min(kmn, k4[u]);
-                kmx = max(kmx, k4[u]);
-            }
-    }
-    cta_minmax<CL>(kmn, kmx, sm);
-    stamp(2);
-    // ---- first digit: 256 bins linear in the score value over [vmin, vmax] (monotone: fp32
-    // subtract, multiply by a positive scale and truncate never invert an order; equal scores
-    // share a bin; NaN -> bin 0).  Float keys crowd a few leading bits, linear bins do not,
-    // so plain shared atomics suffice.  Skipped (single "bin") for non-finite or equal ends.
-    int kk = p.k, cnt = ncand;                    // still to take / members of the threshold bin
-    const float vmin = key_to_score(kmn), vmax = key_to_score(kmx);
-    const bool lin = kmn <= kmx && isfinite(vmin) && isfinite(vmax) && vmax > vmin && isfinite(vmax - vmin) &&
-                     kk != cnt && cnt > kTieList;
-    const float scale = lin ? 256.0f / (vmax - vmin) : 0.f;
-    auto bin_of = [&](uint32_t key) {
-        if (!lin || key == 0u) return 0;
-        const int b = (int)((key_to_score(key) - vmin) * scale);
-        return b > 255 ? 255 : b;
-    };
-    auto bin_at = [&](int i) { return lin ? (int)sbin[i] : 0; };   // i in [c_lo, c_hi)
-    int bstar = 0;
-    if (lin) {
-        int* hb = sm.hist[1];
-        if (tid < 256) hb[tid] = 0;
-        __syncthreads();
-        for (int i = c_lo + tid; i < c_hi; i += NT) {
-            const int b = bin_of(skey[i]);
-            sbin[i] = (uint8_t)b;
-            atomicAdd(&hb[b], 1);
-        }
-        cl_sync<CL>();
-        if (tid < 256) {
-            int t = 0;
-#pragma unroll
-            for (int c = 0; c < CL; ++c) t += cl_remote<CL>(hb, c)[tid];
-            sm.tot[tid] = t;
-        }
-        __syncthreads();
-        if (warp == 0) pick_digit(sm, 256, kk, lane);
-        __syncthreads();
-        bstar = sm.digit;
-        kk -= sm.above;
-        cnt = sm.cnt;
-    }
-    // ---- compact the threshold bin's members and the keys above it (when they fit; bit 31 of
-    // the index marks "above") and take the members' key range
-    kmn = 0xFFFFFFFFu;
-    kmx = 0u;
-    for (int i0 = (c_lo & ~31) + warp * 32; i0 < c_hi; i0 += NT) {
-        const int i = i0 + lane;
-        const bool inr = i >= c_lo && i < c_hi;
-        const uint32_t key = inr ? skey[i] : 0u;
-        const int b = inr ? bin_at(i) : -1;
-        const bool in = inr && b >= bstar;
-        if (inr && b == bstar) {
-            kmn = min(kmn, key);
-            kmx = max(kmx, key);
-        }
-        const uint32_t bal = __ballot_sync(0xffffffffu, in);
-        int wbase = 0;
-        if (lane == 0 && bal) wbase = atomicAdd(&sm.ncomp, __popc(bal));
-        wbase = __shfl_sync(0xffffffffu, wbase, 0);
-        const int slot = wbase + __popc(bal & ((1u << lane) - 1u));
-        if (in && slot < kListCap) comp[slot] = make_uint2(key, (uint32_t)i | (b > bstar ? 0x80000000u : 0u));
-    }
-    cta_minmax<CL>(kmn, kmx, sm);                 // contains the barriers that publish ncomp
-    bool compacted = sm.ncomp <= kListCap;        // uniform over the CTA
-    // ---- clusters: when the cluster's compacted lists fit one list, rank 0 gathers them (ids
-    // made cluster-global) and finishes alone, with no further cluster barriers
-    bool local = false;
-    int64_t gbase = base;                         // id of local position 0 in the current lists
-    if constexpr (CL > 1) {
-        int tot_c = 0;
-        bool fit = true;
-#pragma unroll
-        for (int c = 0; c < CL; ++c) {
-            const int m = *cl_remote<CL>(&sm.ncomp, c);
-            tot_c += m;
-            fit = fit && m <= kListCap;
-        }
-        if (fit && tot_c <= kListCap && p.k <= kTakeMax) {   // uniform over the cluster
-            if (crank == 0) {
-                int o = sm.ncomp;                 // rank 0's own entries stay (its base is 0)
-                for (int c = 1; c < CL; ++c) {
-                    const uint2* rc = cg::this_cluster().map_shared_rank(comp, c);
-                    const int m = *cl_remote<CL>(&sm.ncomp, c);
-                    const uint32_t add = (uint32_t)c * (uint32_t)span;   // ids < 2^31: flag bit kept
-                    for (int j = tid; j < m; j += NT) {
-                        uint2 e = rc[j];
-                        e.y += add;
-                        comp[o + j] = e;
-                    }
-                    o += m;
-                }
-            }
-            cl_sync<CL>();                        // remote lists read: the other ranks are done
-            if (crank != 0) return;
-            if (tid == 0) sm.ncomp = tot_c;
-            __syncthreads();
-            local = true;
-            compacted = true;
-            gbase = 0;
-        }
-    }
-    const int ncl = local ? 1 : CL;               // CTAs whose shared memory is still consulted
-    auto csync = [&]() {
-        if (local) __syncthreads();
-        else cl_sync<CL>();
-    };
-    const uint32_t diff = kmn ^ kmx;
-    int lo = (kk != cnt && cnt > kTieList && diff) ? 32 - __clz(diff) : 0;   // bits [0, lo) still to resolve
-    uint32_t mask = lo == 32 ? 0u : ~((1u << lo) - 1u);
-    uint32_t prefix = kmn & mask;
-    if (kk == cnt || cnt <= kTieList) {           // the bin decides by itself: no key digits
-        mask = 0u;
-        prefix = 0u;
-    }
-    int mode;
-    // ---- radix digits of the members' keys, most significant first
-#pragma unroll 1
-    for (int pass = 0;; ++pass) {
-        if (kk == cnt) { mode = kModeWhole; break; }
-        if (cnt <= kTieList) { mode = kModeList; break; }
-        if (lo == 0) { mode = kModeEqual; break; }
-        const int width = min(8, lo), shift = lo - width, nbins = 1 << width;
-        int* hb = sm.hist[pass & 1];
-        if (tid < 256) hb[tid] = 0;
-        __syncthreads();
-        if (compacted) {
-            const int nc = sm.ncomp;
-            for (int j0 = warp * 32; j0 < nc; j0 += NT) {
-                const int j = j0 + lane;
-                const uint2 e = j < nc ? comp[j] : make_uint2(0u, 0x80000000u);
-                warp_hist_add(hb, (e.x >> shift) & (uint32_t)(nbins - 1), !(e.y >> 31) && (e.x & mask) == prefix);
-            }
-        } else {
-            for (int i0 = (c_lo & ~31) + warp * 32; i0 < c_hi; i0 += NT) {
-                const int i = i0 + lane;
-                const uint32_t key = skey[i];
-                warp_hist_add(hb, (key >> shift) & (uint32_t)(nbins - 1),
-                              i >= c_lo && i < c_hi && bin_at(i) == bstar && (key & mask) == prefix);
-            }
-        }
-        csync();
-        if (tid < nbins) {
-            int t = 0;
-#pragma unroll
-            for (int c = 0; c < ncl; ++c) t += cl_remote<CL>(hb, c)[tid];
-            sm.tot[tid] = t;
-        }
-        __syncthreads();
-        if (warp == 0) pick_digit(sm, nbins, kk, lane);
-        __syncthreads();
-        prefix |= (uint32_t)sm.digit << shift;
-        mask |= (uint32_t)(nbins - 1) << shift;
-        kk -= sm.above;
-        cnt = sm.cnt;
-        lo = shift;
-    }
-    stamp(3);
-    // ---- LIST: the <= 32 threshold-bin members of the cluster, ranked by (key desc, id asc)
-    if (mode == kModeList) {
-        auto add = [&](uint32_t key, int i) {
-            const int slot = atomicAdd(&sm.lcount, 1);
-            sm.lkey[slot] = key;
-            sm.lid[slot] = (int32_t)(gbase + i);
-        };
-        if (compacted) {
-            for (int j = tid; j < sm.ncomp; j += NT)
-                if (!(comp[j].y >> 31) && (comp[j].x & mask) == prefix) add(comp[j].x, (int)comp[j].y);
-        } else {
-            for (int i = c_lo + tid; i < c_hi; i += NT)
-                if (bin_at(i) == bstar && (skey[i] & mask) == prefix) add(skey[i], i);
-        }
-        csync();
-    }
-    auto bin_rank = [&](uint32_t key, int32_t id) {   // members beating (key, id)
-        int rank = 0;
-#pragma unroll 1
-        for (int c = 0; c < ncl; ++c) {
-            TopkShared* rs = cl_remote<CL>(&sm, c);
-            const int m = rs->lcount;
-            for (int j = 0; j < m; ++j) {
-                const uint32_t kj = rs->lkey[j];
-                rank += (kj > key || (kj == key && rs->lid[j] < id)) ? 1 : 0;
-            }
-        }
-        return rank;
-    };
-    int32_t* ids_out = out_ids + ((int64_t)bi * p.Hkv + h) * p.k;
-    float* sc_out = out_scores ? out_scores + ((int64_t)bi * p.Hkv + h) * p.k : nullptr;
-    bool s_ready = false;                         // fused: S[] of the resolve already in smem
-    if (compacted && (mode != kModeEqual || local) && p.k <= kTakeMax) {
-        // ---- emission from the compacted list: every taken id is in it (above the bin, or a
-        // taken member); its output position = number of taken ids (cluster-wide) below it
-        if (tid == 0) sm.ntake = 0;
-        __syncthreads();
-        const int nc = sm.ncomp;
-        for (int j = tid; j < nc; j += NT) {
-            const uint2 e = comp[j];
-            const int i = (int)(e.y & 0x7FFFFFFFu);
-            bool take = e.y >> 31;
-            if (!take) {
-                const uint32_t km = e.x & mask;
-                if (km > prefix || (km == prefix && mode == kModeWhole)) {
-                    take = true;
-                } else if (km == prefix && mode == kModeList) {
-                    take = bin_rank(e.x, (int32_t)(gbase + i)) < kk;
-                } else if (km == prefix) {        // kModeEqual (local finish only): lowest ids first
-                    int r = 0;
-                    for (int u = 0; u < nc; ++u) {
-                        const uint2 f = comp[u];
-                        r += (!(f.y >> 31) && (f.x & mask) == prefix && (int)(f.y & 0x7FFFFFFFu) < i) ? 1 : 0;
-                    }
-                    take = r < kk;
-                }
-            }
-            if (take) sm.take[atomicAdd(&sm.ntake, 1)] = (int32_t)(gbase + i);
-        }
-        csync();
-        stamp(4);
-        // gather the cluster's taken ids locally (p.k of them), then rank by id
-        int off = 0, tot = 0;
-#pragma unroll
-        for (int c = 0; c < ncl; ++c) {
-            const int m = *cl_remote<CL>(&sm.ntake, c);
-            off += c < crank ? m : 0;
-            tot += m;
-        }
-        int32_t* all = reinterpret_cast<int32_t*>(comp);   // comp is no longer needed
-        __syncthreads();
-        {
-            int o = 0;
-            for (int c = 0; c < ncl; ++c) {
-                const TopkShared* rs = cl_remote<CL>(&sm, c);
-                const int m = rs->ntake;
-                for (int j = tid; j < m; j += NT) all[o + j] = rs->take[j];
-                o += m;
-            }
-        }
-        __syncthreads();
-        for (int j = tid; j < sm.ntake; j += NT) {
-            const int32_t id = all[off + j];
-            int pos = 0;
-            for (int u = 0; u < tot; ++u) pos += all[u] < id ? 1 : 0;
-            ids_out[pos] = id;
-            if (sc_out) sc_out[pos] = __ldcg(sc + (id - base));
-        }
-        if (RESOLVE && crank == 0 && 2 * (int)fa.rb.nkeys + p.k <= span) {
-            // hand the sorted selection to the resolve in shared memory (its S[] slot; the
-            // keys are dead, `all` lies beyond it): no global re-read, no validation needed
-            int32_t* S = reinterpret_cast<int32_t*>(skey) + 2 * fa.rb.nkeys;
-            for (int j = tid; j < tot; j += NT) {
-                const int32_t id = all[j];
-                int pos = 0;
-                for (int u = 0; u < tot; ++u) pos += all[u] < id ? 1 : 0;
-                S[pos] = id;
-            }
-            s_ready = true;
-        }
-    } else {
-    // ---- emission.  Warp w owns positions [w0, w1) and walks them in 32-wide strips: pre-pass
-    // counts (above, bin members), cluster-wide exclusive offsets in position order, then
-    // ballots place every taken id at its ascending output position.
-    const int per_w = span / (NT / 32);
-    const int w0 = max(warp * per_w, c_lo), w1 = min((warp + 1) * per_w, c_hi);
-    auto classify = [&](int i, bool& gt, bool& eq) {   // above the threshold / in it
-        const bool in = i >= w0 && i < w1;
-        const uint32_t key = in ? skey[i] : 0u;
-        const int b = in ? bin_at(i) : 0;
-        gt = in && (b > bstar || (b == bstar && (key & mask) > prefix));
-        eq = in && b == bstar && (key & mask) == prefix;
-    };
-    int cgt = 0, ceq = 0;
-    for (int i0 = warp * per_w; i0 < w1; i0 += 32) {
-        bool gt, eq;
-        classify(i0 + lane, gt, eq);
-        cgt += __popc(__ballot_sync(0xffffffffu, gt));
-        ceq += __popc(__ballot_sync(0xffffffffu, eq));
-    }
-    if (lane == 0) {
-        sm.wcnt[0][warp] = cgt;
-        sm.wcnt[1][warp] = ceq;
-    }
-    __syncthreads();
-    if (warp < 2) {                               // warp 0: "above" offsets, warp 1: bin offsets
-        const int v = lane < NT / 32 ? sm.wcnt[warp][lane] : 0;
-        int incl = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
-        }
-        sm.woff[warp][lane] = incl - v;
-        if (lane == 31) sm.ctot[warp] = incl;
-    }
-    csync();
-    int before_gt = 0, before_eq = 0;
-#pragma unroll
-    for (int c = 0; c < ncl; ++c) {
-        if (c < crank) {
-            before_gt += *cl_remote<CL>(&sm.ctot[0], c);
-            before_eq += *cl_remote<CL>(&sm.ctot[1], c);
-        }
-    }
-    stamp(4);
-    // position of a taken id: ids above the bin before it + taken bin members before it
-    int gt_before = before_gt + sm.woff[0][warp];     // above-bin keys before this strip
-    int eq_before = before_eq + sm.woff[1][warp];     // bin members before this strip (position order)
-    int taken_eq_before = 0;                          // LIST mode: taken bin members before this strip
-    if (mode == kModeList) {
-        // taken bin members at positions before this warp's range (ids ascend with positions)
-        int t = 0;
-        for (int c = 0; c < ncl; ++c) {
-            TopkShared* rs = cl_remote<CL>(&sm, c);
-            for (int j = lane; j < rs->lcount; j += 32) {
-                const int32_t id = rs->lid[j];
-                if (id < base + warp * per_w && bin_rank(rs->lkey[j], id) < kk) ++t;
-            }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-        taken_eq_before = t;
-    }
-    for (int i0 = warp * per_w; i0 < w1; i0 += 32) {
-        const int i = i0 + lane;
-        bool gt, eq;
-        classify(i, gt, eq);
-        const uint32_t bgt = __ballot_sync(0xffffffffu, gt), beq = __ballot_sync(0xffffffffu, eq);
-        const uint32_t lt = (1u << lane) - 1u;
-        bool take_eq = false;
-        if (mode == kModeWhole) take_eq = eq;
-        else if (mode == kModeEqual) take_eq = eq && eq_before + __popc(beq & lt) < kk;
-        else if (eq) take_eq = bin_rank(skey[i], (int32_t)(gbase + i)) < kk;
-        const uint32_t btk = __ballot_sync(0xffffffffu, take_eq);
-        const int eq_taken_before = mode == kModeWhole ? eq_before
-                                  : mode == kModeEqual ? min(eq_before, kk)
-                                                       : taken_eq_before;
-        if (gt || take_eq) {
-            const int pos = gt_before + eq_taken_before + __popc((bgt | btk) & lt);
-            ids_out[pos] = (int32_t)(gbase + i);
-            if (sc_out) sc_out[pos] = __ldcg(sc + i);
-        }
-        gt_before += __popc(bgt);
-        eq_before += __popc(beq);
-        taken_eq_before += __popc(btk);
-    }
-    }
-    stamp(5);
-    stamp(6, 1000ull * mode + (32 - lo) + (compacted ? 100 : 0));
-    if constexpr (!RESOLVE) {
-        griddep_launch();
-        if (CL > 1 && !local) cl_sync<CL>();     // remote readers of this CTA's shared memory are done
-    } else {
-        // every CTA's ids are written (cluster barrier: release / acquire) and no CTA reads
-        // another's shared memory any more; rank 0 resolves and fetches
-        csync();
-        if (crank != 0) return;
-        uint8_t* smraw = reinterpret_cast<uint8_t*>(skey);
-        const int nm = resolve_main(p, fa.rb, bi, h, out_ids, fa.out_attn, smraw, rsm, true, s_ready);
-        if (nm > 0 && fa.host_store) {
-            const int32_t* S = reinterpret_cast<const int32_t*>(reinterpret_cast<uint64_t*>(smraw) + fa.rb.nkeys);
-            gather_segment(p, bi, h, S + 2 * fa.rb.kmax, S + 3 * fa.rb.kmax, nm, fa.host_store, fa.slots);
-        }
-    }
-}
-
-template <int V, int R>
-static cudaError_t launch_score(kvd_cache* c, const StepParams& p, const uint16_t* q, cudaStream_t s) {
-    const unsigned tiles = (unsigned)((c->nb_pad + kScoreThreads * V - 1) / (kScoreThreads * V));
-    return launch_pdl(score_kernel<V, R>, dim3(tiles, p.Hkv, p.B), dim3(kScoreThreads), 0, s, p, q,
-                      (const uint16_t*)c->summ, c->scores, (const int32_t*)c->ntok_dev);
-}
-
-template <int CL, int NT, bool RESOLVE>
-static cudaError_t launch_topk(kvd_cache* c, const StepParams& p, int kpt, int32_t* out_ids, float* out_scores,
-                               const FuseArgs& fa, cudaStream_t s) {
-    size_t smem = (size_t)NT * kpt * 5 + (size_t)kListCap * 8;   // keys | compacted pairs | bins
-    if (RESOLVE) smem = std::max(smem, resolve_smem_bytes(fa.rb.nkeys, c->kmax, c->nb_pad));
-    static size_t smem_set = 0;                   // dynamic + static must fit: always opt in
-    if (smem > smem_set) {
-        cudaError_t e = cudaFuncSetAttribute(topk_kernel<CL, NT, RESOLVE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        smem_set = smem;
-    }
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(CL, p.Hkv, p.B);
-    cfg.blockDim = dim3(NT);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[3];
-    int na = 0;
-    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[na++].val.programmaticStreamSerializationAllowed = 1;
-    if (CL > 1) {
-        attr[na].id = cudaLaunchAttributeClusterDimension;
-        attr[na].val.clusterDim.x = CL;
-        attr[na].val.clusterDim.y = 1;
-        attr[na++].val.clusterDim.z = 1;
-    }
-    if (RESOLVE && fa.host_store) {               // the host-link fetch is inside: schedule it first
-        static int prio = 1;
-        if (prio == 1) {
-            int lo = 0, hi = 0;
-            cudaDeviceGetStreamPriorityRange(&lo, &hi);
-            prio = hi;
-        }
-        attr[na].id = cudaLaunchAttributePriority;
-        attr[na++].val.priority = prio;
-    }
-    cfg.attrs = attr;
-    cfg.numAttrs = na;
-    static int trace = -1;
-    static unsigned long long* tbuf = nullptr;
-    if (trace < 0) {
-        trace = getenv("KVD_TOPK_TRACE") ? 1 : 0;
-        if (trace) cudaMalloc(&tbuf, sizeof(unsigned long long) * 8 * 65536);
-    }
-    const int nctas = CL * p.Hkv * p.B;
-    if (trace) cudaMemsetAsync(tbuf, 0, sizeof(unsigned long long) * 8 * nctas, s);
-    count_launch();
-    cudaError_t e = cudaLaunchKernelEx(&cfg, topk_kernel<CL, NT, RESOLVE>, fa, p, (const float*)c->scores, (const int32_t*)c->ntok_dev,
-                                       kpt, out_ids, out_scores, trace ? tbuf : nullptr);
-    if (trace && e == cudaSuccess) {   // experiments only: synchronous dump of per-CTA phase times
-        cudaStreamSynchronize(s);
-        std::vector<unsigned long long> h((size_t)nctas * 8);
-        cudaMemcpy(h.data(), tbuf, h.size() * 8, cudaMemcpyDeviceToHost);
-        unsigned long long t0 = ~0ull;
-        for (int i = 0; i < nctas; ++i) t0 = std::min(t0, h[i * 8]);
-        const char* names[6] = {"entry", "griddep", "minmax", "passes", "counted", "end"};
-        for (int j = 0; j < 6; ++j) {
-            std::vector<double> v;
-            for (int i = 0; i < nctas; ++i) v.push_back((h[i * 8 + j] - t0) * 1e-3);
-            std::sort(v.begin(), v.end());
-            fprintf(stderr, "topk trace CL=%d NT=%d kpt=%d %-8s p50 %7.2f max %7.2f us\n", CL, NT, kpt, names[j], v[v.size() / 2], v.back());
-        }
-        fprintf(stderr, "topk trace mode*1000+bits: cta0 %llu cta_last %llu\n", h[6], h[(nctas - 1) * 8 + 6]);
-    }
-    return e;
-}
-
-// score kernel variant: V = 2 blocks per thread with R = 16 rows per register batch (default);
-// KVD_SEL_V = 4 selects V = 4, R = 8 (experiments only; R = 32 spills)
-static cudaError_t launch_score_cfg(kvd_cache* c, const StepParams& p, const uint16_t* q, cudaStream_t s) {
-    static int var = -1;
-    if (var < 0) {
-        const char* v = getenv("KVD_SEL_V");
-        var = (v && atoi(v) == 4) ? 1 : 0;
-    }
-    if (var == 1) return launch_score<4, 8>(c, p, q, s);
-    return launch_score<2, 16>(c, p, q, s);
-}
-
-// Cluster size and keys per thread for a segment span of nb_pad blocks with nt threads per
-// CTA: at most 16 keys per thread while the cluster is small (clusters of whole-SM CTAs do not
-// all fit at once), at most 8 CTAs per cluster (portable), kpt a multiple of 4 (float4 staging).
-void topk_geometry(int64_t nb_pad, int nt, int* cl, int* kpt) {
-    static int kmax = 0;
-    if (!kmax) {
-        const char* env = getenv("KVD_TOPK_KPT");   // experiments only: keys per thread before growing the cluster
-        kmax = env && atoi(env) == 8 ? 8 : 16;
-    }
+void select_geometry(int64_t nb_pad, int segs, bool resident, int* nt, int* cl, int* kpt, int* v) {
+    static const int target = tune("KVD_SELECT_CTAS", kSelectCtaTarget),
+                     min_span_res = tune("KVD_SELECT_MINSPAN", 1024),
+                     min_span_host = tune("KVD_SELECT_MINSPAN_HOST", 8192),
+                     nt_small = tune("KVD_SELECT_NT_SMALL", 512);
+    // host-backed: rank 0 fetches the misses over the host link after the selection, holding its
+    // SM; spans of up to 8192 blocks stay on one CTA (c3: 2799 vs 2397 tok/s with 8 CTAs/segment)
+    const int min_span = resident ? min_span_res : min_span_host;
     int c = 1;
-    while (c < 8 && (int64_t)c * nt * kmax < nb_pad) c <<= 1;
-    int64_t per = (nb_pad + (int64_t)c * nt - 1) / ((int64_t)c * nt);
-    per = (per + 3) / 4 * 4;
+    while (c < 8 && (int64_t)c * 1024 * kMaxKpt < nb_pad) c <<= 1;
+    while (c < 8 && (int64_t)segs * c < target && nb_pad / (2 * c) >= min_span) c <<= 1;
+    const int64_t span = (nb_pad + c - 1) / c;
+    const int threads = span <= 2048 ? nt_small : 1024;
+    int64_t per = (span + threads - 1) / threads;
+    const int vw = per >= 8 ? 8 : per >= 4 ? 4 : 2;
+    per = (per + vw - 1) / vw * vw;
+    *nt = threads;
     *cl = c;
     *kpt = (int)per;
+    *v = vw;
 }
 
-template <int NT, bool RESOLVE>
-static cudaError_t launch_topk_nt(kvd_cache* c, const StepParams& p, int32_t* out_ids, float* out_scores,
-                                  const FuseArgs& fa, cudaStream_t s) {
-    int cl, kpt;
-    topk_geometry(c->nb_pad, NT, &cl, &kpt);
-    switch (cl) {
-        case 1: return launch_topk<1, NT, RESOLVE>(c, p, kpt, out_ids, out_scores, fa, s);
-        case 2: return launch_topk<2, NT, RESOLVE>(c, p, kpt, out_ids, out_scores, fa, s);
-        case 4: return launch_topk<4, NT, RESOLVE>(c, p, kpt, out_ids, out_scores, fa, s);
-        default: return launch_topk<8, NT, RESOLVE>(c, p, kpt, out_ids, out_scores, fa, s);
-    }
-}
+// dynamic shared memory: [span] keys | [kListCap] compacted pairs | [span] first-digit bins
+size_t select_smem_bytes(int nt, int kpt) { return (size_t)nt * kpt * 5 + (size_t)kListCap * 8; }
 
-static int topk_threads() {
-    static int nt = 0;
-    if (!nt) {
-        const char* env = getenv("KVD_TOPK_THREADS");   // experiments only: 256, 512 or 1024
-        nt = env ? atoi(env) : 1024;
-        if (nt != 256 && nt != 512) nt = 1024;
-    }
-    return nt;
+size_t select_static_smem() { return sizeof(TopkShared) + sizeof(ResolveShared) + sizeof(float) * kHeadDim; }
+
+template <bool RESOLVE>
+static cudaError_t launch_select_any(kvd_cache* c, const StepParams& p, const uint16_t* q, int32_t* out_ids,
+                                     float* out_scores, const FuseArgs& fa, cudaStream_t s) {
+    int nt, cl, kpt, v;
+    select_geometry(c->nb_pad, p.B * p.Hkv, c->resident, &nt, &cl, &kpt, &v);
+    return nt == 512 ? launch_select_nt<512, RESOLVE>(c, p, q, cl, kpt, v, out_ids, out_scores, fa, s)
+                     : launch_select_nt<1024, RESOLVE>(c, p, q, cl, kpt, v, out_ids, out_scores, fa, s);
 }
 
 cudaError_t launch_select(kvd_cache* c, const StepParams& p, const uint16_t* q, int32_t* out_ids, float* out_scores,
                           cudaStream_t s) {
-    cudaError_t e = launch_score_cfg(c, p, q, s);
-    if (e != cudaSuccess || p.k == 0) return e != cudaSuccess ? e : cudaGetLastError();
     const FuseArgs fa{};
-    const int nt = topk_threads();
-    e = nt == 256 ? launch_topk_nt<256, false>(c, p, out_ids, out_scores, fa, s)
-      : nt == 512 ? launch_topk_nt<512, false>(c, p, out_ids, out_scores, fa, s)
-                  : launch_topk_nt<1024, false>(c, p, out_ids, out_scores, fa, s);
-    if (e != cudaSuccess) return e;
-    return cudaGetLastError();
+    cudaError_t e = launch_select_any<false>(c, p, q, out_ids, out_scores, fa, s);
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
-// kvd_select_resolve_fetch: score_kernel, then the fused top-k + resolve + fetch kernel.
+// kvd_select_resolve_fetch: one kernel scores, selects, resolves and copies the misses.
 cudaError_t launch_select_resolve(kvd_cache* c, const StepParams& p, const uint16_t* q, int32_t* out_ids,
                                   float* out_scores, int32_t* out_attn, cudaStream_t s) {
-    cudaError_t e = launch_score_cfg(c, p, q, s);
-    if (e != cudaSuccess) return e;
-    if (p.k == 0) return launch_resolve(c, p, out_ids, out_attn, s);   // nothing to select
     FuseArgs fa;
     fa.rb = resolve_bufs(c);
     fa.out_attn = out_attn;
-    static int inner = -1;                        // misses copied inside the fused kernel (default)
-    if (inner < 0) {
-        const char* env = getenv("KVD_FUSED_GATHER");   // experiments only: 0 = separate gather kernel
-        inner = env && atoi(env) == 0 ? 0 : 1;
-    }
-    fa.host_store = (c->resident || !inner) ? nullptr : c->host_store;
+    fa.host_store = c->resident ? nullptr : c->host_store;
     fa.slots = c->slots;
-    const int nt = topk_threads();
-    e = nt == 256 ? launch_topk_nt<256, true>(c, p, out_ids, out_scores, fa, s)
-      : nt == 512 ? launch_topk_nt<512, true>(c, p, out_ids, out_scores, fa, s)
-                  : launch_topk_nt<1024, true>(c, p, out_ids, out_scores, fa, s);
-    if (e != cudaSuccess) return e;
-    if (!c->resident && !inner) e = launch_gather(c, p, s);
-    if (e != cudaSuccess) return e;
-    return cudaGetLastError();
+    cudaError_t e = launch_select_any<true>(c, p, q, out_ids, out_scores, fa, s);
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 }  // namespace kvd

@@ -1,10 +1,12 @@
 // kvd_abi.cu — the C ABI of libkvd.so (include/kvd.h): configuration and
 // allocation, synchronous argument validation, step-call dispatch to the
 // kernels, introspection.  No exception crosses this boundary.
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -18,6 +20,9 @@ using namespace kvd;
 namespace {
 
 thread_local std::string g_err;
+#ifdef KVD_EXPERIMENTS
+unsigned long long* g_exp_trace = nullptr;   // [kExpUnits][kExpPhases] phase stamps (tuning builds)
+#endif
 
 kvd_status fail(kvd_status st, const char* fmt, ...) {
     char buf[512];
@@ -73,18 +78,29 @@ kvd_status check_config(const kvd_config* cfg, Geometry* g) {
     g->resident = g->C >= g->nb_max;
     g->kmax = cfg->max_select;
     if (g->kmax > g->nb_max) return fail(KVD_EINVAL, "max_select > blocks per request");
-    if (resolve_smem_bytes(g->resident ? 0 : g->C, g->kmax, g->nb_pad) > kMaxSmemBytes)
-        return fail(KVD_EINVAL, "slots_per_segment=%lld too large for on-chip victim selection (host-backed cache)",
-                    (long long)g->C);
+    if (g->nb_pad > kMaxSelectBlocks) return fail(KVD_EINVAL, "context too long: > %d blocks", kMaxSelectBlocks);
+    {
+        // on-chip working sets (dynamic + static shared memory of the step kernels, kvd.h)
+        int nt, cl, kpt, v;
+        select_geometry(g->nb_pad, 1 << 30, g->resident, &nt, &cl, &kpt, &v);   // fewest CTAs: most keys each
+        const size_t sel = select_smem_bytes(nt, kpt);
+        const size_t res = resolve_smem_bytes(g->resident ? 0 : g->C, g->kmax, g->nb_pad);
+        if (std::max(sel, res) + select_static_smem() > kMaxSmemBytes ||
+            res + resolve_static_smem() > kMaxSmemBytes)
+            return fail(KVD_EINVAL, "slots_per_segment=%lld too large for on-chip victim selection (host-backed cache)",
+                        (long long)g->C);
+    }
     g->pmax = (cfg->sink_tokens + P - 1) / P + (cfg->local_tokens > 0 ? (cfg->local_tokens + P - 1) / P + 1 : 0);
     g->A = (cfg->host_layer_alias <= 0 || cfg->host_layer_alias > g->L) ? g->L : cfg->host_layer_alias;
     g->rec_bytes = 2ll * P * kRowBytes;
     if (g->pmax > 256) return fail(KVD_EINVAL, "sink/local tokens pin %d blocks (> 256)", g->pmax);
-    const int64_t wmax = g->kmax + g->pmax;
-    (void)wmax;
+    // a host-backed cache keeps every pinned block of a request in its own slot (R14): slots
+    // 0 .. pinned-1 must exist for the longest request (kvd_load_prefix places them there)
+    if (!g->resident && g->C < g->pmax)
+        return fail(KVD_EINVAL, "slots_per_segment=%lld < %d pinned blocks (sink/local tokens)", (long long)g->C,
+                    g->pmax);
     g->max_splits = kMaxPieces;
     if ((int64_t)g->Hkv * g->nb_max * 4 > kSlotOfBytes) return fail(KVD_EINVAL, "context too long for setup scratch");
-    if (g->nb_pad > kMaxSelectBlocks) return fail(KVD_EINVAL, "context too long: > %d blocks", kMaxSelectBlocks);
     return KVD_OK;
 }
 
@@ -108,7 +124,7 @@ Sizes sizes_of(const Geometry& g) {
     s.miss = rsegs * (size_t)(g.kmax > 0 ? g.kmax : 1) * 2 * 4 + rsegs * 4;
     s.part_o = rsegs * g.max_splits * 8 * kHeadDim * 4;
     s.part_ml = rsegs * g.max_splits * 8 * 2 * 4;
-    s.small = rsegs * 8 + 64 + 4 + (size_t)g.R * 4 + g.rec_bytes;
+    s.small = rsegs * 12 + 64 + 4 + (size_t)g.R * 4 + g.rec_bytes;
     s.host = g.resident ? 0 : (size_t)g.A * g.R * g.Hkv * g.nb_max * g.rec_bytes;
     return s;
 }
@@ -163,8 +179,20 @@ kvd_status check_step(kvd_cache* c, int32_t layer, const int32_t* req_ids, int32
     p->step_dev = c->step_dev;
     p->host_layer = layer % c->A;
     p->rec_bytes = (int32_t)c->rec_bytes;
-    p->nsplit = (int)(((p->W + c->E - 1) / c->E + kSplitTiles - 1) / kSplitTiles);
     p->scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)KVD_HEAD_DIM));
+    p->kt_slots = c->kt_on ? c->kt_slots : nullptr;
+    p->kt_acc = c->kt_acc;
+    p->kt_base = (layer * c->R + p->req[0]) * kKtKinds;
+    p->exp_trace = nullptr;
+#ifdef KVD_EXPERIMENTS
+    if (getenv("KVD_EXP_TRACE")) {
+        if (!g_exp_trace) {
+            cudaMalloc(&g_exp_trace, (size_t)kExpUnits * kExpPhases * 8);
+            cudaMemset(g_exp_trace, 0, (size_t)kExpUnits * kExpPhases * 8);
+        }
+        p->exp_trace = g_exp_trace;
+    }
+#endif
     return KVD_OK;
 }
 
@@ -183,7 +211,11 @@ extern "C" {
 
 const char* kvd_last_error(void) { return g_err.c_str(); }
 
-const char* kvd_version(void) { return "kvd 0.2 sm_100a"; }
+#ifdef KVD_EXPERIMENTS
+const char* kvd_version(void) { return "kvd 0.3 sm_100a (experiments build)"; }
+#else
+const char* kvd_version(void) { return "kvd 0.3 sm_100a"; }
+#endif
 
 uint64_t kvd_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
@@ -211,6 +243,10 @@ kvd_status kvd_create_cache(const kvd_config* cfg, kvd_cache** out) {
     c->pmax = g.pmax; c->A = g.A; c->E = g.E; c->nmax = g.nmax; c->nb_max = g.nb_max; c->nb_pad = g.nb_pad;
     c->C = g.C; c->resident = g.resident; c->rec_bytes = g.rec_bytes; c->max_splits = g.max_splits;
     c->ntok.assign((size_t)g.R, 0);
+    {
+        int lo = 0, hi = 0;
+        if (cudaDeviceGetStreamPriorityRange(&lo, &hi) == cudaSuccess) c->prio_hi = hi;
+    }
     const Sizes s = sizes_of(g);
     const size_t rsegs = (size_t)g.R * g.Hkv;
     cudaError_t e = cudaSuccess;
@@ -260,7 +296,7 @@ void kvd_destroy_cache(kvd_cache* c) {
     cudaSetDevice(c->cfg.device);
     cudaDeviceSynchronize();
     void* dev[] = {c->slots, c->summ, c->scores, c->table, c->slot_block, c->last_use, c->phase,
-                   c->use_count, c->miss, c->miss_count, c->part_o, c->part_ml, c->stats,
+                   c->use_count, c->miss, c->miss_count, c->part_o, c->part_ml, c->kt_slots, c->kt_acc, c->stats,
                    c->err, c->ntok_dev, c->zero_rec, c->stage_kv, c->stage_rec};
     for (void* p : dev)
         if (p) cudaFree(p);
@@ -435,6 +471,63 @@ kvd_status kvd_read_scores(kvd_cache* c, int32_t layer, int32_t req, int32_t hea
     const int64_t seg = ((int64_t)layer * c->R + req) * c->Hkv + head;
     const int64_t nb = (c->ntok[(size_t)req] + c->P - 1) / c->P;
     KVD_CUDA(cudaMemcpy(out, c->scores + seg * c->nb_pad, (size_t)nb * 4, cudaMemcpyDeviceToHost));
+    return KVD_OK;
+}
+
+#ifdef KVD_EXPERIMENTS
+// experiment builds only: copy (and clear) the phase stamps [units][8]
+kvd_status kvd_exp_read_trace(uint64_t* out, int32_t units) {
+    if (!out || units < 1 || units > kExpUnits) return fail(KVD_EINVAL, "bad trace arguments");
+    if (!g_exp_trace) return fail(KVD_ESTATE, "no trace");
+    KVD_CUDA(cudaDeviceSynchronize());
+    KVD_CUDA(cudaMemcpy(out, g_exp_trace, (size_t)units * kExpPhases * 8, cudaMemcpyDeviceToHost));
+    KVD_CUDA(cudaMemset(g_exp_trace, 0, (size_t)kExpUnits * kExpPhases * 8));
+    return KVD_OK;
+}
+#endif
+
+kvd_status kvd_probe_zero_copy(const void* host, void* dev, size_t bytes, int32_t ctas, kvd_stream stream) {
+    if (!host || !dev || bytes % 16 || ctas < 1) return fail(KVD_EINVAL, "bad probe arguments");
+    cudaPointerAttributes a{};
+    KVD_CUDA(cudaPointerGetAttributes(&a, host));
+    if (a.type != cudaMemoryTypeHost) return fail(KVD_EINVAL, "probe source is not pinned host memory");
+    KVD_CUDA(launch_zero_copy(a.devicePointer ? a.devicePointer : host, dev, bytes, ctas,
+                              reinterpret_cast<cudaStream_t>(stream)));
+    return KVD_OK;
+}
+
+kvd_status kvd_enable_kernel_timer(kvd_cache* c, int32_t enable) {
+    if (!c) return fail(KVD_EINVAL, "cache is NULL");
+    KVD_CUDA(cudaSetDevice(c->cfg.device));
+    KVD_CUDA(cudaDeviceSynchronize());
+    const size_t nslots = (size_t)c->L * c->R * kKtKinds;
+    if (enable && !c->kt_slots) {
+        KVD_CUDA(dalloc(&c->kt_slots, nslots * 16));
+        KVD_CUDA(dalloc(&c->kt_acc, (size_t)kKtKinds * 16));
+    }
+    if (c->kt_slots) {
+        std::vector<unsigned long long> init(nslots * 2);
+        for (size_t i = 0; i < nslots; ++i) {
+            init[2 * i] = ~0ull;
+            init[2 * i + 1] = 0;
+        }
+        KVD_CUDA(cudaMemcpy(c->kt_slots, init.data(), nslots * 16, cudaMemcpyHostToDevice));
+        KVD_CUDA(cudaMemset(c->kt_acc, 0, (size_t)kKtKinds * 16));
+    }
+    c->kt_on = enable != 0;
+    return KVD_OK;
+}
+
+kvd_status kvd_read_kernel_timer(kvd_cache* c, uint64_t* ns, uint64_t* launches) {
+    if (!c || !ns || !launches) return fail(KVD_EINVAL, "NULL argument");
+    if (!c->kt_acc) return fail(KVD_ESTATE, "kernel timer was never enabled");
+    KVD_CUDA(cudaDeviceSynchronize());
+    unsigned long long v[2 * kKtKinds];
+    KVD_CUDA(cudaMemcpy(v, c->kt_acc, sizeof v, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < kKtKinds; ++i) {
+        ns[i] = v[2 * i];
+        launches[i] = v[2 * i + 1];
+    }
     return KVD_OK;
 }
 

@@ -274,23 +274,25 @@ __device__ inline int resolve_main(const StepParams& p, const ResolveBufs& rb, i
 
 
 // (a4) inside a segment's CTA: all threads copy the nm missed 8 KiB records host -> slot.
-// The (record, 16-byte chunk) space is flattened over the CTA and every thread keeps up to 8
-// zero-copy loads in flight, so the whole miss set is requested in one host-link round trip.
+// The (record, 16-byte chunk) space is flattened and cut into nparts equal slices (one per CTA
+// of the segment's cluster); every thread keeps up to 8 zero-copy loads in flight, so the whole
+// slice is requested in one host-link round trip.
 __device__ __forceinline__ void gather_segment(const StepParams& p, int bi, int h, const int32_t* M, const int32_t* dest,
                                                int nm, const uint8_t* __restrict__ host_store,
-                                               uint8_t* __restrict__ slots) {
+                                               uint8_t* __restrict__ slots, int part, int nparts) {
     const int r = p.req[bi];
     const int cpr = p.rec_bytes / 16;                       // 16-byte chunks per record (power of two)
     const int lcpr = __ffs(cpr) - 1;
     const int total = nm << lcpr;
+    const int xa = (int)((int64_t)part * total / nparts), xb = (int)((int64_t)(part + 1) * total / nparts);
     const uint8_t* hbase = host_store + (((int64_t)p.host_layer * p.R + r) * p.Hkv + h) * p.nb_max * (int64_t)p.rec_bytes;
     uint8_t* sbase = slots + (((int64_t)p.layer * p.R + r) * p.Hkv + h) * p.C * (int64_t)p.rec_bytes;
-    for (int x0 = threadIdx.x; x0 < total; x0 += 8 * blockDim.x) {
+    for (int x0 = xa + threadIdx.x; x0 < xb; x0 += 8 * blockDim.x) {
         int4 v[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             const int x = x0 + u * blockDim.x;
-            if (x < total) {
+            if (x < xb) {
                 const int i = x >> lcpr, c = x & (cpr - 1);
                 v[u] = ld_host16(reinterpret_cast<const int4*>(hbase + (int64_t)M[i] * p.rec_bytes) + c);
             }
@@ -298,7 +300,7 @@ __device__ __forceinline__ void gather_segment(const StepParams& p, int bi, int 
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             const int x = x0 + u * blockDim.x;
-            if (x < total) {
+            if (x < xb) {
                 const int i = x >> lcpr, c = x & (cpr - 1);
                 reinterpret_cast<int4*>(sbase + (int64_t)dest[i] * p.rec_bytes)[c] = v[u];
             }

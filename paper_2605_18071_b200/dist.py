@@ -51,6 +51,12 @@ def rank_heads(parts):
     return [req for req, _, _ in parts], h0, h1
 
 
+def whole_requests(all_parts, Hkv):
+    """True when every rank owns whole requests (all Hkv heads of each): no rank holds a partial
+    head range, so no output needs gathering (request sharding)."""
+    return all(h0 == 0 and h1 == Hkv for parts in all_parts for _, h0, h1 in parts)
+
+
 def assemble_heads(gathered, all_parts, B, Hkv, G):
     """Per-rank outputs [world][L][B_r][Hq_r][d] (all_gather_into_tensor of each
     rank's fp32 attention outputs) -> the global [L][B][Hq][d] tensor."""

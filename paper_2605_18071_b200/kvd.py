@@ -56,7 +56,8 @@ EXPORTS = ["kvd_required_bytes", "kvd_create_cache", "kvd_destroy_cache", "kvd_g
            "kvd_read_segment", "kvd_read_slot", "kvd_read_host_record", "kvd_read_summaries",
            "kvd_read_scores", "kvd_get_stats", "kvd_reset_stats", "kvd_check", "kvd_last_error",
            "kvd_version", "kvd_set_device_step", "kvd_launch_count",
-           "kvd_select_resolve_fetch"]
+           "kvd_select_resolve_fetch", "kvd_enable_kernel_timer", "kvd_read_kernel_timer",
+           "kvd_probe_zero_copy"]
 
 
 def lib():
@@ -90,6 +91,9 @@ def lib():
             "kvd_version": ([], ctypes.c_char_p),
             "kvd_launch_count": ([], ctypes.c_uint64),
             "kvd_select_resolve_fetch": ([p, i32, p, p, i32, i32, u32, p, p, p, p], i32),
+            "kvd_enable_kernel_timer": ([p, i32], i32),
+            "kvd_read_kernel_timer": ([p, p, p], i32),
+            "kvd_probe_zero_copy": ([p, p, ctypes.c_size_t, i32, p], i32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -243,6 +247,24 @@ class KVCache:
 
     def check(self):
         _check(lib().kvd_check(self.h))
+
+    KERNEL_KINDS = ("select", "resolve", "gather", "attn")
+
+    def enable_kernel_timer(self, enable=True):
+        """Device-side launch timing of every step kernel (kvd.h); zeroes the accumulators."""
+        _check(lib().kvd_enable_kernel_timer(self.h, 1 if enable else 0))
+
+    def read_kernel_timer(self):
+        """{kind: (summed launch ns, launches)} since the last enable."""
+        ns = np.zeros(4, np.uint64)
+        n = np.zeros(4, np.uint64)
+        _check(lib().kvd_read_kernel_timer(self.h, ptr(ns), ptr(n)))
+        return {k: (int(ns[i]), int(n[i])) for i, k in enumerate(self.KERNEL_KINDS)}
+
+
+def probe_zero_copy(host, dev, nbytes, ctas, stream=None):
+    """Zero-copy host-link probe (kvd_probe_zero_copy): pinned host -> device, gather pattern."""
+    _check(lib().kvd_probe_zero_copy(ptr(host), ptr(dev), nbytes, ctas, _stream(stream)))
 
 
 def record_to_kv(rec, P, d=128):

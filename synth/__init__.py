@@ -57,6 +57,7 @@ def lib():
         L.synth_request_kv.argtypes = [u64, i64, i64, i32, i64, i32, p, p]
         L.synth_queries.argtypes = [u64, i64, i64, i64, i32, i32, i64, i64, ctypes.c_double, p]
         L.synth_batch_queries.argtypes = [u64, i64, p, i32, i32, i32, i32, i64, i64, ctypes.c_double, p]
+        L.synth_batch_queries_x.argtypes = [u64, i64, i64, p, i32, i32, i32, i32, i64, i64, ctypes.c_double, p]
         L.synth_segment_plan.argtypes = [u64, i64, i64, i64, i64, i32, p, p, p]
         for f in (L.synth_segment_kv, L.synth_request_kv, L.synth_queries, L.synth_batch_queries,
                   L.synth_segment_plan):
@@ -117,12 +118,15 @@ def queries(seed, layer, req, head, G, d=128, t0=0, nsteps=1, alpha=0.9):
     return out
 
 
-def batch_queries(seed, layer, reqs, Hkv, G, d=128, t0=0, nsteps=1, alpha=0.9):
-    """Queries of a batch for one layer: [nsteps][B][Hkv*G][d] uint16."""
+def batch_queries(seed, layer, reqs, Hkv, G, d=128, t0=0, nsteps=1, alpha=0.9, stream_layer=None):
+    """Queries of a batch for one layer: [nsteps][B][Hkv*G][d] uint16.  The queries follow
+    the key topics of `layer`; `stream_layer` (default `layer`) keys their random streams, so
+    a layer whose keys alias another's (host-layer aliasing) still gets its own queries."""
     reqs = np.ascontiguousarray(np.asarray(reqs, np.int32))
     B = len(reqs)
     out = np.empty((nsteps, B, Hkv * G, d), np.uint16)
-    lib().synth_batch_queries(seed, layer, _ptr(reqs), B, Hkv, G, d, t0, nsteps, float(alpha), _ptr(out))
+    ls = layer if stream_layer is None else stream_layer
+    lib().synth_batch_queries_x(seed, layer, ls, _ptr(reqs), B, Hkv, G, d, t0, nsteps, float(alpha), _ptr(out))
     return out
 
 

@@ -131,14 +131,17 @@ static void normalise(double* x, int32_t d) {
 }
 
 /* Decode queries of one segment's G query heads for steps t0 .. t0+nsteps-1:
- * out [nsteps][G][d] bf16.  The AR(1) state is replayed from t = 0. */
-void synth_queries(uint64_t seed, int64_t l, int64_t r, int64_t h, int32_t G, int32_t d,
-                   int64_t t0, int64_t nsteps, double alpha, uint16_t* out) {
+ * out [nsteps][G][d] bf16.  The AR(1) state is replayed from t = 0.  The topic
+ * centres are those of the keys of layer lk; the random streams (topic walk,
+ * base and head noise) are those of layer ls (ls == lk: synth_queries). */
+static void queries_impl(uint64_t seed, int64_t lk, int64_t ls, int64_t r, int64_t h, int32_t G, int32_t d,
+                         int64_t t0, int64_t nsteps, double alpha, uint16_t* out) {
+    const int64_t l = ls;
     float* mu = (float*)malloc(sizeof(float) * SYN_TOPICS * (size_t)d);
     double* u = (double*)malloc(sizeof(double) * (size_t)d);
     double* x = (double*)malloc(sizeof(double) * (size_t)d);
     double* e = (double*)malloc(sizeof(double) * (size_t)d);
-    topic_centres(seed, l, r, h, d, mu);
+    topic_centres(seed, lk, r, h, d, mu);
     uint64_t kt = seg_key(seed, l, r, h, ST_QTOPIC), kb = seg_key(seed, l, r, h, ST_QBASE),
              kh = seg_key(seed, l, r, h, ST_QHEAD);
     int32_t tau = (int32_t)(ctr_u64(kt, 0) % SYN_TOPICS);
@@ -166,20 +169,31 @@ void synth_queries(uint64_t seed, int64_t l, int64_t r, int64_t h, int32_t G, in
     free(mu); free(u); free(x); free(e);
 }
 
+void synth_queries(uint64_t seed, int64_t l, int64_t r, int64_t h, int32_t G, int32_t d,
+                   int64_t t0, int64_t nsteps, double alpha, uint16_t* out) {
+    queries_impl(seed, l, l, r, h, G, d, t0, nsteps, alpha, out);
+}
+
 /* Queries of a whole batch for one layer and a range of steps:
- * out [nsteps][B][Hq][d] with Hq = Hkv*G; request ids req[B]. */
-void synth_batch_queries(uint64_t seed, int64_t l, const int32_t* req, int32_t B, int32_t Hkv,
-                         int32_t G, int32_t d, int64_t t0, int64_t nsteps, double alpha,
-                         uint16_t* out) {
+ * out [nsteps][B][Hq][d] with Hq = Hkv*G; request ids req[B].  Key topics of
+ * layer lk, random streams of layer ls (synth_batch_queries: ls == lk). */
+void synth_batch_queries_x(uint64_t seed, int64_t lk, int64_t ls, const int32_t* req, int32_t B, int32_t Hkv,
+                           int32_t G, int32_t d, int64_t t0, int64_t nsteps, double alpha, uint16_t* out) {
     int64_t Hq = (int64_t)Hkv * G;
     #pragma omp parallel for schedule(dynamic) collapse(2)
     for (int32_t b = 0; b < B; ++b)
         for (int32_t h = 0; h < Hkv; ++h) {
             uint16_t* tmp = (uint16_t*)malloc(sizeof(uint16_t) * (size_t)(nsteps * G * d));
-            synth_queries(seed, l, req[b], h, G, d, t0, nsteps, alpha, tmp);
+            queries_impl(seed, lk, ls, req[b], h, G, d, t0, nsteps, alpha, tmp);
             for (int64_t t = 0; t < nsteps; ++t)
                 memcpy(out + ((t * B + b) * Hq + (int64_t)h * G) * d, tmp + t * G * d,
                        sizeof(uint16_t) * (size_t)G * (size_t)d);
             free(tmp);
         }
+}
+
+void synth_batch_queries(uint64_t seed, int64_t l, const int32_t* req, int32_t B, int32_t Hkv,
+                         int32_t G, int32_t d, int64_t t0, int64_t nsteps, double alpha,
+                         uint16_t* out) {
+    synth_batch_queries_x(seed, l, l, req, B, Hkv, G, d, t0, nsteps, alpha, out);
 }

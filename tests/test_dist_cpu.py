@@ -6,7 +6,7 @@ import socket
 import pytest
 import torch.multiprocessing as mp
 
-from paper_2605_18071_b200.dist import rank_requests, unit_partition
+from paper_2605_18071_b200.dist import rank_requests, unit_partition, whole_requests
 
 
 def test_rank_requests_disjoint_cover():
@@ -29,6 +29,30 @@ def test_unit_partition_c4_heads_sharded():
     # BASELINE c4: 4 requests x 4 KV heads over 8 GPUs -> 2 heads of one request per rank (R21)
     parts = unit_partition(4, 4, 8)
     assert parts[0] == [(0, 0, 2)] and parts[1] == [(0, 2, 4)] and parts[7] == [(3, 2, 4)]
+
+
+@pytest.mark.parametrize("B,Hkv,world,whole", [(64, 8, 1, True), (64, 8, 2, True), (64, 8, 4, True),
+                                               (64, 8, 8, True), (4, 4, 8, False), (4, 4, 2, True),
+                                               (16, 8, 32, False)])
+def test_whole_requests_decides_the_gather(B, Hkv, world, whole):
+    # c5 ("batch 64 partitioned at 1/2/4/8"): whole requests per rank -> no collective at all;
+    # c4 at 8 GPUs: two heads of one request per rank -> the outputs are all-gathered
+    assert whole_requests(unit_partition(B, Hkv, world), Hkv) == whole
+
+
+def test_bench_self_launch_command(monkeypatch):
+    # `bench.py --gpus N` without WORLD_SIZE launches N ranks through torch.distributed.run
+    import sys
+    import bench
+    seen = {}
+    monkeypatch.setattr(bench.subprocess, "call", lambda cmd: seen.setdefault("cmd", cmd) and 0)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4", "--steps", "3"])
+    monkeypatch.delenv("WORLD_SIZE", raising=False)
+    args = bench.parse(["--gpus", "4", "--steps", "3"])
+    bench.self_launch(args)
+    cmd = seen["cmd"]
+    assert cmd[1:3] == ["-m", "torch.distributed.run"] and "--nproc-per-node=4" in cmd
+    assert "127.0.0.1" in cmd and cmd[-4:] == ["--gpus", "4", "--steps", "3"]
 
 
 def _free_port():

@@ -200,3 +200,45 @@ def test_max_batch_many_segments(fused):
     workers, so most workers finalise whole segments in place; host-backed with evictions."""
     c = Case(L=1, B=256, Hq=32, Hkv=8, n=600, P=16, k=8, C=20, policy="lru", seed=42, fused=fused)
     c.run(steps=2, check_state=True)
+
+
+# ---- a cluster whose CTAs disagree on whether their threshold-bin list fits (ADVICE r1 high):
+# one outlier score stretches the linear first digit so that almost every candidate lands in the
+# threshold bin; the 4-CTA cluster's full CTAs overflow the 4096-entry list while its short last
+# CTA does not.  Keys are (nearly) distinct, so the LIST / WHOLE modes run, not EQUAL.
+@pytest.mark.parametrize("fused", [False, True])
+def test_topk_cluster_mixed_list_overflow(monkeypatch, fused):
+    n, P = 40000, 1
+
+    def fake_request_kv(seed, layer, req, Hkv, n_, d=128, out_k=None, out_v=None):
+        rng = np.random.default_rng(1000 + 10 * req + layer)
+        K = np.zeros((Hkv, n_, d), np.float32)
+        K[:, :, 0] = rng.standard_normal((Hkv, n_)).astype(np.float32)
+        K[:, :, 1] = rng.standard_normal((Hkv, n_)).astype(np.float32)
+        K[:, 5000, 0] = 3.0e4                                      # the outlier (CTA 0)
+        V = rng.standard_normal((Hkv, n_, d)).astype(np.float32)
+        return _bf16(K), _bf16(V)
+    monkeypatch.setattr(synth, "request_kv", fake_request_kv)
+    c = Case(L=1, B=2, Hq=8, Hkv=2, n=n, P=P, k=96, C=None, policy="la", seed=23, ragged=True, fused=fused)
+
+    def queries(l, t):
+        q = np.zeros((c.B, c.Hq, 128), np.float32)
+        q[:, :, 0] = 1.0
+        q[:, :, 1] = 0.25 * (t + 1)                                # dim 1 makes the keys distinct
+        return _bf16(q)
+    c.queries = queries
+    c.run(steps=2)
+
+
+# ---- the split-K plan is a function of the segment (its k) only: a request attended alone and
+# the same request inside a 16-request call give bit-identical outputs (SURVEY §8.6)
+@pytest.mark.parametrize("fused", [False, True])
+def test_attention_bitwise_independent_of_batch(fused):
+    alone = Case(L=1, B=1, Hq=8, Hkv=2, n=8192, P=16, k=128, C=None, seed=24, reqs=[5], R=16, fused=fused)
+    batch = Case(L=1, B=16, Hq=8, Hkv=2, n=8192, P=16, k=128, C=None, seed=24, fused=fused)
+    for t in range(2):
+        ga = alone.gpu_layer(0, alone.queries(0, t), t + 1)
+        gb = batch.gpu_layer(0, batch.queries(0, t), t + 1)
+        assert np.array_equal(ga["ids"][0], gb["ids"][5])
+        assert np.array_equal(ga["out"][0].view(np.uint32), gb["out"][5].view(np.uint32))
+        assert np.array_equal(ga["lse"][0].view(np.uint32), gb["lse"][5].view(np.uint32))

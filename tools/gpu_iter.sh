@@ -1,18 +1,11 @@
 #!/bin/bash
-# quick iteration: GPU parity + bench c2/c3/c4 lines.  usage: tools/gpu_iter.sh <tag> [extra bench args]
-tag=${1:-it}; shift
-mkdir -p gpurun_out
-timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/${tag}_pytest.log 2>&1; echo "pytest rc $?"; tail -15 gpurun_out/${tag}_pytest.log | grep -v "^$" | tail -8
-for c in c2 c3 c4; do
-  timeout 600 python bench.py --config $c --steps 20 --warmup 5 --no-cpu-baseline "$@" > gpurun_out/${tag}_bench_$c.json 2> gpurun_out/${tag}_bench_$c.err; echo "$c rc $?"
-  python - gpurun_out/${tag}_bench_$c.json <<'PY'
-import json,sys
-try:
-    d=json.loads(open(sys.argv[1]).read().strip().splitlines()[-1])
-    k=d["kernels"]
-    print(d["config"]["workload"], "tok/s %.0f ms/step %.3f e2e %.0f hit %.3f launches %s" % (d["value"], d["ms_per_step"], (d["e2e"] or {}).get("value",0), d["hit_rate"], d["gpu_launches"]),
-      "| sel %.1fus %.0fGB/s | res+fetch %.1fus | attn %.1fus %.0fGB/s" % (k["select"]["ms_per_launch"]*1e3, k["select"]["gbs"], k["resolve_fetch"]["ms_per_launch"]*1e3, k["attn"]["ms_per_launch"]*1e3, k["attn"]["gbs"]), "clk", d["clocks"]["sm_mhz"], d["clocks"]["reasons"])
-except Exception as e: print("parse fail", e)
-PY
-  tail -3 gpurun_out/${tag}_bench_$c.err
+# iteration: GPU parity, bench lines, then an experiments build with phase traces.  usage: tools/gpu_iter.sh <tag> [cfgs]
+tag=${1:-it}; shift; cfgs=${@:-c2 c3 c4}; mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/${tag}_pytest_gpu.log 2>&1; echo "pytest rc $?"; tail -3 gpurun_out/${tag}_pytest_gpu.log
+for c in $cfgs; do
+  timeout 600 python bench.py --config $c --no-cpu-baseline --steps 10 --warmup 3 > gpurun_out/${tag}_$c.json 2>gpurun_out/${tag}_$c.err; echo -n "$c: "; python tools/line_summary.py gpurun_out/${tag}_$c.json
 done
+KVD_BUILD_EXPERIMENTS=1 python -c "from paper_2605_18071_b200 import build as b; b.build(force=True)" || exit 1
+python tools/exp_trace.py --config c2 --chain-size 1 --reps 2 2>&1 | tail -13
+python tools/exp_trace.py --config c3 --chain-size 1 --reps 1 2>&1 | tail -13
+python tools/exp_trace.py --config c4 --chain-size 1 --reps 1 2>&1 | tail -13

@@ -32,7 +32,8 @@ def hot(rep, kernel, n=20):
     txt = ncu(rep, "--page", "source", "--csv", "-k", kernel, "--print-source", "sass")
     rows = list(csv.reader(io.StringIO(txt)))
     hi = next(i for i, r in enumerate(rows) if r and r[0] == "Address")
-    h, data = rows[hi], [r for r in rows[hi + 1:] if len(r) == len(rows[hi])]
+    h = rows[hi]
+    data = [r for r in rows[hi + 1:] if len(r) == len(h) and r[0] != "Address"]
     si, src = h.index("Warp Stall Sampling (All Samples)"), h.index("Source")
     tot = sum(float(r[si] or 0) for r in data) or 1
     print(f"-- hottest SASS of {kernel} ({len(data)} instructions)")
