@@ -9,7 +9,6 @@
 //   table      [L][R][Hkv][nb_pad] int32 block -> slot | -1
 //   slot_block/last_use/phase/use_count [L][R][Hkv][C]
 //   miss       [R][Hkv][kmax] int2 (block, slot) + miss_count [R][Hkv]
-//   partials   [R][Hkv][kMaxPieces][8][128] fp32 + (m, l) [R][Hkv][kMaxPieces][8][2]
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -72,8 +71,6 @@ struct kvd_cache {
     uint32_t* use_count = nullptr;
     int32_t* miss = nullptr;
     int32_t* miss_count = nullptr;
-    float* part_o = nullptr;
-    float* part_ml = nullptr;
     unsigned long long* kt_slots = nullptr;  // kernel timer (bench instrumentation)
     unsigned long long* kt_acc = nullptr;
     bool kt_on = false;
@@ -110,15 +107,15 @@ cudaError_t launch_select_resolve(kvd_cache* c, const StepParams& p, const uint1
 cudaError_t launch_attention(kvd_cache* c, const StepParams& p, const uint16_t* q, const int32_t* attn, float* out,
                              float* out_lse, cudaStream_t s);
 
-// Split-K plan of one segment's attention: its TS tiles are cut into NP pieces of
-// kPieceTiles tiles or more (at most kMaxPieces), piece i = tiles [i*TS/NP, (i+1)*TS/NP).
-// A function of TS (i.e. of k) only -- not of how many segments share a launch or a GPU -- so
-// every output is bit-identical however the requests are batched, chained or sharded.
+// Split-K plan of one segment's attention: its TS tiles are cut into NP pieces, a multiple of
+// 4 (one thread-block cluster of NP/4 CTAs x 4 warps per segment, k_attn.cu) of about
+// kPieceTiles tiles, 4 <= NP <= kMaxPieces; piece j = tiles [j*TS/NP, (j+1)*TS/NP).  A function
+// of TS (i.e. of k) only -- not of how many segments share a launch or a GPU -- so every output
+// is bit-identical however the requests are batched, chained or sharded.
 __host__ __device__ inline int attn_pieces(int TS) {
-    const int pt0 = (TS + kMaxPieces - 1) / kMaxPieces;
-    const int pt = pt0 > kPieceTiles ? pt0 : kPieceTiles;
-    const int np = (TS + pt - 1) / pt;
-    return np > 0 ? np : 1;
+    int c = (TS + 4 * kPieceTiles - 1) / (4 * kPieceTiles);
+    c = c < 1 ? 1 : c > kMaxPieces / 4 ? kMaxPieces / 4 : c;
+    return 4 * c;
 }
 
 __host__ __device__ inline SegGeom seg_geom(int64_t n64, int P, int sink, int local) {

@@ -29,7 +29,7 @@ void select_geometry(int64_t nb_pad, int segs, bool resident, int* nt, int* cl, 
     static const int target = tune("KVD_SELECT_CTAS", kSelectCtaTarget),
                      min_span_res = tune("KVD_SELECT_MINSPAN", 1024),
                      min_span_host = tune("KVD_SELECT_MINSPAN_HOST", 8192),
-                     nt_small = tune("KVD_SELECT_NT_SMALL", 512);
+                     nt_small = tune("KVD_SELECT_NT_SMALL", 512), nt_large = tune("KVD_SELECT_NT_LARGE", 1024);
     // host-backed: rank 0 fetches the misses over the host link after the selection, holding its
     // SM; spans of up to 8192 blocks stay on one CTA (c3: 2799 vs 2397 tok/s with 8 CTAs/segment)
     const int min_span = resident ? min_span_res : min_span_host;
@@ -37,7 +37,7 @@ void select_geometry(int64_t nb_pad, int segs, bool resident, int* nt, int* cl, 
     while (c < 8 && (int64_t)c * 1024 * kMaxKpt < nb_pad) c <<= 1;
     while (c < 8 && (int64_t)segs * c < target && nb_pad / (2 * c) >= min_span) c <<= 1;
     const int64_t span = (nb_pad + c - 1) / c;
-    const int threads = span <= 2048 ? nt_small : 1024;
+    const int threads = span <= 2048 ? nt_small : nt_large;
     int64_t per = (span + threads - 1) / threads;
     const int vw = per >= 8 ? 8 : per >= 4 ? 4 : 2;
     per = (per + vw - 1) / vw * vw;

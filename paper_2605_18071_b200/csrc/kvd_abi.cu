@@ -105,10 +105,8 @@ kvd_status check_config(const kvd_config* cfg, Geometry* g) {
 }
 
 struct Sizes {
-    size_t slots, summ, scores, table, meta4, meta1, miss, part_o, part_ml, small, host;
-    size_t dev_total() const {
-        return slots + summ + scores + table + 3 * meta4 + meta1 + miss + part_o + part_ml + small;
-    }
+    size_t slots, summ, scores, table, meta4, meta1, miss, small, host;
+    size_t dev_total() const { return slots + summ + scores + table + 3 * meta4 + meta1 + miss + small; }
 };
 
 Sizes sizes_of(const Geometry& g) {
@@ -122,8 +120,6 @@ Sizes sizes_of(const Geometry& g) {
     s.meta4 = segs * g.C * 4;
     s.meta1 = segs * g.C;
     s.miss = rsegs * (size_t)(g.kmax > 0 ? g.kmax : 1) * 2 * 4 + rsegs * 4;
-    s.part_o = rsegs * g.max_splits * 8 * kHeadDim * 4;
-    s.part_ml = rsegs * g.max_splits * 8 * 2 * 4;
     s.small = rsegs * 12 + 64 + 4 + (size_t)g.R * 4 + g.rec_bytes;
     s.host = g.resident ? 0 : (size_t)g.A * g.R * g.Hkv * g.nb_max * g.rec_bytes;
     return s;
@@ -262,8 +258,6 @@ kvd_status kvd_create_cache(const kvd_config* cfg, kvd_cache** out) {
     ALLOC(phase, s.meta1);
     ALLOC(miss, rsegs * (size_t)(g.kmax > 0 ? g.kmax : 1) * 2 * 4);
     ALLOC(miss_count, rsegs * 4);
-    ALLOC(part_o, s.part_o);
-    ALLOC(part_ml, s.part_ml);
     ALLOC(stats, 64);
     ALLOC(err, 4);
     ALLOC(ntok_dev, (size_t)g.R * 4);
@@ -296,7 +290,7 @@ void kvd_destroy_cache(kvd_cache* c) {
     cudaSetDevice(c->cfg.device);
     cudaDeviceSynchronize();
     void* dev[] = {c->slots, c->summ, c->scores, c->table, c->slot_block, c->last_use, c->phase,
-                   c->use_count, c->miss, c->miss_count, c->part_o, c->part_ml, c->kt_slots, c->kt_acc, c->stats,
+                   c->use_count, c->miss, c->miss_count, c->kt_slots, c->kt_acc, c->stats,
                    c->err, c->ntok_dev, c->zero_rec, c->stage_kv, c->stage_rec};
     for (void* p : dev)
         if (p) cudaFree(p);

@@ -76,7 +76,7 @@ def main():
              ["entry", "after_wait", "scored", "first_digit", "compacted", "radix_done", "emitted", "end"])
         R.cache.sparse_decode(0, q, R.reqs[:nb], R.attn[0, :nb], R.W, R.out[0, :nb], R.lse[0, :nb], stream=s)
         s.synchronize()
-        show(f"[{rep}] attn_kernel", read(lib, 16384), ["entry", "after_wait", "tile0", "stream_end", "flushed"])
+        show(f"[{rep}] attn_kernel", read(lib, 16384), ["entry", "after_wait", "tile0", "stream_end", "merged"])
 
 
 if __name__ == "__main__":
