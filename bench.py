@@ -86,6 +86,7 @@ def parse(argv=None):
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-isolated", action="store_true", help="skip the whole-batch per-kernel roofline pass")
     ap.add_argument("--no-graph", action="store_true", help="launch layer by layer instead of graph replay")
     ap.add_argument("--chains", type=int, default=None,
                     help="micro-batch chains (SFC overlap): the batch is split into this many request groups, "
@@ -541,6 +542,36 @@ def run_gpu(args):
         ems = kdist.max_over_ranks(e0.elapsed_time(e1) / args.steps, dev)
         e2e = {"value": tokens_per_step / (ems * 1e-3), "unit": "tokens/s", "ms_per_step": ems,
                "h2d_bytes_per_step": int(R.q_cur.numel() * 2), "d2h_bytes_per_step": int(R.out.numel() * 4)}
+    # ---- per-kernel rooflines of whole-batch launches (chains = 1: every kernel serves the rank's
+    # whole batch and runs alone), device-timed with the kernel timer on the same step graph
+    # structure: the kernels' own achieved bandwidth, free of the chains' concurrency
+    iso = None
+    if not args.no_graph and not args.no_isolated:
+        saved = (R.chains, R.chain_streams)
+        R.chains, R.chain_streams = [(0, len(R.reqs))], [torch.cuda.Stream(device=dev)]
+        R.cache.enable_kernel_timer(True)
+        R.prepare_graph(s)
+        for _ in range(2):
+            run()
+        R.cache.enable_kernel_timer(True)
+        ms_iso = kdist.max_over_ranks(timed_steps(args.steps), dev)
+        kti = R.cache.read_kernel_timer()
+        R.cache.enable_kernel_timer(False)
+        R.chains, R.chain_streams = saved
+        R.prepare_graph(s)
+        iso = {"ms_per_step": ms_iso, "chains": 1}
+        for kind, by in (("select", b["select"] + (b["resolve"] if R.fused else 0)), ("attn", b["attn"])):
+            ns, nl = kti[kind]
+            if nl:
+                us = ns / nl * 1e-3
+                gbs = by * segs_per_layer / (us * 1e-6) / 1e9
+                iso[kind] = {"kernel": KIND_NAMES[kind], "avg_launch_us": us, "segments_per_launch": segs_per_layer,
+                             "hbm_bytes_per_launch": by * segs_per_layer, "achieved_gbs": gbs,
+                             "frac_hbm": gbs / hbm_peak, "launches_per_step": nl / args.steps}
+        if "attn" in iso:
+            roof_attn = {"achieved": iso["attn"]["achieved_gbs"], "peak": hbm_peak, "unit": "GB/s",
+                         "frac": iso["attn"]["frac_hbm"],
+                         "scope": "attention kernel, whole-batch launches (chains = 1), device-timed"}
     R.cache.check()
     clocks = clk.stop()
 
@@ -561,7 +592,7 @@ def run_gpu(args):
                    "l2": "inputs larger than L2 (no flush)"},
         "hit_rate": hit_rate, "misses_per_segment": misses_per_seg,
         "roofline": roof, "roofline_attn": roof_attn, "hbm_step": hbm_step, "host_link_step": link_step,
-        "kernels": kernels, "host_link": link, "e2e": e2e,
+        "kernels": kernels, "kernels_isolated": iso, "host_link": link, "e2e": e2e,
         "ms_per_step_with_kernel_timer": ms_timer,
         "gpu_launches": R.launches_per_step * args.steps,
         "clocks": clocks, "setup_s": R.setup_s,

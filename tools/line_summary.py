@@ -16,4 +16,6 @@ for path in sys.argv[1:]:
                   for k, v in d["kernels"].items())
     print(f"{d['config']['workload']} {d['value']:.0f} tok/s {d['ms_per_step']:.3f} ms (timer {d.get('ms_per_step_with_kernel_timer') or 0:.3f})"
           f" hit {d['hit_rate']:.3f} roof {r['bound']} {r['frac']:.2f} hbm_step {d['hbm_step']['frac']:.2f} | {ks}"
-          f" | e2e {(d.get('e2e') or {}).get('value', 0):.0f}")
+          f" | e2e {(d.get('e2e') or {}).get('value', 0):.0f}"
+          + (" | iso " + " ".join(f"{k}:{v['avg_launch_us']:.1f}us/{v['frac_hbm']:.2f}" for k, v in d["kernels_isolated"].items()
+                                  if isinstance(v, dict)) if d.get("kernels_isolated") else ""))

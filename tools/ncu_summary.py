@@ -18,10 +18,13 @@ def summarise(path):
         t = m["gpu__time_duration.sum"]
         rd = sum(m.get("dram__bytes_read.sum", [0])) / len(t)
         wr = sum(m.get("dram__bytes_write.sum", [0])) / len(t)
+        pr = sum(m.get("pcie__read_bytes.sum", [0])) / len(t)
+        pw = sum(m.get("pcie__write_bytes.sum", [0])) / len(t)
         avg = sum(t) / len(t)
-        out.append((n, len(t), avg, sum(t) / tot, rd, wr))
+        out.append((n, len(t), avg, sum(t) / tot, rd, wr, pr, pw))
         print(f"  {n:16s} n={len(t):4d} avg={avg / 1e3:9.2f} us share={sum(t) / tot:.3f} "
-              f"dram rd={rd / 1e6:8.2f} MB wr={wr / 1e6:7.2f} MB -> {(rd + wr) / avg:7.1f} GB/s")
+              f"dram rd={rd / 1e6:8.2f} MB wr={wr / 1e6:7.2f} MB -> {(rd + wr) / avg:7.1f} GB/s"
+              f"  pcie rd={pr / 1e6:7.2f} MB wr={pw / 1e6:6.2f} MB -> {(pr + pw) / avg:6.1f} GB/s")
     return out
 
 
