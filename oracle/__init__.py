@@ -63,6 +63,10 @@ def lib():
         L.or_fetch.restype = None
         L.or_attention.argtypes = [p, i32, i32, p, p, i64, i32, p, i32, p, p]
         L.or_attention.restype = None
+        L.or_index_build.argtypes = [p, i64, i32, i32, p, p]
+        L.or_index_build.restype = i64
+        L.or_index_select.argtypes = [p, p, p, p, i64, i64, i32, p, i32, i32, p, p, p]
+        L.or_index_select.restype = i32
         _lib = L
     return _lib
 
@@ -193,6 +197,45 @@ def attention(q, K, V, P, blocks):
     return o, lse
 
 
+# ---------------------------------------------------------------- O9..O10 hierarchical index
+IDX_WINDOW = 64        # blocks per k-means window (OR_IDX_WIN)
+IDX_FANOUT = 4         # stage 1 keeps ceil(IDX_FANOUT * k / ratio) centroids (reading R27)
+
+
+def index_build(S, ratio):
+    """O9: block summaries S [nb][d] bf16 -> (centroids [nc][d] bf16, cent_of [nb] int32)."""
+    S = _c(S, np.uint16)
+    nb, d = S.shape
+    cent = np.empty((max(nb, 1), d), np.uint16)
+    cent_of = np.empty(max(nb, 1), np.int32)
+    nc = lib().or_index_build(_p(S), nb, d, ratio, _p(cent), _p(cent_of))
+    return cent[:nc].copy(), cent_of[:nb].copy()
+
+
+def index_fanout(k, ratio, nc):
+    """Stage-1 centroid count m for top-k (reading R27)."""
+    return min(nc, -(-IDX_FANOUT * k // ratio))
+
+
+def index_select(qbar, S, cent, cent_of, is_pinned, k, m):
+    """O10: (ids [k] ascending, centroid scores [nc], lookahead scores [nb])."""
+    qbar = _c(qbar, np.float32)
+    S = _c(S, np.uint16)
+    cent = _c(cent, np.uint16)
+    cent_of = _c(cent_of, np.int32)
+    is_pinned = _c(is_pinned, np.uint8)
+    nb, d = S.shape
+    nc = cent.shape[0]
+    ids = np.empty(max(k, 1), np.int32)
+    cs = np.empty(max(nc, 1), np.float32)
+    la = np.empty(max(nb, 1), np.float32)
+    rc = lib().or_index_select(_p(qbar), _p(S), _p(cent), _p(cent_of), nb, nc, d, _p(is_pinned), k, m,
+                               _p(ids), _p(cs), _p(la))
+    if rc:
+        raise OracleError(rc, "index_select")
+    return ids[:k], cs[:nc], la[:nb]
+
+
 # ---------------------------------------------------------------- composition
 def segment_select(q_group, S, is_pinned, k):
     """O2 -> O3 -> O5 for one segment: returns (ids, scores)."""
@@ -200,10 +243,16 @@ def segment_select(q_group, S, is_pinned, k):
     return topk(scores, is_pinned, k), scores
 
 
-def segment_step(cache, q_group, S, K, V, P, k, step, policy, W):
+def segment_step(cache, q_group, S, K, V, P, k, step, policy, W, index=None):
     """One decode step of one segment, in the paper's order (PAPER.md:241-244,
-    386): select (O2,O3,O5) -> resolve (O6) -> attend (O8).  Returns a dict."""
-    ids, scores = segment_select(q_group, S, cache.is_pinned, k)
+    386): select (O2,O3,O5; or the hierarchical index O9-O10 when index =
+    (centroids, cent_of, ratio)) -> resolve (O6) -> attend (O8).  Returns a dict."""
+    if index is None:
+        ids, scores = segment_select(q_group, S, cache.is_pinned, k)
+    else:
+        cent, cent_of, ratio = index
+        ids, _, scores = index_select(group_query(q_group), S, cent, cent_of, cache.is_pinned, k,
+                                      index_fanout(k, ratio, cent.shape[0]))
     attn, miss, nm, nh = cache.resolve(ids, step, policy, scores, W)
     o, lse = attention(q_group, K, V, P, attn[:, 0])
     return dict(ids=ids, scores=scores, attn=attn, miss=miss, n_miss=nm, n_hit=nh, o=o, lse=lse)

@@ -366,3 +366,134 @@ void or_attention(const uint16_t* q, int32_t G, int32_t d, const uint16_t* K,
     }
     free(tok); free(z); free(acc);
 }
+
+/* ================================================= O9-O10 hierarchical index
+ * "the KV cache is partitioned into chunks, and the mean key of each page is used
+ * as its representative, forming higher-level centroids for similarity grouping.
+ * Unlike global K-means-based ANNS approaches, this hierarchical structure
+ * preserves local semantic continuity among contiguous tokens";
+ * "a larger number of centroids improves selection granularity but increases
+ * selection cost, as each query must compare against more index representatives"
+ * (PAPER.md:549).  Reading R27: blocks (the chunks, with their O1
+ * summaries) are clustered inside windows of OR_IDX_WIN consecutive blocks (local
+ * grouping) by Lloyd k-means into ceil(len / ratio) centroids per window:
+ *   init     centroid i of a window of len blocks = summary of block
+ *            start + floor(i * len / nw)  (fp32 of its bf16 values)
+ *   assign   block b -> argmin_c dist(b, c), dist = fma chain over j = 0..127 of
+ *            (s_b[j] - c[j])^2 from +0 (fp32), ties -> lowest c
+ *   update   c[j] = (sum over members in block order from +0) / count (fp32, IEEE);
+ *            a centroid without members keeps its value
+ *   OR_IDX_ITERS (assign, update) rounds, then a final assign.  Centroids left
+ *   without members are dropped; the others are numbered window by window in
+ *   ascending order and stored as bf16 (RNE) vectors.
+ * Outputs: centroids [nc][d] bf16, cent_of[nb] (block -> centroid), returns nc. */
+#define OR_IDX_WIN 64
+#define OR_IDX_ITERS 4
+
+static float or_dist(const float* a, const float* c, int32_t d) {
+    float acc = 0.0f;
+    for (int32_t j = 0; j < d; ++j) {
+        float diff = a[j] - c[j];
+        acc = fmaf(diff, diff, acc);
+    }
+    return acc;
+}
+
+int64_t or_index_build(const uint16_t* S, int64_t nb, int32_t d, int32_t ratio,
+                       uint16_t* centroids, int32_t* cent_of) {
+    int64_t nc = 0;
+    float* x = (float*)malloc(sizeof(float) * OR_IDX_WIN * (size_t)d);
+    float* c = (float*)malloc(sizeof(float) * OR_IDX_WIN * (size_t)d);
+    int32_t* as = (int32_t*)malloc(sizeof(int32_t) * OR_IDX_WIN);
+    int32_t* cnt = (int32_t*)malloc(sizeof(int32_t) * OR_IDX_WIN);
+    int32_t* newid = (int32_t*)malloc(sizeof(int32_t) * OR_IDX_WIN);
+    for (int64_t w0 = 0; w0 < nb; w0 += OR_IDX_WIN) {
+        int32_t len = (int32_t)(nb - w0 < OR_IDX_WIN ? nb - w0 : OR_IDX_WIN);
+        int32_t nw = (len + ratio - 1) / ratio;
+        for (int32_t b = 0; b < len; ++b)
+            for (int32_t j = 0; j < d; ++j) x[b * d + j] = bf16_to_f32(S[(w0 + b) * d + j]);
+        for (int32_t i = 0; i < nw; ++i) {
+            int32_t b = (int32_t)(((int64_t)i * len) / nw);
+            for (int32_t j = 0; j < d; ++j) c[i * d + j] = x[b * d + j];
+        }
+        for (int32_t it = 0; it <= OR_IDX_ITERS; ++it) {
+            /* assign */
+            for (int32_t b = 0; b < len; ++b) {
+                int32_t best = 0;
+                float bd = or_dist(x + b * d, c, d);
+                for (int32_t i = 1; i < nw; ++i) {
+                    float di = or_dist(x + b * d, c + i * d, d);
+                    if (di < bd) { bd = di; best = i; }
+                }
+                as[b] = best;
+            }
+            if (it == OR_IDX_ITERS) break;          /* final assignment only */
+            /* update */
+            for (int32_t i = 0; i < nw; ++i) {
+                int32_t n = 0;
+                for (int32_t b = 0; b < len; ++b) n += as[b] == i;
+                if (n == 0) continue;
+                for (int32_t j = 0; j < d; ++j) {
+                    float acc = 0.0f;
+                    for (int32_t b = 0; b < len; ++b)
+                        if (as[b] == i) acc = acc + x[b * d + j];
+                    c[i * d + j] = acc / (float)n;
+                }
+            }
+        }
+        for (int32_t i = 0; i < nw; ++i) cnt[i] = 0;
+        for (int32_t b = 0; b < len; ++b) cnt[as[b]]++;
+        for (int32_t i = 0; i < nw; ++i) {
+            if (cnt[i] == 0) { newid[i] = -1; continue; }
+            newid[i] = (int32_t)nc;
+            for (int32_t j = 0; j < d; ++j) centroids[nc * d + j] = or_f32_to_bf16_rne(c[i * d + j]);
+            ++nc;
+        }
+        for (int32_t b = 0; b < len; ++b) cent_of[w0 + b] = newid[as[b]];
+    }
+    free(x); free(c); free(as); free(cnt); free(newid);
+    return nc;
+}
+
+/* O10 two-stage descent ("identifying critical KV entries via the index";
+ * reading R27): stage 1 scores every centroid like a block (O3: fma chain of qbar x
+ * centroid) and keeps the m best (score desc, centroid index asc; NaN lowest,
+ * -0 == +0); stage 2 takes the non-pinned member blocks of those centroids as
+ * candidates -- every non-pinned block if they are fewer than k -- scores them
+ * exactly (O3) and returns the k best candidates (O5 order), ascending by id.
+ * cscores[nc] receives the centroid scores, la[nb] the lookahead eviction score of
+ * every block: its exact score if it was a candidate, else its centroid's score.
+ * Returns 0, or 2 (ERANGE) when k exceeds the non-pinned blocks. */
+int32_t or_index_select(const float* qbar, const uint16_t* S, const uint16_t* centroids,
+                        const int32_t* cent_of, int64_t nb, int64_t nc, int32_t d,
+                        const uint8_t* is_pinned, int32_t k, int32_t m,
+                        int32_t* ids, float* cscores, float* la) {
+    or_block_scores(qbar, centroids, nc, d, cscores);
+    uint8_t* zero = (uint8_t*)calloc((size_t)(nc > 0 ? nc : 1), 1);
+    if (m > nc) m = (int32_t)nc;
+    int32_t* top = (int32_t*)malloc(sizeof(int32_t) * (size_t)(m > 0 ? m : 1));
+    int32_t rc = or_topk(cscores, nc, zero, m, top);            /* O5 order over centroids */
+    free(zero);
+    if (rc) { free(top); return rc; }
+    uint8_t* chosen = (uint8_t*)calloc((size_t)(nc > 0 ? nc : 1), 1);
+    for (int32_t i = 0; i < m; ++i) chosen[top[i]] = 1;
+    free(top);
+    /* candidates: non-pinned members of the chosen centroids; all non-pinned if < k */
+    uint8_t* excl = (uint8_t*)malloc((size_t)(nb > 0 ? nb : 1));   /* 1 = not a candidate */
+    int64_t ncand = 0, nfree = 0;
+    for (int64_t b = 0; b < nb; ++b) {
+        nfree += !is_pinned[b];
+        excl[b] = (uint8_t)(is_pinned[b] || !chosen[cent_of[b]]);
+        ncand += !excl[b];
+    }
+    free(chosen);
+    if (ncand < k)
+        for (int64_t b = 0; b < nb; ++b) excl[b] = is_pinned[b];
+    float* bs = (float*)malloc(sizeof(float) * (size_t)(nb > 0 ? nb : 1));
+    or_block_scores(qbar, S, nb, d, bs);                         /* exact scores (O3) */
+    for (int64_t b = 0; b < nb; ++b) la[b] = excl[b] ? cscores[cent_of[b]] : bs[b];
+    if (k > nfree) { free(bs); free(excl); return 2; }
+    rc = or_topk(bs, nb, excl, k, ids);                          /* O5 over the candidates */
+    free(bs); free(excl);
+    return rc;
+}
