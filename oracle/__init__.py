@@ -212,9 +212,11 @@ def index_build(S, ratio):
     return cent[:nc].copy(), cent_of[:nb].copy()
 
 
-def index_fanout(k, ratio, nc):
-    """Stage-1 centroid count m for top-k (reading R27)."""
-    return min(nc, -(-IDX_FANOUT * k // ratio))
+def index_fanout(k, ratio, nc, pinned):
+    """Stage-1 centroid count m for top-k (reading R27): ceil(IDX_FANOUT * k / ratio), at least
+    k + pinned (every centroid has a member, so the m best centroids then hold >= k non-pinned
+    members and stage 2 always has k candidates), at most nc."""
+    return min(nc, max(-(-IDX_FANOUT * k // ratio), k + int(pinned)))
 
 
 def index_select(qbar, S, cent, cent_of, is_pinned, k, m):
@@ -252,7 +254,7 @@ def segment_step(cache, q_group, S, K, V, P, k, step, policy, W, index=None):
     else:
         cent, cent_of, ratio = index
         ids, _, scores = index_select(group_query(q_group), S, cent, cent_of, cache.is_pinned, k,
-                                      index_fanout(k, ratio, cent.shape[0]))
+                                      index_fanout(k, ratio, cent.shape[0], cache.is_pinned.sum()))
     attn, miss, nm, nh = cache.resolve(ids, step, policy, scores, W)
     o, lse = attention(q_group, K, V, P, attn[:, 0])
     return dict(ids=ids, scores=scores, attn=attn, miss=miss, n_miss=nm, n_hit=nh, o=o, lse=lse)

@@ -31,7 +31,7 @@ def test_ratio_one_reduces_to_flat_topk(n, P, k, seed):
     for t in range(3):
         q = synth.queries(seed, 0, 0, 0, 4, t0=t, nsteps=1)[0]
         ids, _, la = oracle.index_select(oracle.group_query(q), S, cent, cent_of, pin, k,
-                                         oracle.index_fanout(k, 1, cent.shape[0]))
+                                         oracle.index_fanout(k, 1, cent.shape[0], pin.sum()))
         ref, sc = oracle.segment_select(q, S, pin, k)
         assert np.array_equal(ids, ref)
         cand = np.zeros(len(pin), bool)
@@ -114,8 +114,8 @@ def test_descent_matches_independent_restatement(seed, alpha):
     S = oracle.block_summaries(K, P)
     cent, cent_of = oracle.index_build(S, ratio)
     pin = oracle.pinned_blocks(n, P)
-    m = oracle.index_fanout(k, ratio, cent.shape[0])
-    assert m == 128
+    m = oracle.index_fanout(k, ratio, cent.shape[0], pin.sum())
+    assert m == 128 + 5
     for t in range(2):
         q = synth.queries(seed, 0, 1, 2, 4, t0=t, nsteps=1, alpha=alpha)[0]
         qb = oracle.group_query(q)
@@ -124,6 +124,21 @@ def test_descent_matches_independent_restatement(seed, alpha):
         assert np.array_equal(ids, rid)
         assert np.array_equal(cs.view(np.uint32), rcs.view(np.uint32))
         assert np.array_equal(la.view(np.uint32), rla.view(np.uint32))
+
+
+def test_fanout_always_leaves_k_candidates():
+    # m >= k + pinned and every centroid owns a block: stage 2 never runs short of candidates
+    for n, P, ratio, k in [(2048, 16, 8, 100), (5000, 4, 16, 200), (1500, 16, 2, 60)]:
+        K, _ = synth.segment_kv(4, 0, 0, 0, n)
+        S = oracle.block_summaries(K, P)
+        cent, cent_of = oracle.index_build(S, ratio)
+        pin = oracle.pinned_blocks(n, P)
+        m = oracle.index_fanout(k, ratio, cent.shape[0], pin.sum())
+        for t in range(3):
+            qb = oracle.group_query(synth.queries(4, 0, 0, 0, 4, t0=t, nsteps=1)[0])
+            top = np.lexsort((np.arange(cent.shape[0]), -oracle.block_scores(qb, cent).astype(np.float64)))[:m]
+            cand = np.isin(cent_of, top) & ~pin.astype(bool)
+            assert cand.sum() >= k
 
 
 def test_few_candidates_fall_back_to_every_block():
@@ -151,7 +166,7 @@ def test_index_recall_on_clustered_workload_is_high():
     for t in range(4):
         q = synth.queries(0, 0, 0, 0, 4, t0=t, nsteps=1)[0]
         ids, _, _ = oracle.index_select(oracle.group_query(q), S, cent, cent_of, pin, k,
-                                        oracle.index_fanout(k, 4, cent.shape[0]))
+                                        oracle.index_fanout(k, 4, cent.shape[0], pin.sum()))
         ref, _ = oracle.segment_select(q, S, pin, k)
         rec.append(len(set(ids) & set(ref)) / k)
     assert np.mean(rec) > 0.8, rec
