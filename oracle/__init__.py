@@ -67,6 +67,10 @@ def lib():
         L.or_index_build.restype = i64
         L.or_index_select.argtypes = [p, p, p, p, i64, i64, i32, p, i32, i32, p, p, p]
         L.or_index_select.restype = i32
+        L.or_mckp_greedy.argtypes = [p, p, i32, i32, ctypes.c_double, p]
+        L.or_mckp_greedy.restype = ctypes.c_double
+        L.or_mckp_exact.argtypes = [p, p, i32, i32, ctypes.c_double, p]
+        L.or_mckp_exact.restype = ctypes.c_double
         _lib = L
     return _lib
 
@@ -236,6 +240,21 @@ def index_select(qbar, S, cent, cent_of, is_pinned, k, m):
     if rc:
         raise OracleError(rc, "index_select")
     return ids[:k], cs[:nc], la[:nb]
+
+
+# ---------------------------------------------------------------- O11 2D window scaling (MCKP)
+def mckp(benefit, cost, budget, exact=False):
+    """O11: (total benefit, choice [pairs]) for benefit / cost [pairs][sizes] (PAPER.md:480-496);
+    greedy by benefit-to-cost ratio, or exhaustive (exact=True, tiny instances)."""
+    b = _c(benefit, np.float64)
+    c = _c(cost, np.float64)
+    pairs, sizes = b.shape
+    choice = np.empty(pairs, np.int32)
+    f = lib().or_mckp_exact if exact else lib().or_mckp_greedy
+    tot = f(_p(b), _p(c), pairs, sizes, float(budget), _p(choice))
+    if tot < 0:
+        raise OracleError(-1, "mckp (infeasible or too large)")
+    return tot, choice
 
 
 # ---------------------------------------------------------------- composition

@@ -497,3 +497,68 @@ int32_t or_index_select(const float* qbar, const uint16_t* S, const uint16_t* ce
     free(bs); free(excl);
     return rc;
 }
+
+/* ============================================ O11 2D layer-head window scaling
+ * "For each layer l and head h, profiling yields: Benefit_{l,h}(w): transfer reduction
+ * achieved with window size w, Cost_{l,h}(w): additional GPU memory consumed by that window
+ * size.  Given a total GPU cache budget M, the objective is max sum Benefit s.t. sum Cost <= M
+ * ... a variant of the multiple-choice knapsack problem ... for small models, exhaustive search
+ * is feasible; for larger ones, we employ a greedy algorithm that starts from the smallest
+ * windows and iteratively enlarges the window with the highest benefit-to-cost ratio until the
+ * GPU cache budget is met".  benefit/cost: [pairs][sizes], sizes in
+ * increasing cost order.  choice[pairs] receives the chosen size index.
+ *
+ * or_mckp_greedy: all pairs at size 0; repeatedly apply the single upgrade (pair p -> size s > its
+ * current size) with the highest (benefit gain) / (cost gain) among those that fit the budget
+ * (ties: lower pair, then lower size); stop when none fits.  Returns the total benefit, or
+ * -1 if the smallest sizes already exceed the budget. */
+double or_mckp_greedy(const double* benefit, const double* cost, int32_t pairs, int32_t sizes,
+                      double budget, int32_t* choice) {
+    double used = 0.0, total = 0.0;
+    for (int32_t p = 0; p < pairs; ++p) { choice[p] = 0; used += cost[p * sizes]; total += benefit[p * sizes]; }
+    if (used > budget) return -1.0;
+    for (;;) {
+        int32_t bp = -1, bs = -1;
+        double br = 0.0;
+        for (int32_t p = 0; p < pairs; ++p) {
+            int32_t cur = choice[p];
+            for (int32_t s = cur + 1; s < sizes; ++s) {
+                double dc = cost[p * sizes + s] - cost[p * sizes + cur];
+                double db = benefit[p * sizes + s] - benefit[p * sizes + cur];
+                if (used + dc > budget) continue;
+                double r = dc > 0 ? db / dc : (db > 0 ? INFINITY : 0.0);
+                if (db <= 0.0 && dc >= 0.0) continue;            /* no gain */
+                if (bp < 0 || r > br) { bp = p; bs = s; br = r; }
+            }
+        }
+        if (bp < 0) break;
+        used += cost[bp * sizes + bs] - cost[bp * sizes + choice[bp]];
+        total += benefit[bp * sizes + bs] - benefit[bp * sizes + choice[bp]];
+        choice[bp] = bs;
+    }
+    return total;
+}
+
+/* or_mckp_exact: the optimum by enumeration of every allocation (sizes^pairs <= 1e7), ties ->
+ * the lexicographically smallest allocation.  Returns the best total benefit or -1. */
+double or_mckp_exact(const double* benefit, const double* cost, int32_t pairs, int32_t sizes,
+                     double budget, int32_t* choice) {
+    double combos = 1.0;
+    for (int32_t p = 0; p < pairs; ++p) combos *= sizes;
+    if (combos > 1e7 || pairs < 1) return -1.0;
+    int32_t* cur = (int32_t*)calloc((size_t)pairs, sizeof(int32_t));
+    double best = -1.0;
+    for (;;) {
+        double c = 0.0, b = 0.0;
+        for (int32_t p = 0; p < pairs; ++p) { c += cost[p * sizes + cur[p]]; b += benefit[p * sizes + cur[p]]; }
+        if (c <= budget && b > best) {
+            best = b;
+            for (int32_t p = 0; p < pairs; ++p) choice[p] = cur[p];
+        }
+        int32_t p = pairs - 1;                    /* next allocation, lexicographic */
+        while (p >= 0 && ++cur[p] == sizes) cur[p--] = 0;
+        if (p < 0) break;
+    }
+    free(cur);
+    return best;
+}
