@@ -60,6 +60,11 @@ CONFIGS = {
                desc="Qwen2.5-7B-1M shapes (28 layers, 28q/4kv, d128), 1M ctx, batch 4, GPU cache 25%, host-backed"),
     "c4k": dict(chains=4, L=28, B=4, Hq=28, Hkv=4, n=1 << 20, P=16, k=1024, C=16384, alias=2, shard="strong",
                 desc="c4 with top-k 1024 blocks (16384 tokens = 1.56% of 1M, SURVEY 8.2)"),
+    "c4h": dict(chains=4, L=28, B=4, Hq=28, Hkv=4, n=1 << 20, P=16, k=128, C=16384, alias=2, shard="strong", index=4,
+                desc="c4 with the hierarchical centroid index (k-means over block summaries, 4 blocks per centroid; "
+                     "PAPER.md:388-391, DESIGN.md R27)"),
+    "c3h": dict(chains=16, L=32, B=16, Hq=32, Hkv=8, n=131072, P=16, k=128, C=2048, alias=4, shard="weak", index=4,
+                desc="c3 with the hierarchical centroid index (4 blocks per centroid)"),
     "c5": dict(chains=16, L=32, B=64, Hq=32, Hkv=8, n=131072, P=16, k=128, C=768, alias=2, shard="strong",
                desc="Llama-3.1-8B shapes, 128k ctx, batch 64 partitioned over the GPUs, GPU cache 768 "
                     "slots/segment (9.4%), host-backed"),
@@ -119,15 +124,25 @@ def cpu_cores():
 
 # ---------------------------------------------------------------- algorithmic bytes
 def per_segment_bytes(cfg, misses_per_seg=0.0, victims=True):
-    """Algorithmic bytes per segment per step, by row."""
+    """Algorithmic bytes per segment per step, by row.  With the
+    hierarchical index (R27) select reads the centroids (256 B each, ~nb/ratio) and the member
+    summaries of the m chosen centroids (~ratio * m blocks) instead of every block summary."""
     nb = (cfg["n"] + cfg["P"] - 1) // cfg["P"]
     G = cfg["Hq"] // cfg["Hkv"]
     k = cfg["k"]
+    ratio = cfg.get("index", 0)
+    if ratio:
+        nc = -(-nb // ratio)
+        p_ = 1 + (64 + cfg["P"] - 1) // cfg["P"]
+        m = min(nc, max(-(-4 * k // ratio), k + p_))
+        sel_blocks = nc + ratio * m               # centroid rows + member rows (expected)
+    else:
+        sel_blocks = nb
     C = cfg["C"] if cfg["C"] is not None else nb
     p = 1 + (64 + cfg["P"] - 1) // cfg["P"]          # sink block + local blocks (n % P == 0)
     resident = C >= nb
     return dict(
-        select=SUMMARY * nb + 2 * G * 128 + 8 * k,          # summaries + q + (ids, scores)
+        select=SUMMARY * sel_blocks + 2 * G * 128 + 8 * k,  # summaries (or centroids + members) + q + ids
         resolve=4 * k + (0 if resident or not victims else 13 * C + 4 * C),   # table probes + victim scan (LA)
         attn=RECORD * (k + p) + 2 * G * 128 + 4 * G * 128 + 4 * G,   # K/V pages + q + o + lse
         fetch=RECORD * misses_per_seg,                     # host link read (and HBM write)
@@ -243,7 +258,8 @@ class Runner:
         self.A = A
         self.cache = KVCache(num_layers=L, num_q_heads=Hq, num_kv_heads=Hkv, block_tokens=P, max_requests=B,
                              max_context=n, slots_per_segment=C, max_select=k, sink_tokens=4, local_tokens=64,
-                             policy=args.policy, host_layer_alias=(0 if self.A == L else self.A), device=dev.index)
+                             policy=args.policy, host_layer_alias=(0 if self.A == L else self.A), device=dev.index,
+                             index_ratio=cfg.get("index", 0))
         self.W = self.cache.attn_width(k)
         t0 = time.time()
         Kd = torch.empty((Hkv, n, 128), dtype=torch.int16, device=dev)

@@ -103,6 +103,14 @@ typedef struct {
                                     affordance for hosts with less RAM than the KV: the caller must
                                     load identical prefixes for layers l and l' when l == l' mod A. */
     int32_t device;              /* CUDA device ordinal */
+    int32_t index_ratio;         /* 0: flat index -- every block summary is scored (default).
+                                    r in 1..64: hierarchical centroid index (
+                                    DESIGN.md R27): kvd_load_prefix clusters each segment's block
+                                    summaries by k-means inside windows of 64 blocks into
+                                    ceil(len / r) centroids per window; the select calls score the
+                                    centroids, keep the m = min(nc, max(ceil(4k/r), k + pinned)) best
+                                    and score only their member blocks (exact top-k among those).
+                                    Needs min(blocks, 64 m) <= 16384 (KVD_EINVAL otherwise). */
 } kvd_config;
 
 typedef struct {
@@ -224,10 +232,32 @@ kvd_status kvd_read_host_record(kvd_cache* c, int32_t layer, int32_t req, int32_
 /* Copy a segment's summaries as [nb][128] bf16 (block-major, unpadded). */
 kvd_status kvd_read_summaries(kvd_cache* c, int32_t layer, int32_t req, int32_t head,
                               uint16_t* out);
-/* Copy a segment's current block scores [nb] fp32 (last select of that layer). */
+/* Hierarchical index of one segment (index_ratio > 0): *nc receives the centroid count;
+ * centroids [nc][128] bf16 (block-major copy) and cent_of [nb] (block -> centroid) may be NULL. */
+kvd_status kvd_read_index(kvd_cache* c, int32_t layer, int32_t req, int32_t head, int64_t* nc,
+                          uint16_t* centroids, int32_t* cent_of);
+/* Copy a segment's current block scores [nb] fp32 (last select of that layer; with the
+ * hierarchical index: the lookahead scores -- exact for the candidates, else the centroid's). */
 kvd_status kvd_read_scores(kvd_cache* c, int32_t layer, int32_t req, int32_t head, float* out);
 
 kvd_status kvd_get_stats(kvd_cache* c, kvd_stats* out);   /* synchronises the device */
+
+/* 2D layer-head window scaling (R28).
+ * kvd_set_segment_capacity: layer-head pair (layer, head) of every request may use only slots
+ * 0 .. slots-1 of its segment (its "window"); pinned <= slots <= slots_per_segment.  Shrinking
+ * drops the residents of the cut slots (their blocks are fetched again when selected).  Host-backed
+ * caches only (KVD_ESTATE otherwise).  Synchronises the device.  A step call needs k + pinned <=
+ * the smallest capacity of its layer (KVD_ECAPACITY).
+ * kvd_get_segment_stats: per layer-head counters since kvd_reset_stats, [L][Hkv] each: selected
+ * (non-pinned) blocks resolved and misses -- the profile of Benefit(w) (transfer reduction).
+ * kvd_plan_window_scaling: the offline planner: greedy multiple-choice knapsack over `pairs`
+ * layer-head pairs x `sizes` candidate windows (benefit / cost [pairs][sizes], sizes in increasing
+ * cost); choice[pairs] receives the chosen size index.  Host only (no GPU); KVD_EINVAL if the
+ * smallest sizes exceed the budget. */
+kvd_status kvd_set_segment_capacity(kvd_cache* c, int32_t layer, int32_t head, int64_t slots);
+kvd_status kvd_get_segment_stats(kvd_cache* c, uint64_t* selected, uint64_t* misses);
+kvd_status kvd_plan_window_scaling(const double* benefit, const double* cost, int32_t pairs, int32_t sizes,
+                                   double budget, int32_t* choice);
 
 /* Kernel timer (measurement; bench.py).  While enabled, every step kernel records its own
  * launch duration on the device: from the earliest start of any of its CTAs / warps after

@@ -47,6 +47,11 @@ struct StepParams {
     unsigned long long* kt_acc;       // [kKtKinds][2] (ns, launches)
     int32_t kt_base;                  // slot of (layer, first request): (layer*R + req[0]) * kKtKinds
     unsigned long long* exp_trace;    // experiment builds: phase stamps (NULL otherwise)
+    // hierarchical index (kvd_config.index_ratio > 0): select_kernel's view for stage 1
+    int32_t sel_mode;                 // 0 = block summaries; 1 = centroids of the segment (stage 1)
+    int32_t sel_ratio;                // blocks per centroid (stage-1 fan-out, reading R27)
+    int32_t sel_stride;               // stage 1: output stride per segment (m_max)
+    const int32_t* sel_count;         // stage 1: centroids per segment [L][R][Hkv]
     int32_t req[KVD_MAX_BATCH];
 };
 
@@ -71,6 +76,22 @@ struct kvd_cache {
     uint32_t* use_count = nullptr;
     int32_t* miss = nullptr;
     int32_t* miss_count = nullptr;
+    // hierarchical index (index_ratio > 0; k_index.cu, DESIGN.md §3 R27)
+    int index_ratio = 0;
+    int64_t nc_pad = 0;                    // centroid rows per segment (multiple of 128)
+    int m_max = 0;                         // stage-1 centroids per segment at most
+    uint16_t* cent = nullptr;              // [L][R][Hkv][128][nc_pad] bf16, dim-major
+    float* cscores = nullptr;              // [L][R][Hkv][nc_pad] fp32 (stage-1 scores)
+    int32_t* ncent = nullptr;              // [L][R][Hkv] centroids per segment
+    int32_t* cent_of = nullptr;            // [L][R][Hkv][nb_pad] block -> centroid
+    int32_t* memb = nullptr;               // [L][R][Hkv][nb_pad] blocks ordered by (centroid, block)
+    int32_t* moff = nullptr;               // [L][R][Hkv][nc_pad + 1] member offsets
+    int32_t* csel = nullptr;               // [R][Hkv][m_max] stage-1 selection (scratch)
+    uint8_t* idx_stage = nullptr;          // setup scratch of the index build
+    // 2D window scaling (R28): per layer-head capacity; per layer-head selection / miss counters
+    std::vector<int64_t> cap_host;         // [L][Hkv]
+    int32_t* cap_dev = nullptr;            // [L][Hkv]
+    unsigned long long* seg_stats = nullptr;   // [L][Hkv][2]
     unsigned long long* kt_slots = nullptr;  // kernel timer (bench instrumentation)
     unsigned long long* kt_acc = nullptr;
     bool kt_on = false;
@@ -101,6 +122,17 @@ size_t select_static_smem();                                                // k
 constexpr size_t kMaxSmemBytes = 227 * 1024;
 cudaError_t launch_resolve(kvd_cache* c, const StepParams& p, const int32_t* ids, int32_t* out_attn, cudaStream_t s);
 cudaError_t launch_gather(kvd_cache* c, const StepParams& p, cudaStream_t s);
+cudaError_t launch_index_build(kvd_cache* c, int layer, int req, int64_t n, cudaStream_t s);   // k_index.cu
+cudaError_t launch_index_select(kvd_cache* c, const StepParams& p, const uint16_t* q, int32_t* out_ids,
+                                float* out_scores, int32_t* out_attn, cudaStream_t s);   // k_index.cu
+size_t cand_smem_bytes(int64_t nb_pad);                                                     // k_index.cu
+size_t index_stage_bytes(int Hkv, int64_t nb_pad);                                          // k_index.cu
+cudaError_t launch_select_centroids(kvd_cache* c, const StepParams& p, const uint16_t* q, cudaStream_t s);  // k_select.cu
+constexpr int kIdxWindow = 64;        // blocks per k-means window (oracle OR_IDX_WIN)
+constexpr int kIdxIters = 4;          // Lloyd rounds before the final assignment (OR_IDX_ITERS)
+constexpr int kIdxFanout = 4;         // stage-1 centroids: ceil(kIdxFanout * k / ratio), >= k + pinned
+constexpr int kCandCap = 16384;       // stage-2 candidates per segment at most (64 * m_max)
+cudaError_t launch_shrink_capacity(kvd_cache* c, int layer, int head, int64_t cap, cudaStream_t s);   // k_resolve.cu
 cudaError_t launch_zero_copy(const void* host, void* dev, size_t bytes, int ctas, cudaStream_t s);
 cudaError_t launch_select_resolve(kvd_cache* c, const StepParams& p, const uint16_t* q, int32_t* out_ids,
                                   float* out_scores, int32_t* out_attn, cudaStream_t s);

@@ -104,6 +104,28 @@ cudaError_t launch_zero_copy(const void* host, void* dev, size_t bytes, int ctas
     return cudaGetLastError();
 }
 
+// kvd_set_segment_capacity: drop the residents of slots >= cap of layer-head (layer, head) in
+// every request (pinned blocks live in slots < pinned <= cap).  grid (R), 256 threads.
+__global__ void shrink_capacity_kernel(int32_t* table, int32_t* slot_block, int64_t nb_pad, int64_t C, int64_t cap,
+                                       int layer, int head, int R, int Hkv) {
+    const int r = blockIdx.x;
+    const int64_t seg = ((int64_t)layer * R + r) * Hkv + head;
+    int32_t* sb = slot_block + seg * C;
+    int32_t* tb = table + seg * nb_pad;
+    for (int64_t s = cap + threadIdx.x; s < C; s += blockDim.x) {
+        const int32_t b = sb[s];
+        if (b >= 0) {
+            tb[b] = -1;
+            sb[s] = -1;
+        }
+    }
+}
+
+cudaError_t launch_shrink_capacity(kvd_cache* c, int layer, int head, int64_t cap, cudaStream_t s) {
+    shrink_capacity_kernel<<<c->R, 256, 0, s>>>(c->table, c->slot_block, c->nb_pad, c->C, cap, layer, head, c->R, c->Hkv);
+    return cudaGetLastError();
+}
+
 size_t resolve_static_smem() { return sizeof(ResolveShared); }
 
 size_t resolve_smem_bytes(int64_t nkeys, int64_t kmax, int64_t nb_pad) {
@@ -115,6 +137,8 @@ ResolveBufs resolve_bufs(kvd_cache* c) {
     ResolveBufs rb{c->table,    c->slot_block, c->last_use, c->phase, c->use_count, c->scores,
                    c->ntok_dev, c->miss,       c->miss_count, c->kmax, 0,           c->stats,    c->err};
     rb.nkeys = c->resident ? 0 : c->C;            // a fully resident cache never evicts
+    rb.cap = c->cap_dev;
+    rb.seg_stats = c->seg_stats;
     return rb;
 }
 

@@ -57,12 +57,25 @@ static cudaError_t launch_select_any(kvd_cache* c, const StepParams& p, const ui
                                      float* out_scores, const FuseArgs& fa, cudaStream_t s) {
     int nt, cl, kpt, v;
     select_geometry(c->nb_pad, p.B * p.Hkv, c->resident, &nt, &cl, &kpt, &v);
-    return nt == 512 ? launch_select_nt<512, RESOLVE>(c, p, q, cl, kpt, v, out_ids, out_scores, fa, s)
-                     : launch_select_nt<1024, RESOLVE>(c, p, q, cl, kpt, v, out_ids, out_scores, fa, s);
+    return nt == 512 ? launch_select_nt<512, RESOLVE>(c, p, q, c->summ, c->scores, cl, kpt, v, out_ids, out_scores, fa, s)
+                     : launch_select_nt<1024, RESOLVE>(c, p, q, c->summ, c->scores, cl, kpt, v, out_ids, out_scores, fa, s);
+}
+
+// Stage 1 of the hierarchical index (R27): the same kernel over the segment's centroid matrix
+// (p.nb_pad = nc_pad, p.sel_mode = 1), selected centroid ids -> c->csel.  No fetch inside, so the
+// resident geometry (spread over SMs) applies.
+cudaError_t launch_select_centroids(kvd_cache* c, const StepParams& p, const uint16_t* q, cudaStream_t s) {
+    int nt, cl, kpt, v;
+    select_geometry(c->nc_pad, p.B * p.Hkv, true, &nt, &cl, &kpt, &v);
+    const FuseArgs fa{};
+    cudaError_t e = nt == 512 ? launch_select_nt<512, false>(c, p, q, c->cent, c->cscores, cl, kpt, v, c->csel, nullptr, fa, s)
+                              : launch_select_nt<1024, false>(c, p, q, c->cent, c->cscores, cl, kpt, v, c->csel, nullptr, fa, s);
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_select(kvd_cache* c, const StepParams& p, const uint16_t* q, int32_t* out_ids, float* out_scores,
                           cudaStream_t s) {
+    if (c->index_ratio > 0) return launch_index_select(c, p, q, out_ids, out_scores, nullptr, s);
     const FuseArgs fa{};
     cudaError_t e = launch_select_any<false>(c, p, q, out_ids, out_scores, fa, s);
     return e != cudaSuccess ? e : cudaGetLastError();
@@ -71,6 +84,7 @@ cudaError_t launch_select(kvd_cache* c, const StepParams& p, const uint16_t* q, 
 // kvd_select_resolve_fetch: one kernel scores, selects, resolves and copies the misses.
 cudaError_t launch_select_resolve(kvd_cache* c, const StepParams& p, const uint16_t* q, int32_t* out_ids,
                                   float* out_scores, int32_t* out_attn, cudaStream_t s) {
+    if (c->index_ratio > 0) return launch_index_select(c, p, q, out_ids, out_scores, out_attn, s);
     FuseArgs fa;
     fa.rb = resolve_bufs(c);
     fa.out_attn = out_attn;

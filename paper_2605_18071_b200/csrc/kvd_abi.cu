@@ -3,6 +3,7 @@
 // kernels, introspection.  No exception crosses this boundary.
 #include <algorithm>
 #include <atomic>
+#include <climits>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -46,6 +47,8 @@ struct Geometry {
     int L, Hq, Hkv, G, P, R, kmax, pmax, A, E, max_splits;
     int64_t nmax, nb_max, nb_pad, C, rec_bytes;
     bool resident;
+    int ratio, m_max;                 // hierarchical index (0 = flat)
+    int64_t nc_pad;
 };
 
 kvd_status check_config(const kvd_config* cfg, Geometry* g) {
@@ -100,13 +103,30 @@ kvd_status check_config(const kvd_config* cfg, Geometry* g) {
         return fail(KVD_EINVAL, "slots_per_segment=%lld < %d pinned blocks (sink/local tokens)", (long long)g->C,
                     g->pmax);
     g->max_splits = kMaxPieces;
+    g->ratio = cfg->index_ratio;
+    g->nc_pad = 0;
+    g->m_max = 0;
+    if (g->ratio < 0 || g->ratio > kIdxWindow) return fail(KVD_EINVAL, "index_ratio must be 0 (flat) or 1..%d", kIdxWindow);
+    if (g->ratio > 0) {
+        const int64_t nwin = (g->nb_max + kIdxWindow - 1) / kIdxWindow;
+        const int64_t nc_max = nwin * ((kIdxWindow + g->ratio - 1) / g->ratio);
+        g->nc_pad = (nc_max + kScoreCols - 1) / kScoreCols * kScoreCols;
+        const int64_t f = (kIdxFanout * (int64_t)g->kmax + g->ratio - 1) / g->ratio;
+        g->m_max = (int)std::min<int64_t>(nc_max, std::max<int64_t>(f, g->kmax + g->pmax));
+        if (std::min<int64_t>(g->nb_max, (int64_t)kIdxWindow * g->m_max) > kCandCap)
+            return fail(KVD_EINVAL, "hierarchical index: max_select=%d with index_ratio=%d may give %lld candidates "
+                        "(> %d)", g->kmax, g->ratio, (long long)std::min<int64_t>(g->nb_max, (int64_t)kIdxWindow * g->m_max),
+                        kCandCap);
+        if (cand_smem_bytes(g->nb_pad) + 4096 > kMaxSmemBytes)
+            return fail(KVD_EINVAL, "hierarchical index: context too long for the candidate kernel");
+    }
     if ((int64_t)g->Hkv * g->nb_max * 4 > kSlotOfBytes) return fail(KVD_EINVAL, "context too long for setup scratch");
     return KVD_OK;
 }
 
 struct Sizes {
-    size_t slots, summ, scores, table, meta4, meta1, miss, small, host;
-    size_t dev_total() const { return slots + summ + scores + table + 3 * meta4 + meta1 + miss + small; }
+    size_t slots, summ, scores, table, meta4, meta1, miss, small, host, index;
+    size_t dev_total() const { return slots + summ + scores + table + 3 * meta4 + meta1 + miss + small + index; }
 };
 
 Sizes sizes_of(const Geometry& g) {
@@ -122,6 +142,10 @@ Sizes sizes_of(const Geometry& g) {
     s.miss = rsegs * (size_t)(g.kmax > 0 ? g.kmax : 1) * 2 * 4 + rsegs * 4;
     s.small = rsegs * 12 + 64 + 4 + (size_t)g.R * 4 + g.rec_bytes;
     s.host = g.resident ? 0 : (size_t)g.A * g.R * g.Hkv * g.nb_max * g.rec_bytes;
+    s.index = 0;
+    if (g.ratio > 0)   // centroids + centroid scores + counts + cent_of + members + offsets + stage-1 ids
+        s.index = segs * (kHeadDim * g.nc_pad * 2 + g.nc_pad * 4 + 4 + 2 * g.nb_pad * 4 + (g.nc_pad + 1) * 4) +
+                  rsegs * g.m_max * 4;
     return s;
 }
 
@@ -150,9 +174,11 @@ kvd_status check_step(kvd_cache* c, int32_t layer, const int32_t* req_ids, int32
         const int pr = sg.sink_end + (sg.nb - sg.local_begin);
         if (k > sg.nb - pr)
             return fail(KVD_ERANGE, "request %d: k_blocks=%d > %d candidate blocks", r, k, sg.nb - pr);
-        if ((int64_t)k + pr > c->C)
-            return fail(KVD_ECAPACITY, "request %d: k_blocks + pinned = %d > slots_per_segment=%lld", r, k + pr,
-                        (long long)c->C);
+        int64_t cap = c->C;                       // 2D window scaling: the layer's smallest head capacity
+        for (int hh = 0; hh < c->Hkv; ++hh) cap = std::min(cap, c->cap_host[(size_t)layer * c->Hkv + hh]);
+        if ((int64_t)k + pr > cap)
+            return fail(KVD_ECAPACITY, "request %d: k_blocks + pinned = %d > slots %lld of layer %d", r, k + pr,
+                        (long long)cap, layer);
         p->req[b] = r;
     }
     p->B = B;
@@ -238,6 +264,8 @@ kvd_status kvd_create_cache(const kvd_config* cfg, kvd_cache** out) {
     c->L = g.L; c->Hq = g.Hq; c->Hkv = g.Hkv; c->G = g.G; c->P = g.P; c->R = g.R; c->kmax = g.kmax;
     c->pmax = g.pmax; c->A = g.A; c->E = g.E; c->nmax = g.nmax; c->nb_max = g.nb_max; c->nb_pad = g.nb_pad;
     c->C = g.C; c->resident = g.resident; c->rec_bytes = g.rec_bytes; c->max_splits = g.max_splits;
+    c->index_ratio = g.ratio; c->nc_pad = g.nc_pad; c->m_max = g.m_max;
+    c->cap_host.assign((size_t)g.L * g.Hkv, g.C);
     c->ntok.assign((size_t)g.R, 0);
     {
         int lo = 0, hi = 0;
@@ -262,12 +290,29 @@ kvd_status kvd_create_cache(const kvd_config* cfg, kvd_cache** out) {
     ALLOC(err, 4);
     ALLOC(ntok_dev, (size_t)g.R * 4);
     ALLOC(zero_rec, (size_t)g.rec_bytes);
+    ALLOC(cap_dev, (size_t)g.L * g.Hkv * 4);
+    ALLOC(seg_stats, (size_t)g.L * g.Hkv * 16);
+    if (g.ratio > 0) {
+        const size_t segs = (size_t)g.L * g.R * g.Hkv;
+        ALLOC(cent, segs * kHeadDim * g.nc_pad * 2);
+        ALLOC(cscores, segs * g.nc_pad * 4);
+        ALLOC(ncent, segs * 4);
+        ALLOC(cent_of, segs * g.nb_pad * 4);
+        ALLOC(memb, segs * g.nb_pad * 4);
+        ALLOC(moff, segs * (g.nc_pad + 1) * 4);
+        ALLOC(csel, rsegs * (size_t)g.m_max * 4);
+    }
 #undef ALLOC
     if (e == cudaSuccess) e = cudaMemset(c->scores, 0, s.scores);
     if (e == cudaSuccess) e = cudaMemset(c->table, 0xFF, s.table);
     if (e == cudaSuccess) e = cudaMemset(c->slot_block, 0xFF, s.meta4);
     if (e == cudaSuccess) e = cudaMemset(c->miss_count, 0, rsegs * 4);
     if (e == cudaSuccess) e = cudaMemset(c->stats, 0, 64);
+    if (e == cudaSuccess) e = cudaMemset(c->seg_stats, 0, (size_t)g.L * g.Hkv * 16);
+    if (e == cudaSuccess) {
+        std::vector<int32_t> caps((size_t)g.L * g.Hkv, (int32_t)std::min<int64_t>(g.C, INT32_MAX));
+        e = cudaMemcpy(c->cap_dev, caps.data(), caps.size() * 4, cudaMemcpyHostToDevice);
+    }
     if (e == cudaSuccess) e = cudaMemset(c->err, 0, 4);
     if (e == cudaSuccess) e = cudaMemset(c->ntok_dev, 0, (size_t)g.R * 4);
     if (e == cudaSuccess) e = cudaMemset(c->zero_rec, 0, (size_t)g.rec_bytes);
@@ -290,7 +335,7 @@ void kvd_destroy_cache(kvd_cache* c) {
     cudaSetDevice(c->cfg.device);
     cudaDeviceSynchronize();
     void* dev[] = {c->slots, c->summ, c->scores, c->table, c->slot_block, c->last_use, c->phase,
-                   c->use_count, c->miss, c->miss_count, c->kt_slots, c->kt_acc, c->stats,
+                   c->use_count, c->miss, c->miss_count, c->kt_slots, c->kt_acc, c->cap_dev, c->seg_stats, c->cent, c->cscores, c->ncent, c->cent_of, c->memb, c->moff, c->csel, c->idx_stage, c->stats,
                    c->err, c->ntok_dev, c->zero_rec, c->stage_kv, c->stage_rec};
     for (void* p : dev)
         if (p) cudaFree(p);
@@ -349,6 +394,10 @@ kvd_status kvd_load_prefix(kvd_cache* c, int32_t layer, int32_t req, const uint1
         dv = c->stage_kv + kv_elems;
     }
     KVD_CUDA(launch_prefix(c, layer, req, dk, dv, n_tokens, s));
+    if (c->index_ratio > 0) {                     // hierarchical index over the new summaries (R27)
+        if (!c->idx_stage) KVD_CUDA(dalloc(&c->idx_stage, index_stage_bytes(c->Hkv, c->nb_pad)));
+        KVD_CUDA(launch_index_build(c, layer, req, n_tokens, s));
+    }
     KVD_CUDA(cudaStreamSynchronize(s));
     c->ntok[(size_t)req] = n_tokens;
     return KVD_OK;
@@ -456,6 +505,31 @@ kvd_status kvd_read_summaries(kvd_cache* c, int32_t layer, int32_t req, int32_t 
     return KVD_OK;
 }
 
+kvd_status kvd_read_index(kvd_cache* c, int32_t layer, int32_t req, int32_t head, int64_t* nc, uint16_t* centroids,
+                          int32_t* cent_of) {
+    kvd_status st = check_seg(c, layer, req, head);
+    if (st) return st;
+    if (c->index_ratio <= 0) return fail(KVD_ESTATE, "cache has no hierarchical index");
+    if (!nc) return fail(KVD_EINVAL, "nc is NULL");
+    if (c->ntok[(size_t)req] <= 0) return fail(KVD_ESTATE, "request %d not loaded", req);
+    KVD_CUDA(cudaDeviceSynchronize());
+    const int64_t seg = ((int64_t)layer * c->R + req) * c->Hkv + head;
+    int32_t n = 0;
+    KVD_CUDA(cudaMemcpy(&n, c->ncent + seg, 4, cudaMemcpyDeviceToHost));
+    *nc = n;
+    if (centroids) {
+        std::vector<uint16_t> tmp((size_t)(kHeadDim * c->nc_pad));
+        KVD_CUDA(cudaMemcpy(tmp.data(), c->cent + seg * kHeadDim * c->nc_pad, tmp.size() * 2, cudaMemcpyDeviceToHost));
+        for (int64_t i = 0; i < n; ++i)
+            for (int j = 0; j < kHeadDim; ++j) centroids[i * kHeadDim + j] = tmp[(size_t)(j * c->nc_pad + i)];
+    }
+    if (cent_of) {
+        const int64_t nb = (c->ntok[(size_t)req] + c->P - 1) / c->P;
+        KVD_CUDA(cudaMemcpy(cent_of, c->cent_of + seg * c->nb_pad, (size_t)nb * 4, cudaMemcpyDeviceToHost));
+    }
+    return KVD_OK;
+}
+
 kvd_status kvd_read_scores(kvd_cache* c, int32_t layer, int32_t req, int32_t head, float* out) {
     kvd_status st = check_seg(c, layer, req, head);
     if (st) return st;
@@ -525,6 +599,75 @@ kvd_status kvd_read_kernel_timer(kvd_cache* c, uint64_t* ns, uint64_t* launches)
     return KVD_OK;
 }
 
+kvd_status kvd_set_segment_capacity(kvd_cache* c, int32_t layer, int32_t head, int64_t slots) {
+    if (!c) return fail(KVD_EINVAL, "cache is NULL");
+    if (layer < 0 || layer >= c->L || head < 0 || head >= c->Hkv) return fail(KVD_EINVAL, "bad layer / head");
+    if (c->resident) return fail(KVD_ESTATE, "a fully resident cache has no window to scale");
+    if (slots < c->pmax || slots > c->C)
+        return fail(KVD_EINVAL, "slots=%lld outside [%d pinned, %lld allocated]", (long long)slots, c->pmax,
+                    (long long)c->C);
+    KVD_CUDA(cudaSetDevice(c->cfg.device));
+    KVD_CUDA(cudaDeviceSynchronize());
+    int64_t& cur = c->cap_host[(size_t)layer * c->Hkv + head];
+    if (slots < cur) {
+        KVD_CUDA(launch_shrink_capacity(c, layer, head, slots, nullptr));
+        KVD_CUDA(cudaDeviceSynchronize());
+    }
+    cur = slots;
+    const int32_t v = (int32_t)slots;
+    KVD_CUDA(cudaMemcpy(c->cap_dev + (size_t)layer * c->Hkv + head, &v, 4, cudaMemcpyHostToDevice));
+    return KVD_OK;
+}
+
+kvd_status kvd_get_segment_stats(kvd_cache* c, uint64_t* selected, uint64_t* misses) {
+    if (!c || !selected || !misses) return fail(KVD_EINVAL, "NULL argument");
+    KVD_CUDA(cudaDeviceSynchronize());
+    std::vector<unsigned long long> v((size_t)c->L * c->Hkv * 2);
+    KVD_CUDA(cudaMemcpy(v.data(), c->seg_stats, v.size() * 8, cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < (size_t)c->L * c->Hkv; ++i) {
+        selected[i] = v[2 * i];
+        misses[i] = v[2 * i + 1];
+    }
+    return KVD_OK;
+}
+
+// Offline planner of 2D window scaling: greedy multiple-choice knapsack.
+// Every pair starts at its smallest size; the single upgrade (pair, larger size) with the highest
+// benefit gain per cost gain that fits the budget is applied until none fits (ties: lower pair,
+// then smaller size).
+kvd_status kvd_plan_window_scaling(const double* benefit, const double* cost, int32_t pairs, int32_t sizes,
+                                   double budget, int32_t* choice) {
+    if (!benefit || !cost || !choice || pairs < 1 || sizes < 1) return fail(KVD_EINVAL, "bad planner arguments");
+    double used = 0.0;
+    for (int32_t p = 0; p < pairs; ++p) {
+        choice[p] = 0;
+        used += cost[(size_t)p * sizes];
+    }
+    if (used > budget) return fail(KVD_EINVAL, "the smallest windows already exceed the budget");
+    while (true) {
+        int32_t bp = -1, bs = -1;
+        double best = 0.0;
+        for (int32_t p = 0; p < pairs; ++p) {
+            const double* bpair = benefit + (size_t)p * sizes;
+            const double* cpair = cost + (size_t)p * sizes;
+            for (int32_t s = choice[p] + 1; s < sizes; ++s) {
+                const double dc = cpair[s] - cpair[choice[p]], db = bpair[s] - bpair[choice[p]];
+                if (used + dc > budget || (db <= 0.0 && dc >= 0.0)) continue;
+                const double ratio = dc > 0.0 ? db / dc : (db > 0.0 ? INFINITY : 0.0);
+                if (bp < 0 || ratio > best) {
+                    bp = p;
+                    bs = s;
+                    best = ratio;
+                }
+            }
+        }
+        if (bp < 0) break;
+        used += cost[(size_t)bp * sizes + bs] - cost[(size_t)bp * sizes + choice[bp]];
+        choice[bp] = bs;
+    }
+    return KVD_OK;
+}
+
 kvd_status kvd_get_stats(kvd_cache* c, kvd_stats* out) {
     if (!c || !out) return fail(KVD_EINVAL, "NULL argument");
     KVD_CUDA(cudaDeviceSynchronize());
@@ -542,6 +685,7 @@ kvd_status kvd_reset_stats(kvd_cache* c) {
     if (!c) return fail(KVD_EINVAL, "cache is NULL");
     KVD_CUDA(cudaDeviceSynchronize());
     KVD_CUDA(cudaMemset(c->stats, 0, 64));
+    KVD_CUDA(cudaMemset(c->seg_stats, 0, (size_t)c->L * c->Hkv * 16));
     KVD_CUDA(cudaDeviceSynchronize());
     return KVD_OK;
 }
@@ -554,7 +698,8 @@ kvd_status kvd_check(kvd_cache* c) {
     if (e) {
         KVD_CUDA(cudaMemset(c->err, 0, 4));
         return fail(KVD_EDEVICE, "device flagged bad input (code %d: %s)", e,
-                    (e & 1) ? "selection not ascending / out of range / pinned" : "LFU key bounds exceeded");
+                    (e & 1) ? "selection not ascending / out of range / pinned"
+                    : (e & 2) ? "LFU key bounds exceeded" : "hierarchical index candidate bound violated");
     }
     return KVD_OK;
 }

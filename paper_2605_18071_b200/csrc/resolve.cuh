@@ -23,6 +23,8 @@ struct ResolveBufs {
     int64_t nkeys;          // victim-key slots in shared memory: C, or 0 for a fully resident cache
     unsigned long long* stats;
     int32_t* err;
+    const int32_t* cap;     // [L][Hkv] slots a segment may use (2D window scaling, R28), or NULL: C
+    unsigned long long* seg_stats;   // [L][Hkv][2] (selected, misses) per layer-head, or NULL
 };
 
 __device__ __forceinline__ uint64_t victim_key(int policy, uint32_t lu, uint8_t ph, uint32_t uc, int32_t blk,
@@ -75,6 +77,8 @@ __device__ inline int resolve_main(const StepParams& p, const ResolveBufs& rb, i
     uint32_t* lu = rb.last_use + seg * p.C;
     uint8_t* ph = rb.phase + seg * p.C;
     uint32_t* uc = rb.use_count + seg * p.C;
+    // 2D window scaling (R28): this layer-head pair's capacity; slots >= Ceff are never used
+    const int64_t Ceff = rb.cap ? (int64_t)rb.cap[p.layer * p.Hkv + h] : p.C;
     const float* sc = rb.scores + seg * p.nb_pad;
     const int32_t* S_in = ids + ((int64_t)bi * p.Hkv + h) * p.k;
     int32_t* attn = out_attn + ((int64_t)bi * p.Hkv + h) * (int64_t)p.W * 2;
@@ -129,9 +133,9 @@ __device__ inline int resolve_main(const StepParams& p, const ResolveBufs& rb, i
     // ---- 3. free slots, ascending: the first nm
     int nf = 0;
     if (nm > 0) {
-        for (int base = 0; base < p.C && nf < nm; base += blockDim.x) {
+        for (int base = 0; base < Ceff && nf < nm; base += blockDim.x) {
             const int64_t s = base + tid;
-            const int fr = (s < p.C && sb[s] < 0) ? 1 : 0;
+            const int fr = (s < Ceff && sb[s] < 0) ? 1 : 0;
             int tot;
             const int pos = block_exclusive_scan(fr, rsm.scan, &tot);
             if (fr && nf + pos < nm) dest[nf + pos] = (int32_t)s;
@@ -145,7 +149,7 @@ __device__ inline int resolve_main(const StepParams& p, const ResolveBufs& rb, i
         __syncthreads();
         for (int i = tid; i < k; i += blockDim.x) atomicOr(&inS[S[i] >> 5], 1u << (S[i] & 31));
         __syncthreads();
-        for (int64_t s = tid; s < p.C; s += blockDim.x) {
+        for (int64_t s = tid; s < Ceff; s += blockDim.x) {
             const int32_t blk = sb[s];
             uint64_t key = ~0ull;
             if (blk >= 0 && blk >= g.sink_end && blk < g.local_begin && !((inS[blk >> 5] >> (blk & 31)) & 1u))
@@ -159,7 +163,7 @@ __device__ inline int resolve_main(const StepParams& p, const ResolveBufs& rb, i
         for (int shift = 56; shift >= 0; shift -= 8) {
             for (int i = tid; i < 256; i += blockDim.x) rsm.hist[i] = 0;
             __syncthreads();
-            for (int64_t s = tid; s < p.C; s += blockDim.x) {
+            for (int64_t s = tid; s < Ceff; s += blockDim.x) {
                 const uint64_t key = keys[s];
                 if ((key & mask) == prefix) atomicAdd(&rsm.hist[(key >> shift) & 255], 1);
             }
@@ -199,9 +203,9 @@ __device__ inline int resolve_main(const StepParams& p, const ResolveBufs& rb, i
         const uint64_t T = prefix;
         // compact victims (key <= T) in slot order, then place them by key rank
         int nvc = 0;
-        for (int base = 0; base < p.C; base += blockDim.x) {
+        for (int base = 0; base < Ceff; base += blockDim.x) {
             const int64_t s = base + tid;
-            const int isv = (s < p.C && keys[s] <= T) ? 1 : 0;
+            const int isv = (s < Ceff && keys[s] <= T) ? 1 : 0;
             int tot;
             const int pos = block_exclusive_scan(isv, rsm.scan, &tot);
             if (isv && nvc + pos < nv) vtmp[nvc + pos] = (int32_t)s;
@@ -248,6 +252,11 @@ __device__ inline int resolve_main(const StepParams& p, const ResolveBufs& rb, i
         atomicAdd(&rb.stats[2], (unsigned long long)nm);
         atomicAdd(&rb.stats[3], (unsigned long long)pinned);
         atomicAdd(&rb.stats[4], (unsigned long long)nm * (unsigned long long)p.rec_bytes);
+        if (rb.seg_stats) {
+            unsigned long long* ss = rb.seg_stats + ((int64_t)p.layer * p.Hkv + h) * 2;
+            atomicAdd(&ss[0], (unsigned long long)k);
+            atomicAdd(&ss[1], (unsigned long long)nm);
+        }
     }
     __syncthreads();
     if (launch_dependents) griddep_launch();
@@ -272,6 +281,14 @@ __device__ inline int resolve_main(const StepParams& p, const ResolveBufs& rb, i
     return nm;
 }
 
+
+// Arguments of a select kernel that also resolves and fetches (kvd_select_resolve_fetch).
+struct FuseArgs {
+    ResolveBufs rb;
+    int32_t* out_attn;
+    const uint8_t* host_store;    // NULL: fully resident (no misses)
+    uint8_t* slots;
+};
 
 // (a4) inside a segment's CTA: all threads copy the nm missed 8 KiB records host -> slot.
 // The (record, 16-byte chunk) space is flattened and cut into nparts equal slices (one per CTA

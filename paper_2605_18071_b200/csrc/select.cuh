@@ -188,12 +188,6 @@ __device__ __forceinline__ void pick_digit(TopkShared& sm, int nbins, int kk, in
 // Fused variant (RESOLVE): after the selection, CTA rank 0 resolves the segment against the
 // cache (a3, resolve.cuh) and copies its misses from the host store (a4) in the same CTA,
 // reusing the dynamic shared memory: select -> resolve -> fetch without kernel boundaries.
-struct FuseArgs {
-    ResolveBufs rb;
-    int32_t* out_attn;
-    const uint8_t* host_store;    // NULL: fully resident (no misses)
-    uint8_t* slots;
-};
 
 template <int CL, int NT, int V, bool RESOLVE>
 __device__ __forceinline__ void select_body(const FuseArgs& fa, const StepParams& p, const uint16_t* __restrict__ q,
@@ -212,8 +206,23 @@ __device__ __forceinline__ void select_body(const FuseArgs& fa, const StepParams
     uint2* comp = reinterpret_cast<uint2*>(skey + span);
     uint8_t* sbin = reinterpret_cast<uint8_t*>(comp + kListCap);   // first-digit bin of every key
     const int64_t base = (int64_t)crank * span;
-    const SegGeom g = seg_geom(ntok[r], p.P, p.sink_tokens, p.local_tokens);   // ntok: setup only
     const int64_t seg = ((int64_t)p.layer * p.R + r) * p.Hkv + h;
+    // the launch's view: the segment's blocks (pinned excluded, k = p.k), or -- stage 1 of the
+    // hierarchical index (R27) -- its centroids (no pinned; K = min(nc, max(ceil(4k/ratio),
+    // k + pinned)), ids written with stride sel_stride)
+    SegGeom g = seg_geom(ntok[r], p.P, p.sink_tokens, p.local_tokens);   // ntok: setup only
+    int K = p.k, ostride = p.k;
+    if (p.sel_mode == 1) {
+        const int nc = p.sel_count[seg];
+        const int pin = g.sink_end + (g.nb - g.local_begin);
+        const int f = (kIdxFanout * p.k + p.sel_ratio - 1) / p.sel_ratio;
+        K = min(nc, max(f, p.k + pin));
+        ostride = p.sel_stride;
+        g.n = nc;
+        g.nb = nc;
+        g.sink_end = 0;
+        g.local_begin = nc;
+    }
     auto clampi = [](int64_t x, int64_t lo_, int64_t hi_) { return (int)(x < lo_ ? lo_ : x > hi_ ? hi_ : x); };
     const int nbv = clampi((int64_t)g.nb - base, 0, span);       // positions of this CTA holding a block
     const int c_lo = clampi(g.sink_end - base, 0, nbv);
@@ -315,7 +324,7 @@ __device__ __forceinline__ void select_body(const FuseArgs& fa, const StepParams
     }
     cta_minmax<CL>(kmn, kmx, sm);
     if (tid == 0) EXP_STAMP(p.exp_trace, ((bi * gridDim.y + h) * CL + crank), 2);
-    if (p.k == 0) {
+    if (K == 0) {
         // nothing to select (the scores are still kept: lookahead victims, kvd_read_scores).  The
         // cluster barrier ends the remote min/max reads and publishes the scores to rank 0.
         cl_sync<CL>();
@@ -333,7 +342,7 @@ __device__ __forceinline__ void select_body(const FuseArgs& fa, const StepParams
     // subtract, multiply by a positive scale and truncate never invert an order; equal scores
     // share a bin; NaN -> bin 0).  Float keys crowd a few leading bits, linear bins do not,
     // so plain shared atomics suffice.  Skipped (single "bin") for non-finite or equal ends.
-    int kk = p.k, cnt = ncand;                    // still to take / members of the threshold bin
+    int kk = K, cnt = ncand;                    // still to take / members of the threshold bin
     const float vmin = key_to_score(kmn), vmax = key_to_score(kmx);
     const bool lin = kmn <= kmx && isfinite(vmin) && isfinite(vmax) && vmax > vmin && isfinite(vmax - vmin) &&
                      kk != cnt && cnt > kTieList;
@@ -409,7 +418,7 @@ __device__ __forceinline__ void select_body(const FuseArgs& fa, const StepParams
         // every later branch reads the other ranks' shared memory under the same layout, so
         // "compacted" must be one decision for the whole cluster: all ranks' lists fit
         compacted = fit;
-        if (fit && tot_c <= kListCap && p.k <= kTakeMax) {   // uniform over the cluster
+        if (fit && tot_c <= kListCap && K <= kTakeMax) {   // uniform over the cluster
             if (crank == 0) {
                 int o = sm.ncomp;                 // rank 0's own entries stay (its base is 0)
                 for (int c = 1; c < CL; ++c) {
@@ -518,10 +527,10 @@ __device__ __forceinline__ void select_body(const FuseArgs& fa, const StepParams
         }
         return rank;
     };
-    int32_t* ids_out = out_ids + ((int64_t)bi * p.Hkv + h) * p.k;
-    float* sc_out = out_scores ? out_scores + ((int64_t)bi * p.Hkv + h) * p.k : nullptr;
+    int32_t* ids_out = out_ids + ((int64_t)bi * p.Hkv + h) * ostride;
+    float* sc_out = out_scores ? out_scores + ((int64_t)bi * p.Hkv + h) * ostride : nullptr;
     bool s_ready = false;                         // fused: S[] of the resolve already in smem
-    if (compacted && (mode != kModeEqual || local) && p.k <= kTakeMax) {
+    if (compacted && (mode != kModeEqual || local) && K <= kTakeMax) {
         // ---- emission from the compacted list: every taken id is in it (above the bin, or a
         // taken member); its output position = number of taken ids (cluster-wide) below it
         if (tid == 0) sm.ntake = 0;
@@ -549,7 +558,7 @@ __device__ __forceinline__ void select_body(const FuseArgs& fa, const StepParams
             if (take) sm.take[atomicAdd(&sm.ntake, 1)] = (int32_t)(gbase + i);
         }
         csync();
-        // gather the cluster's taken ids locally (p.k of them), then rank by id
+        // gather the cluster's taken ids locally (K of them), then rank by id
         int off = 0, tot = 0;
 #pragma unroll
         for (int c = 0; c < ncl; ++c) {
@@ -576,7 +585,7 @@ __device__ __forceinline__ void select_body(const FuseArgs& fa, const StepParams
             ids_out[pos] = id;
             if (sc_out) sc_out[pos] = __ldcg(sc + (id - base));
         }
-        if (RESOLVE && crank == 0 && 2 * (int)fa.rb.nkeys + p.k <= span) {
+        if (RESOLVE && crank == 0 && 2 * (int)fa.rb.nkeys + K <= span) {
             // hand the sorted selection to the resolve in shared memory (its S[] slot; the
             // keys are dead, `all` lies beyond it): no global re-read, no validation needed
             int32_t* S = reinterpret_cast<int32_t*>(skey) + 2 * fa.rb.nkeys;
@@ -714,8 +723,9 @@ __global__ void __launch_bounds__(NT, 1) select_kernel(FuseArgs fa, StepParams p
 }
 
 template <int CL, int NT, int V, bool RESOLVE>
-inline cudaError_t launch_select_k(kvd_cache* c, const StepParams& p, const uint16_t* q, int kpt, int32_t* out_ids,
-                                   float* out_scores, const FuseArgs& fa, cudaStream_t s) {
+inline cudaError_t launch_select_k(kvd_cache* c, const StepParams& p, const uint16_t* q, const uint16_t* mat,
+                                   float* scores, int kpt, int32_t* out_ids, float* out_scores, const FuseArgs& fa,
+                                   cudaStream_t s) {
     size_t smem = select_smem_bytes(NT, kpt);
     if (RESOLVE) smem = std::max(smem, resolve_smem_bytes(fa.rb.nkeys, c->kmax, c->nb_pad));
     // opt in to the largest dynamic size this instantiation has been launched with (per device
@@ -750,18 +760,19 @@ inline cudaError_t launch_select_k(kvd_cache* c, const StepParams& p, const uint
     cfg.attrs = attr;
     cfg.numAttrs = na;
     count_launch();
-    return cudaLaunchKernelEx(&cfg, select_kernel<CL, NT, V, RESOLVE>, fa, p, q, (const uint16_t*)c->summ, c->scores,
+    return cudaLaunchKernelEx(&cfg, select_kernel<CL, NT, V, RESOLVE>, fa, p, q, mat, scores,
                               (const int32_t*)c->ntok_dev, kpt, out_ids, out_scores);
 }
 
 template <int NT, bool RESOLVE>
-cudaError_t launch_select_nt(kvd_cache* c, const StepParams& p, const uint16_t* q, int cl, int kpt, int v,
-                                    int32_t* out_ids, float* out_scores, const FuseArgs& fa, cudaStream_t s) {
+cudaError_t launch_select_nt(kvd_cache* c, const StepParams& p, const uint16_t* q, const uint16_t* mat, float* scores,
+                             int cl, int kpt, int v, int32_t* out_ids, float* out_scores, const FuseArgs& fa,
+                             cudaStream_t s) {
 #define KVD_SEL_CASE(CLV)                                                                                       \
     case CLV:                                                                                                   \
-        return v == 8 ? launch_select_k<CLV, NT, 8, RESOLVE>(c, p, q, kpt, out_ids, out_scores, fa, s)           \
-             : v == 4 ? launch_select_k<CLV, NT, 4, RESOLVE>(c, p, q, kpt, out_ids, out_scores, fa, s)           \
-                      : launch_select_k<CLV, NT, 2, RESOLVE>(c, p, q, kpt, out_ids, out_scores, fa, s);
+        return v == 8 ? launch_select_k<CLV, NT, 8, RESOLVE>(c, p, q, mat, scores, kpt, out_ids, out_scores, fa, s)           \
+             : v == 4 ? launch_select_k<CLV, NT, 4, RESOLVE>(c, p, q, mat, scores, kpt, out_ids, out_scores, fa, s)           \
+                      : launch_select_k<CLV, NT, 2, RESOLVE>(c, p, q, mat, scores, kpt, out_ids, out_scores, fa, s);
     switch (cl) {
         KVD_SEL_CASE(1)
         KVD_SEL_CASE(2)
@@ -773,13 +784,13 @@ cudaError_t launch_select_nt(kvd_cache* c, const StepParams& p, const uint16_t* 
 }
 
 // explicit instantiations: k_select_nt512.cu, k_select_nt1024.cu (compiled in parallel)
-extern template cudaError_t launch_select_nt<512, false>(kvd_cache*, const StepParams&, const uint16_t*, int, int, int,
-                                                         int32_t*, float*, const FuseArgs&, cudaStream_t);
-extern template cudaError_t launch_select_nt<512, true>(kvd_cache*, const StepParams&, const uint16_t*, int, int, int,
-                                                        int32_t*, float*, const FuseArgs&, cudaStream_t);
-extern template cudaError_t launch_select_nt<1024, false>(kvd_cache*, const StepParams&, const uint16_t*, int, int, int,
-                                                          int32_t*, float*, const FuseArgs&, cudaStream_t);
-extern template cudaError_t launch_select_nt<1024, true>(kvd_cache*, const StepParams&, const uint16_t*, int, int, int,
-                                                         int32_t*, float*, const FuseArgs&, cudaStream_t);
+extern template cudaError_t launch_select_nt<512, false>(kvd_cache*, const StepParams&, const uint16_t*, const uint16_t*,
+    float*, int, int, int, int32_t*, float*, const FuseArgs&, cudaStream_t);
+extern template cudaError_t launch_select_nt<512, true>(kvd_cache*, const StepParams&, const uint16_t*, const uint16_t*,
+    float*, int, int, int, int32_t*, float*, const FuseArgs&, cudaStream_t);
+extern template cudaError_t launch_select_nt<1024, false>(kvd_cache*, const StepParams&, const uint16_t*, const uint16_t*,
+    float*, int, int, int, int32_t*, float*, const FuseArgs&, cudaStream_t);
+extern template cudaError_t launch_select_nt<1024, true>(kvd_cache*, const StepParams&, const uint16_t*, const uint16_t*,
+    float*, int, int, int, int32_t*, float*, const FuseArgs&, cudaStream_t);
 
 }  // namespace kvd

@@ -33,7 +33,7 @@ class Config(ctypes.Structure):
                 ("max_context", ctypes.c_int64), ("slots_per_segment", ctypes.c_int64),
                 ("max_select", ctypes.c_int32), ("sink_tokens", ctypes.c_int32),
                 ("local_tokens", ctypes.c_int32), ("policy", ctypes.c_int32),
-                ("host_layer_alias", ctypes.c_int32), ("device", ctypes.c_int32)]
+                ("host_layer_alias", ctypes.c_int32), ("device", ctypes.c_int32), ("index_ratio", ctypes.c_int32)]
 
 
 class Stats(ctypes.Structure):
@@ -57,7 +57,8 @@ EXPORTS = ["kvd_required_bytes", "kvd_create_cache", "kvd_destroy_cache", "kvd_g
            "kvd_read_scores", "kvd_get_stats", "kvd_reset_stats", "kvd_check", "kvd_last_error",
            "kvd_version", "kvd_set_device_step", "kvd_launch_count",
            "kvd_select_resolve_fetch", "kvd_enable_kernel_timer", "kvd_read_kernel_timer",
-           "kvd_probe_zero_copy"]
+           "kvd_probe_zero_copy", "kvd_read_index", "kvd_set_segment_capacity", "kvd_get_segment_stats",
+           "kvd_plan_window_scaling"]
 
 
 def lib():
@@ -94,6 +95,10 @@ def lib():
             "kvd_enable_kernel_timer": ([p, i32], i32),
             "kvd_read_kernel_timer": ([p, p, p], i32),
             "kvd_probe_zero_copy": ([p, p, ctypes.c_size_t, i32, p], i32),
+            "kvd_read_index": ([p, i32, i32, i32, p, p, p], i32),
+            "kvd_set_segment_capacity": ([p, i32, i32, i64], i32),
+            "kvd_get_segment_stats": ([p, p, p], i32),
+            "kvd_plan_window_scaling": ([p, p, i32, i32, ctypes.c_double, p], i32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -137,10 +142,12 @@ class KVCache:
 
     def __init__(self, *, num_layers, num_q_heads, num_kv_heads, block_tokens, max_requests, max_context,
                  slots_per_segment, max_select, sink_tokens=4, local_tokens=64, policy="lru",
-                 host_layer_alias=0, device=0, head_dim=128):
+                 host_layer_alias=0, device=0, head_dim=128, index_ratio=0):
         self.cfg = Config(num_layers, num_q_heads, num_kv_heads, head_dim, block_tokens, max_requests,
                           max_context, slots_per_segment, max_select, sink_tokens, local_tokens,
-                          POLICY[policy] if isinstance(policy, str) else int(policy), host_layer_alias, device)
+                          POLICY[policy] if isinstance(policy, str) else int(policy), host_layer_alias, device,
+                          index_ratio)
+        self.index_ratio = index_ratio
         h = ctypes.c_void_p()
         _check(lib().kvd_create_cache(ctypes.byref(self.cfg), ctypes.byref(h)))
         self.h = h
@@ -157,7 +164,8 @@ class KVCache:
         cfg = Config(kw["num_layers"], kw["num_q_heads"], kw["num_kv_heads"], kw.get("head_dim", 128),
                      kw["block_tokens"], kw["max_requests"], kw["max_context"], kw["slots_per_segment"],
                      kw["max_select"], kw.get("sink_tokens", 4), kw.get("local_tokens", 64),
-                     POLICY[kw.get("policy", "lru")], kw.get("host_layer_alias", 0), kw.get("device", 0))
+                     POLICY[kw.get("policy", "lru")], kw.get("host_layer_alias", 0), kw.get("device", 0),
+                     kw.get("index_ratio", 0))
         d, hb = ctypes.c_size_t(), ctypes.c_size_t()
         _check(lib().kvd_required_bytes(ctypes.byref(cfg), ctypes.byref(d), ctypes.byref(hb)))
         return d.value, hb.value
@@ -232,6 +240,15 @@ class KVCache:
         _check(lib().kvd_read_summaries(self.h, layer, req, head, ptr(out)))
         return out
 
+    def read_index(self, layer, req, head, nb):
+        """(centroids [nc][128] uint16, cent_of [nb] int32) of a segment's hierarchical index."""
+        nc = ctypes.c_int64()
+        _check(lib().kvd_read_index(self.h, layer, req, head, ctypes.byref(nc), None, None))
+        cent = np.empty((max(nc.value, 1), 128), np.uint16)
+        cof = np.empty(max(nb, 1), np.int32)
+        _check(lib().kvd_read_index(self.h, layer, req, head, ctypes.byref(nc), ptr(cent), ptr(cof)))
+        return cent[:nc.value], cof[:nb]
+
     def read_scores(self, layer, req, head, nb):
         out = np.empty(nb, np.float32)
         _check(lib().kvd_read_scores(self.h, layer, req, head, ptr(out)))
@@ -248,6 +265,18 @@ class KVCache:
     def check(self):
         _check(lib().kvd_check(self.h))
 
+    def set_segment_capacity(self, layer, head, slots):
+        """2D window scaling: slots the layer-head pair may use (kvd_set_segment_capacity)."""
+        _check(lib().kvd_set_segment_capacity(self.h, layer, head, slots))
+
+    def segment_stats(self):
+        """(selected [L][Hkv], misses [L][Hkv]) since reset_stats."""
+        L, H = self.cfg.num_layers, self.cfg.num_kv_heads
+        sel = np.zeros((L, H), np.uint64)
+        mis = np.zeros((L, H), np.uint64)
+        _check(lib().kvd_get_segment_stats(self.h, ptr(sel), ptr(mis)))
+        return sel, mis
+
     KERNEL_KINDS = ("select", "resolve", "gather", "attn")
 
     def enable_kernel_timer(self, enable=True):
@@ -260,6 +289,16 @@ class KVCache:
         n = np.zeros(4, np.uint64)
         _check(lib().kvd_read_kernel_timer(self.h, ptr(ns), ptr(n)))
         return {k: (int(ns[i]), int(n[i])) for i, k in enumerate(self.KERNEL_KINDS)}
+
+
+def plan_window_scaling(benefit, cost, budget):
+    """Greedy MCKP planner of 2D window scaling (kvd_plan_window_scaling): choice [pairs]."""
+    b = np.ascontiguousarray(np.asarray(benefit, np.float64))
+    c = np.ascontiguousarray(np.asarray(cost, np.float64))
+    pairs, sizes = b.shape
+    choice = np.empty(pairs, np.int32)
+    _check(lib().kvd_plan_window_scaling(ptr(b), ptr(c), pairs, sizes, float(budget), ptr(choice)))
+    return choice
 
 
 def probe_zero_copy(host, dev, nbytes, ctas, stream=None):

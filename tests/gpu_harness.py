@@ -27,8 +27,9 @@ def row_normwise_err(o, ref):
 class Case:
     def __init__(self, *, L=1, B=1, Hq=8, Hkv=2, n=4096, P=16, k=32, C=None, policy="lru", seed=0,
                  alpha=0.9, ragged=False, sink=4, local=64, alias=0, reqs=None, R=None, device=0,
-                 fused=False):
+                 fused=False, index_ratio=0, caps=None):
         self.fused = fused            # kvd_select_resolve_fetch instead of select_topk + resolve_and_fetch
+        self.index_ratio = index_ratio  # hierarchical centroid index (R27); 0 = flat
         self.L, self.B, self.Hq, self.Hkv, self.P, self.k = L, B, Hq, Hkv, P, k
         self.G = Hq // Hkv
         self.policy, self.pol = policy, oracle.POLICIES[policy]
@@ -41,12 +42,17 @@ class Case:
         self.alias = alias
         self.cache = KVCache(num_layers=L, num_q_heads=Hq, num_kv_heads=Hkv, block_tokens=P, max_requests=R,
                              max_context=n, slots_per_segment=self.C, max_select=k, sink_tokens=sink,
-                             local_tokens=local, policy=policy, host_layer_alias=alias, device=device)
+                             local_tokens=local, policy=policy, host_layer_alias=alias, device=device,
+                             index_ratio=index_ratio)
         self.W = self.cache.attn_width(k)
+        self.caps = dict(caps or {})              # 2D window scaling: (layer, head) -> slots (R28)
+        for (l, h), cap in self.caps.items():
+            self.cache.set_segment_capacity(l, h, cap)
         self.dev = torch.device("cuda", device)
         self.kv = {}
         self.oc = {}
         self.S = {}
+        self.index = {}
         for l in range(L):
             for r in self.reqs:
                 src_l = l % alias if alias else l
@@ -55,8 +61,11 @@ class Case:
                 for h in range(Hkv):
                     self.kv[(l, r, h)] = (K[h], V[h])
                     self.S[(l, r, h)] = oracle.block_summaries(K[h], P)
+                    if index_ratio:
+                        cent, cent_of = oracle.index_build(self.S[(l, r, h)], index_ratio)
+                        self.index[(l, r, h)] = (cent, cent_of, index_ratio)
                     pinned = oracle.pinned_blocks(self.n[r], P, sink, local)
-                    self.oc[(l, r, h)] = oracle.SegmentCache(len(pinned), self.C, pinned)
+                    self.oc[(l, r, h)] = oracle.SegmentCache(len(pinned), self.caps.get((l, h), self.C), pinned)
         self.ids = torch.empty((B, Hkv, max(k, 1)), dtype=torch.int32, device=self.dev)
         self.sel_scores = torch.empty((B, Hkv, max(k, 1)), dtype=torch.float32, device=self.dev)
         self.attn = torch.empty((B, Hkv, self.W, 2), dtype=torch.int32, device=self.dev)
@@ -89,7 +98,8 @@ class Case:
                 K, V = self.kv[(l, r, h)]
                 qg = q_np[bi, h * self.G:(h + 1) * self.G]
                 res[(bi, h)] = oracle.segment_step(self.oc[(l, r, h)], qg, self.S[(l, r, h)], K, V, self.P,
-                                                   self.k, step, self.pol, self.W)
+                                                   self.k, step, self.pol, self.W,
+                                                   index=self.index.get((l, r, h)))
         return res
 
     def compare_layer(self, l, g, o, check_state=True, check_slots=False):
@@ -100,22 +110,25 @@ class Case:
                 ref = o[(bi, h)]
                 nb = len(ref["scores"])
                 assert np.array_equal(g["ids"][bi, h], ref["ids"]), (l, r, h, "ids")
-                sc = self.cache.read_scores(l, r, h, nb)
-                assert np.array_equal(sc.view(np.uint32), ref["scores"].view(np.uint32)) or \
-                    np.array_equal(sc, ref["scores"]), (l, r, h, "scores")
-                assert np.array_equal(g["sel_scores"][bi, h], ref["scores"][ref["ids"]]), (l, r, h, "sel scores")
+                if not self.index_ratio or self.policy == "la":   # index mode keeps lookahead scores only
+                    sc = self.cache.read_scores(l, r, h, nb)
+                    assert np.array_equal(sc.view(np.uint32), ref["scores"].view(np.uint32)) or \
+                        np.array_equal(sc, ref["scores"]), (l, r, h, "scores")
+                    assert np.array_equal(g["sel_scores"][bi, h], ref["scores"][ref["ids"]]), (l, r, h, "sel scores")
                 assert np.array_equal(g["attn"][bi, h], ref["attn"]), (l, r, h, "attention list")
                 if check_state:
                     st = self.cache.read_segment(l, r, h)
                     oc = self.oc[(l, r, h)]
                     assert np.array_equal(st["table"][:nb], oc.table), (l, r, h, "table")
-                    assert np.array_equal(st["slot_block"], oc.slot_block), (l, r, h, "slot map")
+                    Cs = len(oc.slot_block)                  # the segment's window (2D scaling)
+                    assert np.array_equal(st["slot_block"][:Cs], oc.slot_block), (l, r, h, "slot map")
+                    assert (st["slot_block"][Cs:] == -1).all(), (l, r, h, "slots beyond the window")
                     pin = oc.is_pinned
                     occ = (oc.slot_block >= 0)
                     occ &= ~pin[np.maximum(oc.slot_block, 0)].astype(bool)
-                    assert np.array_equal(st["last_use"][occ], oc.last_use[occ]), (l, r, h, "last_use")
-                    assert np.array_equal(st["phase"][occ], oc.phase[occ]), (l, r, h, "phase")
-                    assert np.array_equal(st["use_count"][occ], oc.use_count[occ]), (l, r, h, "use_count")
+                    assert np.array_equal(st["last_use"][:Cs][occ], oc.last_use[occ]), (l, r, h, "last_use")
+                    assert np.array_equal(st["phase"][:Cs][occ], oc.phase[occ]), (l, r, h, "phase")
+                    assert np.array_equal(st["use_count"][:Cs][occ], oc.use_count[occ]), (l, r, h, "use_count")
                 if check_slots:
                     self.check_slot_bytes(l, r, h)
                 G = self.G
@@ -124,6 +137,14 @@ class Case:
                 assert e <= ATTN_TOL, (l, r, h, "attention err", e)
                 assert np.max(np.abs(g["lse"][bi, h * G:(h + 1) * G] - ref["lse"])) <= LSE_TOL, (l, r, h, "lse")
         return worst
+
+    def check_index(self):
+        """O9 parity: every segment's centroids (bf16 bits) and block -> centroid map bit-exact."""
+        for (l, r, h), (cent, cent_of, _) in self.index.items():
+            gc, gof = self.cache.read_index(l, r, h, len(cent_of))
+            assert gc.shape == cent.shape, (l, r, h, gc.shape, cent.shape)
+            assert np.array_equal(gc, cent), (l, r, h, "centroids")
+            assert np.array_equal(gof, cent_of), (l, r, h, "cent_of")
 
     def check_slot_bytes(self, l, r, h):
         """O7 invariant: every occupied slot holds exactly its block's K/V (from the generator)."""

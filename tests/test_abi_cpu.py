@@ -1,6 +1,8 @@
 """CPU-side checks of the boundary: libkvd.so loads without a GPU, exports every
 symbol include/kvd.h declares, and validates configurations synchronously."""
 import ctypes
+
+import numpy as np
 import os
 import re
 
@@ -103,3 +105,22 @@ def test_step_calls_validate_before_launch():
     assert L.kvd_sparse_decode(None, 0, q, reqs, 1, q, 13, q, q, q) == 1
     assert L.kvd_launch_count() == n0
     assert b"NULL" in L.kvd_last_error() or b"null" in L.kvd_last_error()
+
+
+def test_window_scaling_planner_matches_oracle_greedy():
+    # the product's offline MCKP planner (host code in libkvd) against the oracle's greedy (O11,
+    # itself pinned by exhaustive search), on random profile-like instances
+    import oracle
+    from paper_2605_18071_b200 import kvd
+    rng = np.random.default_rng(7)
+    for _ in range(50):
+        pairs, sizes = int(rng.integers(1, 64)), int(rng.integers(2, 6))
+        step = rng.integers(1, 6, size=(pairs, 1)).astype(np.float64)
+        cost = step * np.arange(1, sizes + 1)[None, :]
+        gains = -np.sort(-rng.random((pairs, sizes - 1)), axis=1) * rng.random((pairs, 1)) * 10
+        benefit = np.concatenate([np.zeros((pairs, 1)), np.cumsum(gains, axis=1)], axis=1)
+        budget = cost[:, 0].sum() + rng.random() * (cost[:, -1].sum() - cost[:, 0].sum())
+        _, ref = oracle.mckp(benefit, cost, budget)
+        assert np.array_equal(kvd.plan_window_scaling(benefit, cost, budget), ref)
+    with pytest.raises(kvd.KVDError):
+        kvd.plan_window_scaling(np.zeros((2, 2)), np.ones((2, 2)), 1.0)

@@ -42,6 +42,10 @@ class OracleSegment:
         nb = (n + P - 1) // P
         C = cfg["C"] if cfg["C"] is not None else nb
         self.oc = oracle.SegmentCache(nb, C, pinned)
+        self.index = None
+        if cfg.get("index"):
+            cent, cent_of = oracle.index_build(self.S, cfg["index"])
+            self.index = (cent, cent_of, cfg["index"])
         self.R, self.cfg, self.G = R, cfg, cfg["Hq"] // cfg["Hkv"]
         self.pol = oracle.POLICIES[args.policy]
 
@@ -50,7 +54,7 @@ class OracleSegment:
         G, h = self.G, self.h
         q = self.R.q_host[t_row, self.l, self.b].numpy().view(np.uint16)[h * G:(h + 1) * G]
         return oracle.segment_step(self.oc, q, self.S, self.K, self.V, self.cfg["P"], self.cfg["k"], t_row + 1,
-                                   self.pol, self.R.W)
+                                   self.pol, self.R.W, index=self.index)
 
     def compare(self, ref):
         R, l, b, h, G = self.R, self.l, self.b, self.h, self.G
@@ -146,4 +150,14 @@ def test_c4k_fullsize_1m_context_k1024():
     # c4 with k = 1024 blocks (1.56 % of 1M): 1029-entry attention lists, 32 pieces per segment
     R, cfg, args = make_runner("c4k", 1, ["--fill", "3"])
     samples = [OracleSegment(R, cfg, args, 0, b, h) for (b, h) in [(1, 2)]]
+    run_checked(R, samples, n_eager=3, n_graph=2)
+
+
+def test_c4h_fullsize_hierarchical_index():
+    # c4 with the hierarchical centroid index: 65536 blocks -> 16384 centroids per segment
+    R, cfg, args = make_runner("c4h", 1, ["--fill", "3"])
+    samples = [OracleSegment(R, cfg, args, 0, b, h) for (b, h) in [(0, 1), (2, 3)]]
+    for o in samples:                                          # index build bit-exact
+        gc, gof = R.cache.read_index(0, o.b, o.h, len(o.index[1]))
+        assert np.array_equal(gc, o.index[0]) and np.array_equal(gof, o.index[1])
     run_checked(R, samples, n_eager=3, n_graph=2)

@@ -242,3 +242,53 @@ def test_attention_bitwise_independent_of_batch(fused):
         assert np.array_equal(ga["ids"][0], gb["ids"][5])
         assert np.array_equal(ga["out"][0].view(np.uint32), gb["out"][5].view(np.uint32))
         assert np.array_equal(ga["lse"][0].view(np.uint32), gb["lse"][5].view(np.uint32))
+
+
+# ---- the hierarchical centroid index (R27; k_index.cu): the k-means build bit-exact against the
+# oracle's O9 (centroid bf16 bits, block -> centroid), then select / resolve / attention as usual
+@pytest.mark.parametrize("ratio,policy,fused", [(4, "la", False), (4, "la", True), (2, "lru", True),
+                                                (8, "lfu", False), (1, "la", True)])
+def test_hierarchical_index_parity(ratio, policy, fused):
+    c = Case(L=1, B=2, Hq=8, Hkv=2, n=20000, P=16, k=32, C=200, policy=policy, seed=51, ragged=True,
+             fused=fused, index_ratio=ratio)
+    c.check_index()
+    c.run(steps=4, check_slots_every=2)
+
+
+def test_hierarchical_index_full_context_cluster_stage1():
+    # a 1M-token segment (65536 blocks, 16384 centroids): stage 1 on an 8-CTA cluster, k = 128
+    c = Case(L=1, B=1, Hq=14, Hkv=2, n=1 << 20, P=16, k=128, C=4096, policy="la", seed=52, fused=True,
+             index_ratio=4)
+    c.check_index()
+    c.run(steps=2)
+
+
+# ---- 2D layer-head window scaling (R28): heterogeneous per layer-head capacities; slot maps
+# bit-exact against oracle caches of those capacities, nothing ever placed beyond a window
+@pytest.mark.parametrize("policy,fused", [("la", True), ("lru", False), ("lfu", True)])
+def test_window_scaling_heterogeneous_capacities(policy, fused):
+    caps = {(0, 0): 40, (0, 1): 90, (1, 0): 160, (1, 1): 45}
+    c = Case(L=2, B=2, Hq=8, Hkv=2, n=6000, P=16, k=32, C=160, policy=policy, seed=61, ragged=True,
+             fused=fused, caps=caps)
+    c.run(steps=10, check_slots_every=3)
+    sel, mis = c.cache.segment_stats()
+    assert sel.sum() == c.cache.stats()["selected"] and mis.sum() == c.cache.stats()["misses"]
+    assert mis[0, 0] > mis[1, 0]                  # the small window misses more
+
+
+def test_window_scaling_shrink_and_errors():
+    c = Case(L=1, B=1, Hq=8, Hkv=2, n=4096, P=16, k=32, C=120, policy="la", seed=62)
+    c.run(steps=4)
+    c.cache.set_segment_capacity(0, 1, 50)        # shrink: residents of slots >= 50 are dropped
+    st = c.cache.read_segment(0, 0, 1)
+    assert (st["slot_block"][50:] == -1).all()
+    assert all(st["table"][b] < 50 for b in np.nonzero(st["table"] >= 0)[0])
+    with pytest.raises(KVDError) as e:
+        c.cache.set_segment_capacity(0, 0, 3)     # below the pinned blocks
+    assert e.value.status == "KVD_EINVAL"
+    c.cache.set_segment_capacity(0, 0, 36)        # 32 + 5 pinned do not fit in 36
+    q = torch.zeros((1, 8, 128), dtype=torch.int16, device="cuda")
+    ids = torch.zeros((1, 2, 32), dtype=torch.int32, device="cuda")
+    with pytest.raises(KVDError) as e:
+        c.cache.select_topk(0, q, [0], 32, ids)
+    assert e.value.status == "KVD_ECAPACITY"
