@@ -87,6 +87,7 @@ struct kvd_cache {
     int32_t* memb = nullptr;               // [L][R][Hkv][nb_pad] blocks ordered by (centroid, block)
     int32_t* moff = nullptr;               // [L][R][Hkv][nc_pad + 1] member offsets
     int32_t* csel = nullptr;               // [R][Hkv][m_max] stage-1 selection (scratch)
+    uint32_t* cand_bits = nullptr;         // [L][R][Hkv][nb_pad / 32] last step's stage-2 candidates
     uint8_t* idx_stage = nullptr;          // setup scratch of the index build
     // 2D window scaling (R28): per layer-head capacity; per layer-head selection / miss counters
     std::vector<int64_t> cap_host;         // [L][Hkv]

@@ -197,14 +197,15 @@ size_t index_stage_bytes(int Hkv, int64_t nb_pad) {
 }
 
 // ---------------------------------------------------------------- select stage 2 (O10)
-constexpr int kCandThreads = 512;
+constexpr int kCandThreads = 1024;
 
 struct CandArgs {
     FuseArgs fa;                    // fused resolve + fetch (fa.out_attn == NULL: select only)
     const uint16_t* summ;
-    float* scores;                  // lookahead scores [seg][nb_pad] (written for the LA policy)
+    float* scores;                  // [seg][nb_pad]: exact scores of this step's candidates
+    uint32_t* cand_bits;            // [seg][nb_pad / 32]: this step's candidates (lookahead victims)
     const float* cscores;           // [seg][nc_pad]
-    const int32_t* csel;            // [B][Hkv][m_max] stage-1 centroids
+    const int32_t* csel;            // [R][Hkv][m_max] stage-1 centroids
     const int32_t* ncent;
     const int32_t* cent_of;
     const int32_t* memb;
@@ -239,8 +240,10 @@ __global__ void __launch_bounds__(kCandThreads, 1) cand_kernel(CandArgs ca, Step
     uint32_t* keys = reinterpret_cast<uint32_t*>(cand + kCandCap);
     if (RESOLVE) resolve_pre(p, ca.fa.rb, bi, h, rsm);
     for (int w = tid; w < nwords; w += kCandThreads) bits[w] = 0u;
+    if (tid == 0) EXP_STAMP(p.exp_trace, 8192 + bi * p.Hkv + h, 0);
     griddep_wait();                               // stage-1 selection and scores; q
     if (tid == 0) kt_begin(p.kt_slots, p.kt_base + kKtSelect);
+    if (tid == 0) EXP_STAMP(p.exp_trace, 8192 + bi * p.Hkv + h, 1);
     if (tid < kHeadDim) {
         const uint16_t* qh = q + ((int64_t)bi * p.Hq + (int64_t)h * p.G) * kHeadDim;
         float a = 0.0f;
@@ -251,14 +254,16 @@ __global__ void __launch_bounds__(kCandThreads, 1) cand_kernel(CandArgs ca, Step
     const int pin = g.sink_end + (g.nb - g.local_begin);
     const int m = min(nc, max((kIdxFanout * p.k + ca.ratio - 1) / ca.ratio, p.k + pin));
     __syncthreads();
-    // ---- candidates: non-pinned members of the m chosen centroids (a warp per centroid)
-    const int32_t* sel = ca.csel + ((int64_t)bi * p.Hkv + h) * ca.m_max;
+    // ---- candidates: non-pinned members of the m chosen centroids.  Thread i < m owns chosen
+    // centroid i: one round trip for the ids, one for the member ranges, then its members
+    // (contiguous in memb, independent loads) are marked in the bitmap.
+    const int32_t* sel = ca.csel + ((int64_t)r * p.Hkv + h) * ca.m_max;   // per request id (see select.cuh)
     const int32_t* moff = ca.moff + seg * (ca.nc_pad + 1);
     const int32_t* memb = ca.memb + seg * p.nb_pad;
-    for (int i = warp; i < m; i += kCandThreads / 32) {
-        const int cidx = __ldcg(&sel[i]);
+    if (tid < m) {
+        const int cidx = __ldcg(&sel[tid]);
         const int a = moff[cidx], e = moff[cidx + 1];
-        for (int x = a + lane; x < e; x += 32) {
+        for (int x = a; x < e; ++x) {
             const int b = memb[x];
             if (b >= g.sink_end && b < g.local_begin) atomicOr(&bits[b >> 5], 1u << (b & 31));
         }
@@ -284,14 +289,13 @@ __global__ void __launch_bounds__(kCandThreads, 1) cand_kernel(CandArgs ca, Step
         if (tid == 0) atomicOr(ca.fa.rb.err, 4);
         ncand = min(ncand, kCandCap);
     }
-    // ---- lookahead scores: every block its centroid's score, candidates their exact score
+    if (tid == 0) EXP_STAMP(p.exp_trace, 8192 + bi * p.Hkv + h, 2);
+    // ---- this step's candidate set, for the lookahead victim keys (resolve.cuh)
+    uint32_t* gbits = ca.cand_bits + seg * (p.nb_pad >> 5);
+    for (int w = tid; w < nwords; w += kCandThreads) gbits[w] = bits[w];
     float* sc = ca.scores + seg * p.nb_pad;
-    if (p.policy == KVD_POLICY_LOOKAHEAD) {
-        const int32_t* cof = ca.cent_of + seg * p.nb_pad;
-        const float* cs = ca.cscores + seg * ca.nc_pad;
-        for (int b = tid; b < nb; b += kCandThreads) sc[b] = __ldcg(&cs[cof[b]]);
-    }
     __syncthreads();
+    if (tid == 0) EXP_STAMP(p.exp_trace, 8192 + bi * p.Hkv + h, 3);
     // ---- exact scores of the candidates (fp32 FMA chain over j = 0..127, R5)
     const uint16_t* sseg = ca.summ + seg * kHeadDim * p.nb_pad;
     for (int c0 = 0; c0 < ncand; c0 += kCandThreads) {
@@ -313,6 +317,7 @@ __global__ void __launch_bounds__(kCandThreads, 1) cand_kernel(CandArgs ca, Step
         }
     }
     __syncthreads();
+    if (tid == 0) EXP_STAMP(p.exp_trace, 8192 + bi * p.Hkv + h, 4);
     // ---- top k of the candidates: 8-bit radix select of the k-th largest key T, then every key
     // above T and the first (k - #above) keys equal to T in candidate (= block) order
     uint32_t prefix = 0u, mask = 0u;
@@ -359,6 +364,7 @@ __global__ void __launch_bounds__(kCandThreads, 1) cand_kernel(CandArgs ca, Step
         __syncthreads();
     }
     const uint32_t T = prefix;                    // the k-th largest key; kk of the keys == T taken
+    if (tid == 0) EXP_STAMP(p.exp_trace, 8192 + bi * p.Hkv + h, 5);
     int32_t* ids_out = out_ids + ((int64_t)bi * p.Hkv + h) * p.k;
     float* sc_out = out_scores ? out_scores + ((int64_t)bi * p.Hkv + h) * p.k : nullptr;
     int taken = 0, eqs = 0;
@@ -378,6 +384,7 @@ __global__ void __launch_bounds__(kCandThreads, 1) cand_kernel(CandArgs ca, Step
         taken += tot;
         eqs += tot_eq;
     }
+    if (tid == 0) EXP_STAMP(p.exp_trace, 8192 + bi * p.Hkv + h, 6);
     if constexpr (RESOLVE) {
         __syncthreads();                          // ids written (read back by the resolve, L2)
         uint8_t* smraw = reinterpret_cast<uint8_t*>(bits);
@@ -389,6 +396,10 @@ __global__ void __launch_bounds__(kCandThreads, 1) cand_kernel(CandArgs ca, Step
     } else {
         griddep_launch();
     }
+#ifdef KVD_EXPERIMENTS
+    __syncthreads();
+    if (tid == 0) EXP_STAMP(p.exp_trace, 8192 + bi * p.Hkv + h, 7);
+#endif
     if (p.kt_slots) {
         __syncthreads();
         if (tid == 0) kt_end(p.kt_slots, p.kt_acc, p.kt_base + kKtSelect, kKtSelect, (unsigned long long)gridDim.x * gridDim.y);
@@ -415,6 +426,7 @@ cudaError_t launch_index_select(kvd_cache* c, const StepParams& p, const uint16_
     ca.fa.slots = c->slots;
     ca.summ = c->summ;
     ca.scores = c->scores;
+    ca.cand_bits = c->cand_bits;
     ca.cscores = c->cscores;
     ca.csel = c->csel;
     ca.ncent = c->ncent;

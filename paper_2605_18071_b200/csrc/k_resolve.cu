@@ -138,6 +138,10 @@ ResolveBufs resolve_bufs(kvd_cache* c) {
                    c->ntok_dev, c->miss,       c->miss_count, c->kmax, 0,           c->stats,    c->err};
     rb.nkeys = c->resident ? 0 : c->C;            // a fully resident cache never evicts
     rb.cap = c->cap_dev;
+    rb.cbits = c->cand_bits;                      // NULL unless the hierarchical index is on
+    rb.cent_of = c->cent_of;
+    rb.cscores = c->cscores;
+    rb.nc_pad = c->nc_pad;
     rb.seg_stats = c->seg_stats;
     return rb;
 }

@@ -117,6 +117,7 @@ kvd_status check_config(const kvd_config* cfg, Geometry* g) {
             return fail(KVD_EINVAL, "hierarchical index: max_select=%d with index_ratio=%d may give %lld candidates "
                         "(> %d)", g->kmax, g->ratio, (long long)std::min<int64_t>(g->nb_max, (int64_t)kIdxWindow * g->m_max),
                         kCandCap);
+        if (g->m_max > 1024) return fail(KVD_EINVAL, "hierarchical index: %d stage-1 centroids > 1024", g->m_max);
         if (cand_smem_bytes(g->nb_pad) + 4096 > kMaxSmemBytes)
             return fail(KVD_EINVAL, "hierarchical index: context too long for the candidate kernel");
     }
@@ -145,7 +146,7 @@ Sizes sizes_of(const Geometry& g) {
     s.index = 0;
     if (g.ratio > 0)   // centroids + centroid scores + counts + cent_of + members + offsets + stage-1 ids
         s.index = segs * (kHeadDim * g.nc_pad * 2 + g.nc_pad * 4 + 4 + 2 * g.nb_pad * 4 + (g.nc_pad + 1) * 4) +
-                  rsegs * g.m_max * 4;
+                  rsegs * g.m_max * 4 + segs * g.nb_pad / 8;
     return s;
 }
 
@@ -301,6 +302,7 @@ kvd_status kvd_create_cache(const kvd_config* cfg, kvd_cache** out) {
         ALLOC(memb, segs * g.nb_pad * 4);
         ALLOC(moff, segs * (g.nc_pad + 1) * 4);
         ALLOC(csel, rsegs * (size_t)g.m_max * 4);
+        ALLOC(cand_bits, segs * g.nb_pad / 8);
     }
 #undef ALLOC
     if (e == cudaSuccess) e = cudaMemset(c->scores, 0, s.scores);
@@ -308,6 +310,7 @@ kvd_status kvd_create_cache(const kvd_config* cfg, kvd_cache** out) {
     if (e == cudaSuccess) e = cudaMemset(c->slot_block, 0xFF, s.meta4);
     if (e == cudaSuccess) e = cudaMemset(c->miss_count, 0, rsegs * 4);
     if (e == cudaSuccess) e = cudaMemset(c->stats, 0, 64);
+    if (e == cudaSuccess && c->cand_bits) e = cudaMemset(c->cand_bits, 0, (size_t)g.L * g.R * g.Hkv * g.nb_pad / 8);
     if (e == cudaSuccess) e = cudaMemset(c->seg_stats, 0, (size_t)g.L * g.Hkv * 16);
     if (e == cudaSuccess) {
         std::vector<int32_t> caps((size_t)g.L * g.Hkv, (int32_t)std::min<int64_t>(g.C, INT32_MAX));
@@ -335,7 +338,7 @@ void kvd_destroy_cache(kvd_cache* c) {
     cudaSetDevice(c->cfg.device);
     cudaDeviceSynchronize();
     void* dev[] = {c->slots, c->summ, c->scores, c->table, c->slot_block, c->last_use, c->phase,
-                   c->use_count, c->miss, c->miss_count, c->kt_slots, c->kt_acc, c->cap_dev, c->seg_stats, c->cent, c->cscores, c->ncent, c->cent_of, c->memb, c->moff, c->csel, c->idx_stage, c->stats,
+                   c->use_count, c->miss, c->miss_count, c->kt_slots, c->kt_acc, c->cap_dev, c->seg_stats, c->cent, c->cscores, c->ncent, c->cent_of, c->memb, c->moff, c->csel, c->cand_bits, c->idx_stage, c->stats,
                    c->err, c->ntok_dev, c->zero_rec, c->stage_kv, c->stage_rec};
     for (void* p : dev)
         if (p) cudaFree(p);
@@ -539,6 +542,16 @@ kvd_status kvd_read_scores(kvd_cache* c, int32_t layer, int32_t req, int32_t hea
     const int64_t seg = ((int64_t)layer * c->R + req) * c->Hkv + head;
     const int64_t nb = (c->ntok[(size_t)req] + c->P - 1) / c->P;
     KVD_CUDA(cudaMemcpy(out, c->scores + seg * c->nb_pad, (size_t)nb * 4, cudaMemcpyDeviceToHost));
+    if (c->index_ratio > 0) {                     // lookahead scores: exact if scored, else the centroid's
+        std::vector<uint32_t> bits((size_t)c->nb_pad / 32);
+        std::vector<int32_t> cof((size_t)nb);
+        std::vector<float> cs((size_t)c->nc_pad);
+        KVD_CUDA(cudaMemcpy(bits.data(), c->cand_bits + seg * (c->nb_pad / 32), bits.size() * 4, cudaMemcpyDeviceToHost));
+        KVD_CUDA(cudaMemcpy(cof.data(), c->cent_of + seg * c->nb_pad, cof.size() * 4, cudaMemcpyDeviceToHost));
+        KVD_CUDA(cudaMemcpy(cs.data(), c->cscores + seg * c->nc_pad, cs.size() * 4, cudaMemcpyDeviceToHost));
+        for (int64_t b = 0; b < nb; ++b)
+            if (!((bits[(size_t)(b >> 5)] >> (b & 31)) & 1u)) out[b] = cs[(size_t)cof[(size_t)b]];
+    }
     return KVD_OK;
 }
 

@@ -24,6 +24,12 @@ struct ResolveBufs {
     unsigned long long* stats;
     int32_t* err;
     const int32_t* cap;     // [L][Hkv] slots a segment may use (2D window scaling, R28), or NULL: C
+    // hierarchical index (R27): a block scored this step (bit set in cbits) has its exact score in
+    // `scores`; any other block is ranked by its centroid's score (lookahead victim keys)
+    const uint32_t* cbits;  // [seg][nb_pad / 32] this step's candidates, or NULL (flat index)
+    const int32_t* cent_of; // [seg][nb_pad]
+    const float* cscores;   // [seg][nc_pad]
+    int64_t nc_pad;
     unsigned long long* seg_stats;   // [L][Hkv][2] (selected, misses) per layer-head, or NULL
 };
 
@@ -152,8 +158,14 @@ __device__ inline int resolve_main(const StepParams& p, const ResolveBufs& rb, i
         for (int64_t s = tid; s < Ceff; s += blockDim.x) {
             const int32_t blk = sb[s];
             uint64_t key = ~0ull;
-            if (blk >= 0 && blk >= g.sink_end && blk < g.local_begin && !((inS[blk >> 5] >> (blk & 31)) & 1u))
-                key = victim_key(p.policy, lu[s], ph[s], uc[s], blk, sc[blk], rb.err);
+            if (blk >= 0 && blk >= g.sink_end && blk < g.local_begin && !((inS[blk >> 5] >> (blk & 31)) & 1u)) {
+                float score = 0.0f;
+                if (p.policy == KVD_POLICY_LOOKAHEAD) {
+                    const bool exact = !rb.cbits || ((__ldcg(&rb.cbits[seg * (p.nb_pad >> 5) + (blk >> 5)]) >> (blk & 31)) & 1u);
+                    score = exact ? __ldcg(&sc[blk]) : __ldcg(&rb.cscores[seg * rb.nc_pad + rb.cent_of[seg * p.nb_pad + blk]]);
+                }
+                key = victim_key(p.policy, lu[s], ph[s], uc[s], blk, score, rb.err);
+            }
             keys[s] = key;
         }
         __syncthreads();

@@ -527,7 +527,8 @@ __device__ __forceinline__ void select_body(const FuseArgs& fa, const StepParams
         }
         return rank;
     };
-    int32_t* ids_out = out_ids + ((int64_t)bi * p.Hkv + h) * ostride;
+    // stage 1 (index) writes per request id: concurrent chains of one step never share rows
+    int32_t* ids_out = out_ids + ((int64_t)(p.sel_mode == 1 ? r : bi) * p.Hkv + h) * ostride;
     float* sc_out = out_scores ? out_scores + ((int64_t)bi * p.Hkv + h) * ostride : nullptr;
     bool s_ready = false;                         // fused: S[] of the resolve already in smem
     if (compacted && (mode != kModeEqual || local) && K <= kTakeMax) {

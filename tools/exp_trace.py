@@ -72,8 +72,12 @@ def main():
         q = R.q_cur[0, :nb]
         R.cache.select_resolve_fetch(0, q, R.reqs[:nb], k, R.t, R.ids[0, :nb], R.attn[0, :nb], stream=s)
         s.synchronize()
-        show(f"[{rep}] select_kernel ({nb} requests)", read(lib, 16384),
+        tr = read(lib, 16384)
+        show(f"[{rep}] select_kernel ({nb} requests)", tr[:8192],
              ["entry", "after_wait", "scored", "first_digit", "compacted", "radix_done", "emitted", "end"])
+        if tr[8192:, 0].any():
+            show(f"[{rep}] cand_kernel (index stage 2)", tr[8192:],
+                 ["entry", "after_wait", "candidates", "la_scores", "scored", "radix", "emitted", "end"])
         R.cache.sparse_decode(0, q, R.reqs[:nb], R.attn[0, :nb], R.W, R.out[0, :nb], R.lse[0, :nb], stream=s)
         s.synchronize()
         show(f"[{rep}] attn_kernel", read(lib, 16384), ["entry", "after_wait", "tile0", "stream_end", "merged"])
