@@ -67,6 +67,10 @@ def lib():
         L.or_index_build.restype = i64
         L.or_index_select.argtypes = [p, p, p, p, i64, i64, i32, p, i32, i32, p, p, p]
         L.or_index_select.restype = i32
+        L.or_minmax_summaries.argtypes = [p, i64, i32, i32, p, p]
+        L.or_minmax_summaries.restype = None
+        L.or_minmax_scores.argtypes = [p, p, p, i64, i32, p]
+        L.or_minmax_scores.restype = None
         L.or_mckp_greedy.argtypes = [p, p, i32, i32, ctypes.c_double, p]
         L.or_mckp_greedy.restype = ctypes.c_double
         L.or_mckp_exact.argtypes = [p, p, i32, i32, ctypes.c_double, p]
@@ -242,6 +246,29 @@ def index_select(qbar, S, cent, cent_of, is_pinned, k, m):
     return ids[:k], cs[:nc], la[:nb]
 
 
+# ---------------------------------------------------------------- O12 Quest min/max summaries
+def minmax_summaries(K, P):
+    """O12: K [n][d] bf16 -> (MN, MX) [nb][d] bf16: channel-wise min / max of each block."""
+    K = _c(K, np.uint16)
+    n, d = K.shape
+    nb = (n + P - 1) // P
+    MN = np.empty((nb, d), np.uint16)
+    MX = np.empty((nb, d), np.uint16)
+    lib().or_minmax_summaries(_p(K), n, d, P, _p(MN), _p(MX))
+    return MN, MX
+
+
+def minmax_scores(qbar, MN, MX):
+    """O12: Quest upper-bound scores [nb] f32."""
+    qbar = _c(qbar, np.float32)
+    MN = _c(MN, np.uint16)
+    MX = _c(MX, np.uint16)
+    nb, d = MN.shape
+    out = np.empty(nb, np.float32)
+    lib().or_minmax_scores(_p(qbar), _p(MN), _p(MX), nb, d, _p(out))
+    return out
+
+
 # ---------------------------------------------------------------- O11 2D window scaling (MCKP)
 def mckp(benefit, cost, budget, exact=False):
     """O11: (total benefit, choice [pairs]) for benefit / cost [pairs][sizes] (PAPER.md:480-496);
@@ -268,7 +295,10 @@ def segment_step(cache, q_group, S, K, V, P, k, step, policy, W, index=None):
     """One decode step of one segment, in the paper's order (PAPER.md:241-244,
     386): select (O2,O3,O5; or the hierarchical index O9-O10 when index =
     (centroids, cent_of, ratio)) -> resolve (O6) -> attend (O8).  Returns a dict."""
-    if index is None:
+    if isinstance(S, tuple):                      # Quest min/max summaries (O12)
+        scores = minmax_scores(group_query(q_group), S[0], S[1])
+        ids = topk(scores, cache.is_pinned, k)
+    elif index is None:
         ids, scores = segment_select(q_group, S, cache.is_pinned, k)
     else:
         cent, cent_of, ratio = index

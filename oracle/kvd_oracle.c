@@ -562,3 +562,42 @@ double or_mckp_exact(const double* benefit, const double* cost, int32_t pairs, i
     free(cur);
     return best;
 }
+
+/* ====================================== O12 Quest min/max block summaries (baseline)
+ * "Quest partitions key entries into chunks and estimates their importance by multiplying the
+ * query vector with the channel-wise minimum and maximum of the keys".
+ * Reading R30: per block and dim, mn[b][j] = min and mx[b][j] = max of the valid tokens' bf16
+ * keys (exact: a min / max of bf16 values is a bf16 value); the block's score bounds the dot
+ * product of the query with any of its keys:
+ *   acc = +0f; for j in 0..d-1: acc = acc + fmaxf(qbar[j] * mn[b][j], qbar[j] * mx[b][j])
+ * (fp32, products rounded, sequential in j).  Selection is then O4-O5 on these scores. */
+void or_minmax_summaries(const uint16_t* K, int64_t n, int32_t d, int32_t P, uint16_t* MN, uint16_t* MX) {
+    int64_t nb = (n + P - 1) / P;
+    for (int64_t b = 0; b < nb; ++b) {
+        int64_t cnt = n - (int64_t)P * b;
+        if (cnt > P) cnt = P;
+        for (int32_t j = 0; j < d; ++j) {
+            uint16_t lo = K[((int64_t)P * b) * d + j], hi = lo;
+            for (int64_t t = 1; t < cnt; ++t) {
+                uint16_t x = K[((int64_t)P * b + t) * d + j];
+                if (bf16_to_f32(x) < bf16_to_f32(lo)) lo = x;
+                if (bf16_to_f32(x) > bf16_to_f32(hi)) hi = x;
+            }
+            MN[b * d + j] = lo;
+            MX[b * d + j] = hi;
+        }
+    }
+}
+
+void or_minmax_scores(const float* qbar, const uint16_t* MN, const uint16_t* MX, int64_t nb, int32_t d,
+                      float* scores) {
+    for (int64_t b = 0; b < nb; ++b) {
+        float acc = 0.0f;
+        for (int32_t j = 0; j < d; ++j) {
+            float a = qbar[j] * bf16_to_f32(MN[b * d + j]);
+            float c = qbar[j] * bf16_to_f32(MX[b * d + j]);
+            acc = acc + fmaxf(a, c);
+        }
+        scores[b] = acc;
+    }
+}
