@@ -65,6 +65,9 @@ CONFIGS = {
                      "PAPER.md:388-391, DESIGN.md R27)"),
     "c3h": dict(chains=16, L=32, B=16, Hq=32, Hkv=8, n=131072, P=16, k=128, C=2048, alias=4, shard="weak", index=4,
                 desc="c3 with the hierarchical centroid index (4 blocks per centroid)"),
+    "c3q": dict(chains=16, L=32, B=16, Hq=32, Hkv=8, n=131072, P=16, k=128, C=2048, alias=4, shard="weak",
+                summary="minmax", desc="c3 with Quest min/max block summaries (the paper's baseline selection, "
+                                       "PAPER.md:211; DESIGN.md R30)"),
     "c5": dict(chains=16, L=32, B=64, Hq=32, Hkv=8, n=131072, P=16, k=128, C=768, alias=2, shard="strong",
                desc="Llama-3.1-8B shapes, 128k ctx, batch 64 partitioned over the GPUs, GPU cache 768 "
                     "slots/segment (9.4%), host-backed"),
@@ -131,7 +134,9 @@ def per_segment_bytes(cfg, misses_per_seg=0.0, victims=True):
     G = cfg["Hq"] // cfg["Hkv"]
     k = cfg["k"]
     ratio = cfg.get("index", 0)
-    if ratio:
+    if cfg.get("summary") == "minmax":
+        sel_blocks = 2 * nb                       # minimum and maximum summaries
+    elif ratio:
         nc = -(-nb // ratio)
         p_ = 1 + (64 + cfg["P"] - 1) // cfg["P"]
         m = min(nc, max(-(-4 * k // ratio), k + p_))
@@ -259,7 +264,7 @@ class Runner:
         self.cache = KVCache(num_layers=L, num_q_heads=Hq, num_kv_heads=Hkv, block_tokens=P, max_requests=B,
                              max_context=n, slots_per_segment=C, max_select=k, sink_tokens=4, local_tokens=64,
                              policy=args.policy, host_layer_alias=(0 if self.A == L else self.A), device=dev.index,
-                             index_ratio=cfg.get("index", 0))
+                             index_ratio=cfg.get("index", 0), summary_kind=cfg.get("summary", "mean"))
         self.W = self.cache.attn_width(k)
         t0 = time.time()
         Kd = torch.empty((Hkv, n, 128), dtype=torch.int16, device=dev)

@@ -111,6 +111,12 @@ typedef struct {
                                     centroids, keep the m = min(nc, max(ceil(4k/r), k + pinned)) best
                                     and score only their member blocks (exact top-k among those).
                                     Needs min(blocks, 64 m) <= 16384 (KVD_EINVAL otherwise). */
+    int32_t summary_kind;        /* 0: mean key per block (default).  1: Quest's
+                                    channel-wise minimum and maximum of the block's keys
+                                    (R30): score = sum over j of
+                                    max(qbar_j * min_j, qbar_j * max_j), fp32 in j order -- the
+                                    paper's comparison baseline as a second selection workload
+                                    (twice the summary bytes).  Not with index_ratio > 0. */
 } kvd_config;
 
 typedef struct {
@@ -232,6 +238,8 @@ kvd_status kvd_read_host_record(kvd_cache* c, int32_t layer, int32_t req, int32_
 /* Copy a segment's summaries as [nb][128] bf16 (block-major, unpadded). */
 kvd_status kvd_read_summaries(kvd_cache* c, int32_t layer, int32_t req, int32_t head,
                               uint16_t* out);
+/* Quest min/max summaries of a segment (summary_kind 1): mn, mx [nb][128] bf16, block-major. */
+kvd_status kvd_read_minmax(kvd_cache* c, int32_t layer, int32_t req, int32_t head, uint16_t* mn, uint16_t* mx);
 /* Hierarchical index of one segment (index_ratio > 0): *nc receives the centroid count;
  * centroids [nc][128] bf16 (block-major copy) and cent_of [nb] (block -> centroid) may be NULL. */
 kvd_status kvd_read_index(kvd_cache* c, int32_t layer, int32_t req, int32_t head, int64_t* nc,

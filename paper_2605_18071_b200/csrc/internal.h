@@ -52,6 +52,7 @@ struct StepParams {
     int32_t sel_ratio;                // blocks per centroid (stage-1 fan-out, reading R27)
     int32_t sel_stride;               // stage 1: output stride per segment (m_max)
     const int32_t* sel_count;         // stage 1: centroids per segment [L][R][Hkv]
+    const uint16_t* summ2;            // Quest min/max summaries (sel_mode 2): the maximum matrix
     int32_t req[KVD_MAX_BATCH];
 };
 
@@ -76,6 +77,8 @@ struct kvd_cache {
     uint32_t* use_count = nullptr;
     int32_t* miss = nullptr;
     int32_t* miss_count = nullptr;
+    int summary_kind = 0;                  // 0 mean key (R2); 1 Quest min (summ) / max (summ2) (R30)
+    uint16_t* summ2 = nullptr;             // [L][R][Hkv][128][nb_pad] bf16 channel-wise maxima
     // hierarchical index (index_ratio > 0; k_index.cu, DESIGN.md §3 R27)
     int index_ratio = 0;
     int64_t nc_pad = 0;                    // centroid rows per segment (multiple of 128)

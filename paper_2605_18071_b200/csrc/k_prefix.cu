@@ -12,9 +12,13 @@ namespace kvd {
 // grid (nb_pad / 32, Hkv), block 128 threads = dims; each CTA handles 32
 // consecutive blocks and transposes through smem so the dim-major rows are
 // written 64 B at a time.
+// kind 0: mean key (R2); kind 1: Quest channel-wise minimum -> summ_lr, maximum -> summ2_lr (R30;
+// exact: a min / max of bf16 values is one of them; strict comparisons keep the first of equals)
 __global__ void __launch_bounds__(128) summary_kernel(const uint16_t* __restrict__ K, int64_t n, int P,
-                                                      int64_t nb_pad, uint16_t* __restrict__ summ_lr) {
+                                                      int64_t nb_pad, uint16_t* __restrict__ summ_lr,
+                                                      uint16_t* __restrict__ summ2_lr, int kind) {
     __shared__ uint16_t tile[128][33];
+    __shared__ uint16_t tile2[128][33];
     const int j = threadIdx.x;
     const int h = blockIdx.y;
     const int64_t b0 = (int64_t)blockIdx.x * 32;
@@ -26,18 +30,34 @@ __global__ void __launch_bounds__(128) summary_kernel(const uint16_t* __restrict
         if (b < nb) {
             int64_t cnt = n - (int64_t)P * b;
             if (cnt > P) cnt = P;
-            float acc = 0.0f;
-            for (int64_t t = 0; t < cnt; ++t) acc = __fadd_rn(acc, bf16_bits(Kh[((int64_t)P * b + t) * kHeadDim + j]));
-            out = f32_to_bf16_rne(__fdiv_rn(acc, (float)cnt));
+            if (kind == 0) {
+                float acc = 0.0f;
+                for (int64_t t = 0; t < cnt; ++t) acc = __fadd_rn(acc, bf16_bits(Kh[((int64_t)P * b + t) * kHeadDim + j]));
+                out = f32_to_bf16_rne(__fdiv_rn(acc, (float)cnt));
+            } else {
+                uint16_t lo = Kh[((int64_t)P * b) * kHeadDim + j], hi = lo;
+                for (int64_t t = 1; t < cnt; ++t) {
+                    const uint16_t x = Kh[((int64_t)P * b + t) * kHeadDim + j];
+                    if (bf16_bits(x) < bf16_bits(lo)) lo = x;
+                    if (bf16_bits(x) > bf16_bits(hi)) hi = x;
+                }
+                out = lo;
+                tile2[j][i] = hi;
+            }
         }
         tile[j][i] = out;
+        if (kind == 0 || b >= nb) tile2[j][i] = 0;
     }
     __syncthreads();
     // write rows: for each dim jj, 32 consecutive blocks (64 B)
     uint16_t* base = summ_lr + (int64_t)h * kHeadDim * nb_pad;
+    uint16_t* base2 = summ2_lr ? summ2_lr + (int64_t)h * kHeadDim * nb_pad : nullptr;
     for (int e = threadIdx.x; e < 128 * 32; e += 128) {
         int jj = e >> 5, i = e & 31;
-        if (b0 + i < nb_pad) base[(int64_t)jj * nb_pad + b0 + i] = tile[jj][i];
+        if (b0 + i < nb_pad) {
+            base[(int64_t)jj * nb_pad + b0 + i] = tile[jj][i];
+            if (base2) base2[(int64_t)jj * nb_pad + b0 + i] = tile2[jj][i];
+        }
     }
 }
 
@@ -112,8 +132,9 @@ cudaError_t launch_prefix(kvd_cache* c, int layer, int req, const uint16_t* dk, 
                           cudaStream_t s) {
     const int64_t sl = ((int64_t)layer * c->R + req) * c->Hkv;      // first segment of (layer, req)
     SegGeom g = seg_geom(n, c->P, c->cfg.sink_tokens, c->cfg.local_tokens);
-    summary_kernel<<<dim3((unsigned)(c->nb_pad / 32), c->Hkv), 128, 0, s>>>(dk, n, c->P, c->nb_pad,
-                                                                          c->summ + sl * kHeadDim * c->nb_pad);
+    summary_kernel<<<dim3((unsigned)(c->nb_pad / 32), c->Hkv), 128, 0, s>>>(
+        dk, n, c->P, c->nb_pad, c->summ + sl * kHeadDim * c->nb_pad,
+        c->summ2 ? c->summ2 + sl * kHeadDim * c->nb_pad : nullptr, c->summary_kind);
     // slot_of scratch: the first kSlotOfBytes of stage_rec
     int32_t* slot_of = reinterpret_cast<int32_t*>(c->stage_rec);
     table_init_kernel<<<c->Hkv, 256, 0, s>>>(c->table + sl * c->nb_pad, c->slot_block + sl * c->C,

@@ -104,6 +104,9 @@ kvd_status check_config(const kvd_config* cfg, Geometry* g) {
                     g->pmax);
     g->max_splits = kMaxPieces;
     g->ratio = cfg->index_ratio;
+    if (cfg->summary_kind < 0 || cfg->summary_kind > 1) return fail(KVD_EINVAL, "summary_kind must be 0 (mean) or 1 (min/max)");
+    if (cfg->summary_kind == 1 && cfg->index_ratio > 0)
+        return fail(KVD_EINVAL, "the hierarchical index clusters mean-key summaries (summary_kind 0)");
     g->nc_pad = 0;
     g->m_max = 0;
     if (g->ratio < 0 || g->ratio > kIdxWindow) return fail(KVD_EINVAL, "index_ratio must be 0 (flat) or 1..%d", kIdxWindow);
@@ -126,11 +129,11 @@ kvd_status check_config(const kvd_config* cfg, Geometry* g) {
 }
 
 struct Sizes {
-    size_t slots, summ, scores, table, meta4, meta1, miss, small, host, index;
-    size_t dev_total() const { return slots + summ + scores + table + 3 * meta4 + meta1 + miss + small + index; }
+    size_t slots, summ, scores, table, meta4, meta1, miss, small, host, index, summ2;
+    size_t dev_total() const { return slots + summ + scores + table + 3 * meta4 + meta1 + miss + small + index + summ2; }
 };
 
-Sizes sizes_of(const Geometry& g) {
+Sizes sizes_of(const Geometry& g, int summary_kind = 0) {
     Sizes s;
     const size_t segs = (size_t)g.L * g.R * g.Hkv;
     const size_t rsegs = (size_t)g.R * g.Hkv;
@@ -144,6 +147,7 @@ Sizes sizes_of(const Geometry& g) {
     s.small = rsegs * 12 + 64 + 4 + (size_t)g.R * 4 + g.rec_bytes;
     s.host = g.resident ? 0 : (size_t)g.A * g.R * g.Hkv * g.nb_max * g.rec_bytes;
     s.index = 0;
+    s.summ2 = summary_kind == 1 ? s.summ : 0;
     if (g.ratio > 0)   // centroids + centroid scores + counts + cent_of + members + offsets + stage-1 ids
         s.index = segs * (kHeadDim * g.nc_pad * 2 + g.nc_pad * 4 + 4 + 2 * g.nb_pad * 4 + (g.nc_pad + 1) * 4) +
                   rsegs * g.m_max * 4 + segs * g.nb_pad / 8;
@@ -207,6 +211,11 @@ kvd_status check_step(kvd_cache* c, int32_t layer, const int32_t* req_ids, int32
     p->kt_acc = c->kt_acc;
     p->kt_base = (layer * c->R + p->req[0]) * kKtKinds;
     p->exp_trace = nullptr;
+    p->sel_mode = c->summary_kind == 1 ? 2 : 0;   // Quest min/max scoring (R30) or mean summaries
+    p->sel_ratio = 0;
+    p->sel_stride = 0;
+    p->sel_count = nullptr;
+    p->summ2 = c->summ2;
 #ifdef KVD_EXPERIMENTS
     if (getenv("KVD_EXP_TRACE")) {
         if (!g_exp_trace) {
@@ -246,7 +255,7 @@ kvd_status kvd_required_bytes(const kvd_config* cfg, size_t* dev_bytes, size_t* 
     Geometry g;
     kvd_status st = check_config(cfg, &g);
     if (st) return st;
-    Sizes s = sizes_of(g);
+    Sizes s = sizes_of(g, cfg->summary_kind);
     if (dev_bytes) *dev_bytes = s.dev_total();
     if (host_pinned_bytes) *host_pinned_bytes = s.host;
     return KVD_OK;
@@ -267,6 +276,7 @@ kvd_status kvd_create_cache(const kvd_config* cfg, kvd_cache** out) {
     c->C = g.C; c->resident = g.resident; c->rec_bytes = g.rec_bytes; c->max_splits = g.max_splits;
     c->index_ratio = g.ratio; c->nc_pad = g.nc_pad; c->m_max = g.m_max;
     c->cap_host.assign((size_t)g.L * g.Hkv, g.C);
+    c->summary_kind = cfg->summary_kind;
     c->ntok.assign((size_t)g.R, 0);
     {
         int lo = 0, hi = 0;
@@ -292,6 +302,7 @@ kvd_status kvd_create_cache(const kvd_config* cfg, kvd_cache** out) {
     ALLOC(ntok_dev, (size_t)g.R * 4);
     ALLOC(zero_rec, (size_t)g.rec_bytes);
     ALLOC(cap_dev, (size_t)g.L * g.Hkv * 4);
+    if (cfg->summary_kind == 1) ALLOC(summ2, s.summ);
     ALLOC(seg_stats, (size_t)g.L * g.Hkv * 16);
     if (g.ratio > 0) {
         const size_t segs = (size_t)g.L * g.R * g.Hkv;
@@ -338,7 +349,7 @@ void kvd_destroy_cache(kvd_cache* c) {
     cudaSetDevice(c->cfg.device);
     cudaDeviceSynchronize();
     void* dev[] = {c->slots, c->summ, c->scores, c->table, c->slot_block, c->last_use, c->phase,
-                   c->use_count, c->miss, c->miss_count, c->kt_slots, c->kt_acc, c->cap_dev, c->seg_stats, c->cent, c->cscores, c->ncent, c->cent_of, c->memb, c->moff, c->csel, c->cand_bits, c->idx_stage, c->stats,
+                   c->use_count, c->miss, c->miss_count, c->kt_slots, c->kt_acc, c->summ2, c->cap_dev, c->seg_stats, c->cent, c->cscores, c->ncent, c->cent_of, c->memb, c->moff, c->csel, c->cand_bits, c->idx_stage, c->stats,
                    c->err, c->ntok_dev, c->zero_rec, c->stage_kv, c->stage_rec};
     for (void* p : dev)
         if (p) cudaFree(p);
@@ -529,6 +540,26 @@ kvd_status kvd_read_index(kvd_cache* c, int32_t layer, int32_t req, int32_t head
     if (cent_of) {
         const int64_t nb = (c->ntok[(size_t)req] + c->P - 1) / c->P;
         KVD_CUDA(cudaMemcpy(cent_of, c->cent_of + seg * c->nb_pad, (size_t)nb * 4, cudaMemcpyDeviceToHost));
+    }
+    return KVD_OK;
+}
+
+kvd_status kvd_read_minmax(kvd_cache* c, int32_t layer, int32_t req, int32_t head, uint16_t* mn, uint16_t* mx) {
+    kvd_status st = check_seg(c, layer, req, head);
+    if (st) return st;
+    if (c->summary_kind != 1) return fail(KVD_ESTATE, "cache keeps mean-key summaries");
+    if (!mn || !mx) return fail(KVD_EINVAL, "NULL argument");
+    if (c->ntok[(size_t)req] <= 0) return fail(KVD_ESTATE, "request %d not loaded", req);
+    KVD_CUDA(cudaDeviceSynchronize());
+    const int64_t seg = ((int64_t)layer * c->R + req) * c->Hkv + head;
+    const int64_t nb = (c->ntok[(size_t)req] + c->P - 1) / c->P;
+    std::vector<uint16_t> tmp((size_t)(kHeadDim * c->nb_pad));
+    for (int which = 0; which < 2; ++which) {
+        const uint16_t* src = (which ? c->summ2 : c->summ) + seg * kHeadDim * c->nb_pad;
+        KVD_CUDA(cudaMemcpy(tmp.data(), src, tmp.size() * 2, cudaMemcpyDeviceToHost));
+        uint16_t* out = which ? mx : mn;
+        for (int64_t b = 0; b < nb; ++b)
+            for (int j = 0; j < kHeadDim; ++j) out[b * kHeadDim + j] = tmp[(size_t)(j * c->nb_pad + b)];
     }
     return KVD_OK;
 }

@@ -275,6 +275,32 @@ __device__ __forceinline__ void select_body(const FuseArgs& fa, const StepParams
         float acc[V];
 #pragma unroll
         for (int v = 0; v < V; ++v) acc[v] = 0.0f;
+        if (p.sel_mode == 2) {
+            // Quest min/max (R30): acc = acc + max(q mn, q mx), products rounded, sequential in j.
+            // The minimum rows were loaded above (bufA / bufB hold rows 0 .. 2R-1 of the minima);
+            // here the rows are streamed in pairs (minimum, maximum) R/2 at a time.
+            const Vec* src2 = reinterpret_cast<const Vec*>(p.summ2 + seg * kHeadDim * p.nb_pad + base) + (ld ? i0 / V : 0);
+#pragma unroll 1
+            for (int j0 = 0; j0 < kHeadDim; j0 += R) {
+                Vec mnv[R], mxv[R];
+#pragma unroll
+                for (int u = 0; u < R; ++u) {
+                    if (ld) mnv[u] = __ldcs(src + (j0 + u) * rstride);
+                    if (ld) mxv[u] = __ldcs(src2 + (j0 + u) * rstride);
+                }
+#pragma unroll
+                for (int u = 0; u < R; ++u) {
+                    const float qj = qbar[j0 + u];
+#pragma unroll
+                    for (int v = 0; v < V; ++v) {
+                        const uint32_t wn = VecOf<V>::word(mnv[u], v >> 1), wx = VecOf<V>::word(mxv[u], v >> 1);
+                        const float a = __fmul_rn(qj, (v & 1) ? bf16_hi(wn) : bf16_lo(wn));
+                        const float b2 = __fmul_rn(qj, (v & 1) ? bf16_hi(wx) : bf16_lo(wx));
+                        acc[v] = __fadd_rn(acc[v], fmaxf(a, b2));
+                    }
+                }
+            }
+        }
         auto consume = [&](const Vec (&buf)[R], int j0) {
 #pragma unroll
             for (int u = 0; u < R; ++u) {
@@ -287,7 +313,7 @@ __device__ __forceinline__ void select_body(const FuseArgs& fa, const StepParams
             }
         };
 #pragma unroll 1
-        for (int j0 = 0; j0 < kHeadDim; j0 += 2 * R) {
+        for (int j0 = 0; j0 < (p.sel_mode == 2 ? 0 : kHeadDim); j0 += 2 * R) {
             consume(bufA, j0);
             if (ld && j0 + 2 * R < kHeadDim) {
 #pragma unroll

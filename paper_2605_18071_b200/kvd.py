@@ -14,6 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libkvd.so")
 
 POLICY = {"lru": 0, "lfu": 1, "la": 2, "lookahead": 2}
+SUMMARY_KIND = {"mean": 0, "minmax": 1}
 STATUS = {0: "KVD_OK", 1: "KVD_EINVAL", 2: "KVD_ERANGE", 3: "KVD_ECAPACITY", 4: "KVD_ENOMEM",
           5: "KVD_ECUDA", 6: "KVD_EDEVICE", 7: "KVD_ESTATE"}
 KVD_MAX_BATCH = 256
@@ -33,7 +34,8 @@ class Config(ctypes.Structure):
                 ("max_context", ctypes.c_int64), ("slots_per_segment", ctypes.c_int64),
                 ("max_select", ctypes.c_int32), ("sink_tokens", ctypes.c_int32),
                 ("local_tokens", ctypes.c_int32), ("policy", ctypes.c_int32),
-                ("host_layer_alias", ctypes.c_int32), ("device", ctypes.c_int32), ("index_ratio", ctypes.c_int32)]
+                ("host_layer_alias", ctypes.c_int32), ("device", ctypes.c_int32), ("index_ratio", ctypes.c_int32),
+                ("summary_kind", ctypes.c_int32)]
 
 
 class Stats(ctypes.Structure):
@@ -58,7 +60,7 @@ EXPORTS = ["kvd_required_bytes", "kvd_create_cache", "kvd_destroy_cache", "kvd_g
            "kvd_version", "kvd_set_device_step", "kvd_launch_count",
            "kvd_select_resolve_fetch", "kvd_enable_kernel_timer", "kvd_read_kernel_timer",
            "kvd_probe_zero_copy", "kvd_read_index", "kvd_set_segment_capacity", "kvd_get_segment_stats",
-           "kvd_plan_window_scaling"]
+           "kvd_plan_window_scaling", "kvd_read_minmax"]
 
 
 def lib():
@@ -99,6 +101,7 @@ def lib():
             "kvd_set_segment_capacity": ([p, i32, i32, i64], i32),
             "kvd_get_segment_stats": ([p, p, p], i32),
             "kvd_plan_window_scaling": ([p, p, i32, i32, ctypes.c_double, p], i32),
+            "kvd_read_minmax": ([p, i32, i32, i32, p, p], i32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -142,11 +145,11 @@ class KVCache:
 
     def __init__(self, *, num_layers, num_q_heads, num_kv_heads, block_tokens, max_requests, max_context,
                  slots_per_segment, max_select, sink_tokens=4, local_tokens=64, policy="lru",
-                 host_layer_alias=0, device=0, head_dim=128, index_ratio=0):
+                 host_layer_alias=0, device=0, head_dim=128, index_ratio=0, summary_kind=0):
         self.cfg = Config(num_layers, num_q_heads, num_kv_heads, head_dim, block_tokens, max_requests,
                           max_context, slots_per_segment, max_select, sink_tokens, local_tokens,
                           POLICY[policy] if isinstance(policy, str) else int(policy), host_layer_alias, device,
-                          index_ratio)
+                          index_ratio, SUMMARY_KIND[summary_kind] if isinstance(summary_kind, str) else summary_kind)
         self.index_ratio = index_ratio
         h = ctypes.c_void_p()
         _check(lib().kvd_create_cache(ctypes.byref(self.cfg), ctypes.byref(h)))
@@ -165,7 +168,7 @@ class KVCache:
                      kw["block_tokens"], kw["max_requests"], kw["max_context"], kw["slots_per_segment"],
                      kw["max_select"], kw.get("sink_tokens", 4), kw.get("local_tokens", 64),
                      POLICY[kw.get("policy", "lru")], kw.get("host_layer_alias", 0), kw.get("device", 0),
-                     kw.get("index_ratio", 0))
+                     kw.get("index_ratio", 0), kw.get("summary_kind", 0))
         d, hb = ctypes.c_size_t(), ctypes.c_size_t()
         _check(lib().kvd_required_bytes(ctypes.byref(cfg), ctypes.byref(d), ctypes.byref(hb)))
         return d.value, hb.value
@@ -239,6 +242,13 @@ class KVCache:
         out = np.empty((nb, 128), np.uint16)
         _check(lib().kvd_read_summaries(self.h, layer, req, head, ptr(out)))
         return out
+
+    def read_minmax(self, layer, req, head, nb):
+        """Quest min/max summaries (summary_kind 1): (mn, mx) [nb][128] uint16."""
+        mn = np.empty((nb, 128), np.uint16)
+        mx = np.empty((nb, 128), np.uint16)
+        _check(lib().kvd_read_minmax(self.h, layer, req, head, ptr(mn), ptr(mx)))
+        return mn, mx
 
     def read_index(self, layer, req, head, nb):
         """(centroids [nc][128] uint16, cent_of [nb] int32) of a segment's hierarchical index."""

@@ -27,7 +27,7 @@ def row_normwise_err(o, ref):
 class Case:
     def __init__(self, *, L=1, B=1, Hq=8, Hkv=2, n=4096, P=16, k=32, C=None, policy="lru", seed=0,
                  alpha=0.9, ragged=False, sink=4, local=64, alias=0, reqs=None, R=None, device=0,
-                 fused=False, index_ratio=0, caps=None):
+                 fused=False, index_ratio=0, caps=None, summary="mean"):
         self.fused = fused            # kvd_select_resolve_fetch instead of select_topk + resolve_and_fetch
         self.index_ratio = index_ratio  # hierarchical centroid index (R27); 0 = flat
         self.L, self.B, self.Hq, self.Hkv, self.P, self.k = L, B, Hq, Hkv, P, k
@@ -43,7 +43,8 @@ class Case:
         self.cache = KVCache(num_layers=L, num_q_heads=Hq, num_kv_heads=Hkv, block_tokens=P, max_requests=R,
                              max_context=n, slots_per_segment=self.C, max_select=k, sink_tokens=sink,
                              local_tokens=local, policy=policy, host_layer_alias=alias, device=device,
-                             index_ratio=index_ratio)
+                             index_ratio=index_ratio, summary_kind=summary)
+        self.summary = summary
         self.W = self.cache.attn_width(k)
         self.caps = dict(caps or {})              # 2D window scaling: (layer, head) -> slots (R28)
         for (l, h), cap in self.caps.items():
@@ -60,7 +61,8 @@ class Case:
                 self.cache.load_prefix(l, r, K, V, self.n[r])
                 for h in range(Hkv):
                     self.kv[(l, r, h)] = (K[h], V[h])
-                    self.S[(l, r, h)] = oracle.block_summaries(K[h], P)
+                    self.S[(l, r, h)] = (oracle.block_summaries(K[h], P) if summary == "mean"
+                                         else oracle.minmax_summaries(K[h], P))
                     if index_ratio:
                         cent, cent_of = oracle.index_build(self.S[(l, r, h)], index_ratio)
                         self.index[(l, r, h)] = (cent, cent_of, index_ratio)

@@ -37,7 +37,8 @@ class OracleSegment:
         n, P = cfg["n"], cfg["P"]
         sl = l % R.A
         self.K, self.V = synth.segment_kv(args.seed, sl, R.greqs[b], h, n)
-        self.S = oracle.block_summaries(self.K, P)
+        self.S = (oracle.minmax_summaries(self.K, P) if cfg.get("summary") == "minmax"
+                  else oracle.block_summaries(self.K, P))
         pinned = oracle.pinned_blocks(n, P)
         nb = (n + P - 1) // P
         C = cfg["C"] if cfg["C"] is not None else nb

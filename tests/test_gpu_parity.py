@@ -292,3 +292,20 @@ def test_window_scaling_shrink_and_errors():
     with pytest.raises(KVDError) as e:
         c.cache.select_topk(0, q, [0], 32, ids)
     assert e.value.status == "KVD_ECAPACITY"
+
+
+# ---- Quest min/max summaries (R30), the paper's comparison baseline as a second selection
+# workload: summaries bit-exact, selection / resolve / attention as usual
+def test_minmax_summaries_bit_exact():
+    c = Case(L=1, B=2, Hq=8, Hkv=2, n=1000, P=16, k=8, ragged=True, summary="minmax")
+    for (l, r, h), (mn, mx) in c.S.items():
+        gmn, gmx = c.cache.read_minmax(l, r, h, mn.shape[0])
+        assert np.array_equal(gmn, mn) and np.array_equal(gmx, mx), (l, r, h)
+
+
+@pytest.mark.parametrize("n,P,C,policy,fused", [(4096, 16, 69, "la", True), (3000, 16, 60, "lru", False),
+                                                (40000, 1, 2000, "la", True), (2000, 4, None, "lfu", False)])
+def test_minmax_select_parity(n, P, C, policy, fused):
+    c = Case(L=1, B=2, Hq=8, Hkv=2, n=n, P=P, k=32, C=C, policy=policy, seed=71, ragged=True, fused=fused,
+             summary="minmax")
+    c.run(steps=4, check_slots_every=2)
