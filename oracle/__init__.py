@@ -71,6 +71,8 @@ def lib():
         L.or_minmax_summaries.restype = None
         L.or_minmax_scores.argtypes = [p, p, p, i64, i32, p]
         L.or_minmax_scores.restype = None
+        L.or_append_block.argtypes = [i64, i64, p, p, p, p, p, p, u32, i32, p]
+        L.or_append_block.restype = i32
         L.or_mckp_greedy.argtypes = [p, p, i32, i32, ctypes.c_double, p]
         L.or_mckp_greedy.restype = ctypes.c_double
         L.or_mckp_exact.argtypes = [p, p, i32, i32, ctypes.c_double, p]
@@ -180,6 +182,28 @@ class SegmentCache:
         if rc:
             raise OracleError(rc, "resolve")
         return attn, miss[:k], nm.value, nh.value
+
+
+def append_token(cache, K, V, S, n, P, k_new, v_new, step, policy, scores, sink=4, local=64, summary="mean"):
+    """O13 + O1: append one token (k_new, v_new [d] bf16) at position n of a segment.
+    Returns the new (K, V, S, pinned): the keys / values grown by one row, the summaries recomputed
+    by O1 (O12 for min/max) over the grown keys, the pinned set of n + 1 tokens; the cache admits
+    the new block when the token opens one (or_append_block)."""
+    K = np.concatenate([K, np.asarray(k_new, np.uint16)[None, :]], axis=0)
+    V = np.concatenate([V, np.asarray(v_new, np.uint16)[None, :]], axis=0)
+    S = block_summaries(K, P) if summary == "mean" else minmax_summaries(K, P)
+    pinned = pinned_blocks(n + 1, P, sink, local)
+    nb_new = len(pinned)
+    cache.is_pinned = _c(pinned, np.uint8)
+    if nb_new > cache.nb:                          # the token opens block nb_new - 1
+        cache.table = np.concatenate([cache.table, np.full(nb_new - cache.nb, -1, np.int32)])
+        cache.nb = nb_new
+        sc = _c(scores, np.float32) if scores is not None else None
+        rc = lib().or_append_block(nb_new, cache.C, _p(cache.is_pinned), _p(cache.table), _p(cache.slot_block),
+                                   _p(cache.last_use), _p(cache.phase), _p(cache.use_count), step, policy, _p(sc))
+        if rc:
+            raise OracleError(rc, "append_block")
+    return K, V, S, pinned
 
 
 def fetch(host_records, slot_pool, miss, n_miss):

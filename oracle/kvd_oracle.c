@@ -601,3 +601,40 @@ void or_minmax_scores(const float* qbar, const uint16_t* MN, const uint16_t* MX,
         scores[b] = acc;
     }
 }
+
+/* ============================================ O13 decode-time append (block admission)
+ * "each step appending new key and value vectors to the cache".  Reading R16
+ * (round 2): the appended token goes to the always-resident local window; when it opens a new
+ * block b (= the old block count), that block is admitted like a miss at `step`: a resident cache
+ * (C >= blocks) keeps block b in slot b; otherwise the free slot with the lowest index, else the
+ * resident block with the smallest O6 policy key among those not pinned after the append (victim:
+ * table entry cleared).  Admitted: last = step, phase = 1, count = 1.  table / is_pinned have the
+ * new block count nb_new = b + 1 entries.  Returns 0, or 3 (ECAPACITY) when nothing is evictable. */
+int32_t or_append_block(int64_t nb_new, int64_t C, const uint8_t* is_pinned, int32_t* table, int32_t* slot_block,
+                        uint32_t* last_use, uint8_t* phase, uint32_t* use_count, uint32_t step, int32_t policy,
+                        const float* scores) {
+    int64_t b = nb_new - 1, dest = -1;
+    if (C >= nb_new) {
+        dest = b;
+    } else {
+        for (int64_t s = 0; s < C && dest < 0; ++s)
+            if (slot_block[s] < 0) dest = s;
+        if (dest < 0) {
+            or_victim best;
+            int have = 0;
+            for (int64_t s = 0; s < C; ++s) {
+                int32_t blk = slot_block[s];
+                if (blk < 0 || blk >= b || is_pinned[blk]) continue;
+                or_victim v = {s, blk, last_use[s], use_count[s], phase[s], scores ? scores[blk] : 0.0f, policy};
+                if (!have || or_victim_cmp(&v, &best) < 0) { best = v; have = 1; }
+            }
+            if (!have) return 3;
+            table[best.block] = -1;
+            dest = best.slot;
+        }
+    }
+    table[b] = (int32_t)dest;
+    slot_block[dest] = (int32_t)b;
+    last_use[dest] = step; phase[dest] = 1; use_count[dest] = 1;
+    return 0;
+}
