@@ -203,6 +203,19 @@ kvd_status kvd_select_resolve_fetch(kvd_cache* c, int32_t layer, const uint16_t*
                                     uint32_t step, int32_t* out_ids, float* out_scores,
                                     int32_t* out_attn, kvd_stream stream);
 
+/* Decode-time append ("each step appending new key and value vectors"; DESIGN.md
+ * R16): one new token for each listed request of `layer`, at position n_r (the layer's token
+ * count), k / v: device bf16 [B][Hkv][128].  The token joins the always-resident local window;
+ * when it opens a new block, that block is admitted at `step` (fully resident: slot = block;
+ * otherwise the lowest free slot of the layer-head's window, else the resident block with the
+ * smallest policy key among those not pinned after the append is evicted).  The token's K / V rows
+ * are written to the slot record (and the host store), the block's summary is recomputed over its
+ * tokens as kvd_load_prefix computes it, and the layer's token count grows by one.  Asynchronous on
+ * `stream`; the host-side token counts advance at the call (do not replay it from a CUDA graph).
+ * KVD_ERANGE when a context is full; KVD_ESTATE with the hierarchical index or host-layer aliasing. */
+kvd_status kvd_append_token(kvd_cache* c, int32_t layer, const int32_t* req_ids, int32_t B, const uint16_t* k,
+                            const uint16_t* v, uint32_t step, kvd_stream stream);
+
 /* CUDA-graph support for (2): when dev_step != NULL, every later resolve reads
  * the decode-step index from *dev_step (device uint32) when the kernel runs and
  * ignores its host `step` argument, so one captured step can be replayed for

@@ -101,7 +101,7 @@ struct kvd_cache {
     bool kt_on = false;
     unsigned long long* stats = nullptr;   // [5] kvd_stats fields
     int32_t* err = nullptr;
-    int32_t* ntok_dev = nullptr;
+    int32_t* ntok_dev = nullptr;           // [L][R] token counts (kernels get the launch layer's row)
     uint8_t* zero_rec = nullptr;           // one zero record (padding entries)
     const uint32_t* step_dev = nullptr;    // kvd_set_device_step
     // setup staging (lazily allocated)
@@ -109,7 +109,7 @@ struct kvd_cache {
     uint8_t* stage_rec = nullptr;
     // host
     uint8_t* host_store = nullptr;          // pinned, mapped (UVA: same pointer on device)
-    std::vector<int64_t> ntok;              // host copy of per-request token counts
+    std::vector<int64_t> ntok;              // host copy of the token counts [L][R] (kvd_append_token grows them)
 };
 
 namespace kvd {
@@ -137,6 +137,8 @@ constexpr int kIdxIters = 4;          // Lloyd rounds before the final assignmen
 constexpr int kIdxFanout = 4;         // stage-1 centroids: ceil(kIdxFanout * k / ratio), >= k + pinned
 constexpr int kCandCap = 16384;       // stage-2 candidates per segment at most (64 * m_max)
 cudaError_t launch_shrink_capacity(kvd_cache* c, int layer, int head, int64_t cap, cudaStream_t s);   // k_resolve.cu
+cudaError_t launch_append(kvd_cache* c, const StepParams& p, const uint16_t* k, const uint16_t* v, const int32_t* n,
+                          cudaStream_t s);                                                  // k_append.cu
 cudaError_t launch_zero_copy(const void* host, void* dev, size_t bytes, int ctas, cudaStream_t s);
 cudaError_t launch_select_resolve(kvd_cache* c, const StepParams& p, const uint16_t* q, int32_t* out_ids,
                                   float* out_scores, int32_t* out_attn, cudaStream_t s);

@@ -400,7 +400,7 @@ static cudaError_t launch_attn_s(kvd_cache* c, const StepParams& p, const uint16
     Work wk;
     wk.TS = (p.W + p.E - 1) / p.E;
     wk.NP = attn_pieces(wk.TS);
-    AttnBufs ab{c->slots, c->ntok_dev, c->zero_rec};
+    AttnBufs ab{c->slots, c->ntok_dev + (int64_t)p.layer * c->R, c->zero_rec};   // token counts of this layer
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(wk.NP / kAttnWarpsPerCta), (unsigned)(p.B * p.Hkv));
     cfg.blockDim = dim3(kAttnWarpsPerCta * 32);

@@ -420,7 +420,7 @@ cudaError_t launch_index_select(kvd_cache* c, const StepParams& p, const uint16_
     cudaError_t e = launch_select_centroids(c, p1, q, s);
     if (e != cudaSuccess) return e;
     CandArgs ca;
-    ca.fa.rb = resolve_bufs(c);
+    ca.fa.rb = resolve_bufs(c, p.layer);
     ca.fa.out_attn = out_attn;
     ca.fa.host_store = c->resident ? nullptr : c->host_store;
     ca.fa.slots = c->slots;
@@ -449,9 +449,9 @@ cudaError_t launch_index_select(kvd_cache* c, const StepParams& p, const uint16_
     }
     const int prio = (fused && ca.fa.host_store) ? c->prio_hi : 0;
     e = fused ? launch_pdl_prio(prio, cand_kernel<true>, dim3(p.Hkv, p.B), dim3(kCandThreads), smem, s, ca, p, q,
-                                (const int32_t*)c->ntok_dev, out_ids, out_scores)
+                                (const int32_t*)c->ntok_dev + (int64_t)p.layer * c->R, out_ids, out_scores)
               : launch_pdl(cand_kernel<false>, dim3(p.Hkv, p.B), dim3(kCandThreads), smem, s, ca, p, q,
-                           (const int32_t*)c->ntok_dev, out_ids, out_scores);
+                           (const int32_t*)c->ntok_dev + (int64_t)p.layer * c->R, out_ids, out_scores);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }

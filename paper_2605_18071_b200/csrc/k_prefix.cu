@@ -160,7 +160,7 @@ cudaError_t launch_prefix(kvd_cache* c, int layer, int req, const uint16_t* dk, 
             }
         }
     }
-    set_ntok_kernel<<<1, 1, 0, s>>>(c->ntok_dev, req, (int32_t)n);
+    set_ntok_kernel<<<1, 1, 0, s>>>(c->ntok_dev + (int64_t)layer * c->R, req, (int32_t)n);
     return cudaGetLastError();
 }
 

@@ -133,10 +133,11 @@ size_t resolve_smem_bytes(int64_t nkeys, int64_t kmax, int64_t nb_pad) {
            sizeof(uint32_t) * (size_t)((nb_pad + 31) / 32);
 }
 
-ResolveBufs resolve_bufs(kvd_cache* c) {
+ResolveBufs resolve_bufs(kvd_cache* c, int layer) {
     ResolveBufs rb{c->table,    c->slot_block, c->last_use, c->phase, c->use_count, c->scores,
                    c->ntok_dev, c->miss,       c->miss_count, c->kmax, 0,           c->stats,    c->err};
     rb.nkeys = c->resident ? 0 : c->C;            // a fully resident cache never evicts
+    rb.ntok = c->ntok_dev + (int64_t)layer * c->R;   // token counts of the launch's layer
     rb.cap = c->cap_dev;
     rb.cbits = c->cand_bits;                      // NULL unless the hierarchical index is on
     rb.cent_of = c->cent_of;
@@ -154,7 +155,7 @@ cudaError_t launch_gather(kvd_cache* c, const StepParams& p, cudaStream_t s) {
 
 cudaError_t launch_resolve(kvd_cache* c, const StepParams& p, const int32_t* ids, int32_t* out_attn,
                            cudaStream_t s) {
-    const ResolveBufs rb = resolve_bufs(c);
+    const ResolveBufs rb = resolve_bufs(c, p.layer);
     const size_t smem = resolve_smem_bytes(rb.nkeys, c->kmax, c->nb_pad);
     static size_t smem_set[64] = {};              // opted-in dynamic size, per device ordinal
     const int dev = c->cfg.device & 63;

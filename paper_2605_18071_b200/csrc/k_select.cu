@@ -86,7 +86,7 @@ cudaError_t launch_select_resolve(kvd_cache* c, const StepParams& p, const uint1
                                   float* out_scores, int32_t* out_attn, cudaStream_t s) {
     if (c->index_ratio > 0) return launch_index_select(c, p, q, out_ids, out_scores, out_attn, s);
     FuseArgs fa;
-    fa.rb = resolve_bufs(c);
+    fa.rb = resolve_bufs(c, p.layer);
     fa.out_attn = out_attn;
     fa.host_store = c->resident ? nullptr : c->host_store;
     fa.slots = c->slots;

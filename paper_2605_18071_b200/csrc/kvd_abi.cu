@@ -174,8 +174,9 @@ kvd_status check_step(kvd_cache* c, int32_t layer, const int32_t* req_ids, int32
         if (r < 0 || r >= c->R) return fail(KVD_EINVAL, "req_ids[%d]=%d out of range", b, r);
         if (seen[(size_t)r]) return fail(KVD_EINVAL, "req_ids[%d]=%d repeated", b, r);
         seen[(size_t)r] = 1;
-        if (c->ntok[(size_t)r] <= 0) return fail(KVD_ESTATE, "request %d has no prefix loaded", r);
-        const SegGeom sg = seg_geom(c->ntok[(size_t)r], c->P, c->cfg.sink_tokens, c->cfg.local_tokens);
+        const int64_t nr = c->ntok[(size_t)layer * c->R + r];
+        if (nr <= 0) return fail(KVD_ESTATE, "request %d has no prefix loaded in layer %d", r, layer);
+        const SegGeom sg = seg_geom(nr, c->P, c->cfg.sink_tokens, c->cfg.local_tokens);
         const int pr = sg.sink_end + (sg.nb - sg.local_begin);
         if (k > sg.nb - pr)
             return fail(KVD_ERANGE, "request %d: k_blocks=%d > %d candidate blocks", r, k, sg.nb - pr);
@@ -277,7 +278,7 @@ kvd_status kvd_create_cache(const kvd_config* cfg, kvd_cache** out) {
     c->index_ratio = g.ratio; c->nc_pad = g.nc_pad; c->m_max = g.m_max;
     c->cap_host.assign((size_t)g.L * g.Hkv, g.C);
     c->summary_kind = cfg->summary_kind;
-    c->ntok.assign((size_t)g.R, 0);
+    c->ntok.assign((size_t)g.L * g.R, 0);
     {
         int lo = 0, hi = 0;
         if (cudaDeviceGetStreamPriorityRange(&lo, &hi) == cudaSuccess) c->prio_hi = hi;
@@ -299,7 +300,7 @@ kvd_status kvd_create_cache(const kvd_config* cfg, kvd_cache** out) {
     ALLOC(miss_count, rsegs * 4);
     ALLOC(stats, 64);
     ALLOC(err, 4);
-    ALLOC(ntok_dev, (size_t)g.R * 4);
+    ALLOC(ntok_dev, (size_t)g.L * g.R * 4);
     ALLOC(zero_rec, (size_t)g.rec_bytes);
     ALLOC(cap_dev, (size_t)g.L * g.Hkv * 4);
     if (cfg->summary_kind == 1) ALLOC(summ2, s.summ);
@@ -328,7 +329,7 @@ kvd_status kvd_create_cache(const kvd_config* cfg, kvd_cache** out) {
         e = cudaMemcpy(c->cap_dev, caps.data(), caps.size() * 4, cudaMemcpyHostToDevice);
     }
     if (e == cudaSuccess) e = cudaMemset(c->err, 0, 4);
-    if (e == cudaSuccess) e = cudaMemset(c->ntok_dev, 0, (size_t)g.R * 4);
+    if (e == cudaSuccess) e = cudaMemset(c->ntok_dev, 0, (size_t)g.L * g.R * 4);
     if (e == cudaSuccess) e = cudaMemset(c->zero_rec, 0, (size_t)g.rec_bytes);
     if (e == cudaSuccess && !g.resident) {
         void* h = nullptr;
@@ -384,9 +385,6 @@ kvd_status kvd_load_prefix(kvd_cache* c, int32_t layer, int32_t req, const uint1
     if (req < 0 || req >= c->R) return fail(KVD_EINVAL, "req %d out of range", req);
     if (n_tokens < 1 || n_tokens > c->nmax)
         return fail(KVD_EINVAL, "n_tokens=%lld outside [1, %lld]", (long long)n_tokens, (long long)c->nmax);
-    if (c->ntok[(size_t)req] > 0 && c->ntok[(size_t)req] != n_tokens)
-        return fail(KVD_ESTATE, "request %d already has %lld tokens in another layer", req,
-                    (long long)c->ntok[(size_t)req]);
     KVD_CUDA(cudaSetDevice(c->cfg.device));
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const size_t kv_elems = (size_t)c->Hkv * n_tokens * kHeadDim;
@@ -413,7 +411,7 @@ kvd_status kvd_load_prefix(kvd_cache* c, int32_t layer, int32_t req, const uint1
         KVD_CUDA(launch_index_build(c, layer, req, n_tokens, s));
     }
     KVD_CUDA(cudaStreamSynchronize(s));
-    c->ntok[(size_t)req] = n_tokens;
+    c->ntok[(size_t)layer * c->R + req] = n_tokens;
     return KVD_OK;
 }
 
@@ -445,6 +443,27 @@ kvd_status kvd_select_resolve_fetch(kvd_cache* c, int32_t layer, const uint16_t*
     if (!q || (!out_ids && k_blocks > 0) || !out_attn) return fail(KVD_EINVAL, "q / out_ids / out_attn is NULL");
     p.step = step;
     return launched(launch_select_resolve(c, p, q, out_ids, out_scores, out_attn, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+kvd_status kvd_append_token(kvd_cache* c, int32_t layer, const int32_t* req_ids, int32_t B, const uint16_t* k,
+                            const uint16_t* v, uint32_t step, kvd_stream stream) {
+    StepParams p;
+    kvd_status st = check_step(c, layer, req_ids, B, 0, &p);
+    if (st) return st;
+    if (!k || !v) return fail(KVD_EINVAL, "k / v is NULL");
+    if (c->index_ratio > 0) return fail(KVD_ESTATE, "append with the hierarchical index needs an index rebuild");
+    if (!c->resident && c->A != c->L) return fail(KVD_ESTATE, "append needs one host layer per layer (host_layer_alias 0)");
+    int32_t n[KVD_MAX_BATCH];
+    for (int b = 0; b < B; ++b) {
+        const int64_t nr = c->ntok[(size_t)layer * c->R + req_ids[b]];
+        if (nr + 1 > c->nmax) return fail(KVD_ERANGE, "request %d: context full (%lld tokens)", req_ids[b], (long long)nr);
+        n[b] = (int32_t)nr;
+    }
+    p.step = step;
+    const cudaError_t e = launch_append(c, p, k, v, n, reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return fail(KVD_ECUDA, "append: %s", cudaGetErrorString(e));
+    for (int b = 0; b < B; ++b) c->ntok[(size_t)layer * c->R + req_ids[b]] += 1;
+    return KVD_OK;
 }
 
 kvd_status kvd_sparse_decode(kvd_cache* c, int32_t layer, const uint16_t* q, const int32_t* req_ids, int32_t B,
@@ -508,10 +527,10 @@ kvd_status kvd_read_summaries(kvd_cache* c, int32_t layer, int32_t req, int32_t 
     kvd_status st = check_seg(c, layer, req, head);
     if (st) return st;
     if (!out) return fail(KVD_EINVAL, "out is NULL");
-    if (c->ntok[(size_t)req] <= 0) return fail(KVD_ESTATE, "request %d not loaded", req);
+    if (c->ntok[(size_t)layer * c->R + req] <= 0) return fail(KVD_ESTATE, "request %d not loaded", req);
     KVD_CUDA(cudaDeviceSynchronize());
     const int64_t seg = ((int64_t)layer * c->R + req) * c->Hkv + head;
-    const int64_t nb = (c->ntok[(size_t)req] + c->P - 1) / c->P;
+    const int64_t nb = (c->ntok[(size_t)layer * c->R + req] + c->P - 1) / c->P;
     std::vector<uint16_t> tmp((size_t)(kHeadDim * c->nb_pad));
     KVD_CUDA(cudaMemcpy(tmp.data(), c->summ + seg * kHeadDim * c->nb_pad, tmp.size() * 2, cudaMemcpyDeviceToHost));
     for (int64_t b = 0; b < nb; ++b)
@@ -525,7 +544,7 @@ kvd_status kvd_read_index(kvd_cache* c, int32_t layer, int32_t req, int32_t head
     if (st) return st;
     if (c->index_ratio <= 0) return fail(KVD_ESTATE, "cache has no hierarchical index");
     if (!nc) return fail(KVD_EINVAL, "nc is NULL");
-    if (c->ntok[(size_t)req] <= 0) return fail(KVD_ESTATE, "request %d not loaded", req);
+    if (c->ntok[(size_t)layer * c->R + req] <= 0) return fail(KVD_ESTATE, "request %d not loaded", req);
     KVD_CUDA(cudaDeviceSynchronize());
     const int64_t seg = ((int64_t)layer * c->R + req) * c->Hkv + head;
     int32_t n = 0;
@@ -538,7 +557,7 @@ kvd_status kvd_read_index(kvd_cache* c, int32_t layer, int32_t req, int32_t head
             for (int j = 0; j < kHeadDim; ++j) centroids[i * kHeadDim + j] = tmp[(size_t)(j * c->nc_pad + i)];
     }
     if (cent_of) {
-        const int64_t nb = (c->ntok[(size_t)req] + c->P - 1) / c->P;
+        const int64_t nb = (c->ntok[(size_t)layer * c->R + req] + c->P - 1) / c->P;
         KVD_CUDA(cudaMemcpy(cent_of, c->cent_of + seg * c->nb_pad, (size_t)nb * 4, cudaMemcpyDeviceToHost));
     }
     return KVD_OK;
@@ -549,10 +568,10 @@ kvd_status kvd_read_minmax(kvd_cache* c, int32_t layer, int32_t req, int32_t hea
     if (st) return st;
     if (c->summary_kind != 1) return fail(KVD_ESTATE, "cache keeps mean-key summaries");
     if (!mn || !mx) return fail(KVD_EINVAL, "NULL argument");
-    if (c->ntok[(size_t)req] <= 0) return fail(KVD_ESTATE, "request %d not loaded", req);
+    if (c->ntok[(size_t)layer * c->R + req] <= 0) return fail(KVD_ESTATE, "request %d not loaded", req);
     KVD_CUDA(cudaDeviceSynchronize());
     const int64_t seg = ((int64_t)layer * c->R + req) * c->Hkv + head;
-    const int64_t nb = (c->ntok[(size_t)req] + c->P - 1) / c->P;
+    const int64_t nb = (c->ntok[(size_t)layer * c->R + req] + c->P - 1) / c->P;
     std::vector<uint16_t> tmp((size_t)(kHeadDim * c->nb_pad));
     for (int which = 0; which < 2; ++which) {
         const uint16_t* src = (which ? c->summ2 : c->summ) + seg * kHeadDim * c->nb_pad;
@@ -568,10 +587,10 @@ kvd_status kvd_read_scores(kvd_cache* c, int32_t layer, int32_t req, int32_t hea
     kvd_status st = check_seg(c, layer, req, head);
     if (st) return st;
     if (!out) return fail(KVD_EINVAL, "out is NULL");
-    if (c->ntok[(size_t)req] <= 0) return fail(KVD_ESTATE, "request %d not loaded", req);
+    if (c->ntok[(size_t)layer * c->R + req] <= 0) return fail(KVD_ESTATE, "request %d not loaded", req);
     KVD_CUDA(cudaDeviceSynchronize());
     const int64_t seg = ((int64_t)layer * c->R + req) * c->Hkv + head;
-    const int64_t nb = (c->ntok[(size_t)req] + c->P - 1) / c->P;
+    const int64_t nb = (c->ntok[(size_t)layer * c->R + req] + c->P - 1) / c->P;
     KVD_CUDA(cudaMemcpy(out, c->scores + seg * c->nb_pad, (size_t)nb * 4, cudaMemcpyDeviceToHost));
     if (c->index_ratio > 0) {                     // lookahead scores: exact if scored, else the centroid's
         std::vector<uint32_t> bits((size_t)c->nb_pad / 32);
@@ -743,7 +762,8 @@ kvd_status kvd_check(kvd_cache* c) {
         KVD_CUDA(cudaMemset(c->err, 0, 4));
         return fail(KVD_EDEVICE, "device flagged bad input (code %d: %s)", e,
                     (e & 1) ? "selection not ascending / out of range / pinned"
-                    : (e & 2) ? "LFU key bounds exceeded" : "hierarchical index candidate bound violated");
+                    : (e & 2) ? "LFU key bounds exceeded"
+                    : (e & 4) ? "hierarchical index candidate bound violated" : "append found no slot");
     }
     return KVD_OK;
 }

@@ -45,7 +45,7 @@ __device__ __forceinline__ uint64_t victim_key(int policy, uint32_t lu, uint8_t 
 }
 
 // Shared state of one segment's resolve (static part; the dynamic part is smraw).
-ResolveBufs resolve_bufs(kvd_cache* c);   // k_resolve.cu
+ResolveBufs resolve_bufs(kvd_cache* c, int layer);   // k_resolve.cu
 
 struct ResolveShared {
     int scan[33];

@@ -788,7 +788,7 @@ inline cudaError_t launch_select_k(kvd_cache* c, const StepParams& p, const uint
     cfg.numAttrs = na;
     count_launch();
     return cudaLaunchKernelEx(&cfg, select_kernel<CL, NT, V, RESOLVE>, fa, p, q, mat, scores,
-                              (const int32_t*)c->ntok_dev, kpt, out_ids, out_scores);
+                              (const int32_t*)c->ntok_dev + (int64_t)p.layer * c->R, kpt, out_ids, out_scores);
 }
 
 template <int NT, bool RESOLVE>

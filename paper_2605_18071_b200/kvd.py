@@ -60,7 +60,7 @@ EXPORTS = ["kvd_required_bytes", "kvd_create_cache", "kvd_destroy_cache", "kvd_g
            "kvd_version", "kvd_set_device_step", "kvd_launch_count",
            "kvd_select_resolve_fetch", "kvd_enable_kernel_timer", "kvd_read_kernel_timer",
            "kvd_probe_zero_copy", "kvd_read_index", "kvd_set_segment_capacity", "kvd_get_segment_stats",
-           "kvd_plan_window_scaling", "kvd_read_minmax"]
+           "kvd_plan_window_scaling", "kvd_read_minmax", "kvd_append_token"]
 
 
 def lib():
@@ -102,6 +102,7 @@ def lib():
             "kvd_get_segment_stats": ([p, p, p], i32),
             "kvd_plan_window_scaling": ([p, p, i32, i32, ctypes.c_double, p], i32),
             "kvd_read_minmax": ([p, i32, i32, i32, p, p], i32),
+            "kvd_append_token": ([p, i32, p, i32, p, p, u32, p], i32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -212,6 +213,11 @@ class KVCache:
         r, B = _reqs(req_ids)
         _check(lib().kvd_select_resolve_fetch(self.h, layer, ptr(q), r.ctypes.data, B, k_blocks, step,
                                               ptr(out_ids), ptr(out_scores), ptr(out_attn), _stream(stream)))
+
+    def append_token(self, layer, req_ids, k, v, step, stream=None):
+        """Decode-time append of one token per request (kvd_append_token); k, v [B][Hkv][128]."""
+        r, B = _reqs(req_ids)
+        _check(lib().kvd_append_token(self.h, layer, r.ctypes.data, B, ptr(k), ptr(v), step, _stream(stream)))
 
     def sparse_decode(self, layer, q, req_ids, attn, W, out, out_lse=None, stream=None):
         r, B = _reqs(req_ids)

@@ -27,7 +27,7 @@ def row_normwise_err(o, ref):
 class Case:
     def __init__(self, *, L=1, B=1, Hq=8, Hkv=2, n=4096, P=16, k=32, C=None, policy="lru", seed=0,
                  alpha=0.9, ragged=False, sink=4, local=64, alias=0, reqs=None, R=None, device=0,
-                 fused=False, index_ratio=0, caps=None, summary="mean"):
+                 fused=False, index_ratio=0, caps=None, summary="mean", extra=0):
         self.fused = fused            # kvd_select_resolve_fetch instead of select_topk + resolve_and_fetch
         self.index_ratio = index_ratio  # hierarchical centroid index (R27); 0 = flat
         self.L, self.B, self.Hq, self.Hkv, self.P, self.k = L, B, Hq, Hkv, P, k
@@ -37,11 +37,12 @@ class Case:
         self.reqs = list(range(B)) if reqs is None else list(reqs)
         R = R if R is not None else max(self.reqs) + 1
         self.n = {r: (n - 17 * r if ragged else n) for r in self.reqs}
-        nb_max = (n + P - 1) // P
+        self.extra = extra                        # decode-time appends this case may make
+        nb_max = (n + extra + P - 1) // P
         self.C = nb_max if C is None else C
         self.alias = alias
         self.cache = KVCache(num_layers=L, num_q_heads=Hq, num_kv_heads=Hkv, block_tokens=P, max_requests=R,
-                             max_context=n, slots_per_segment=self.C, max_select=k, sink_tokens=sink,
+                             max_context=n + extra, slots_per_segment=self.C, max_select=k, sink_tokens=sink,
                              local_tokens=local, policy=policy, host_layer_alias=alias, device=device,
                              index_ratio=index_ratio, summary_kind=summary)
         self.summary = summary
@@ -68,6 +69,8 @@ class Case:
                         self.index[(l, r, h)] = (cent, cent_of, index_ratio)
                     pinned = oracle.pinned_blocks(self.n[r], P, sink, local)
                     self.oc[(l, r, h)] = oracle.SegmentCache(len(pinned), self.caps.get((l, h), self.C), pinned)
+        self.nl = {(l, r): self.n[r] for l in range(L) for r in self.reqs}   # tokens per (layer, request)
+        self.last_scores = {}
         self.ids = torch.empty((B, Hkv, max(k, 1)), dtype=torch.int32, device=self.dev)
         self.sel_scores = torch.empty((B, Hkv, max(k, 1)), dtype=torch.float32, device=self.dev)
         self.attn = torch.empty((B, Hkv, self.W, 2), dtype=torch.int32, device=self.dev)
@@ -102,7 +105,35 @@ class Case:
                 res[(bi, h)] = oracle.segment_step(self.oc[(l, r, h)], qg, self.S[(l, r, h)], K, V, self.P,
                                                    self.k, step, self.pol, self.W,
                                                    index=self.index.get((l, r, h)))
+                self.last_scores[(l, r, h)] = res[(bi, h)]["scores"]
         return res
+
+    def append(self, step):
+        """Decode-time append of the next synthetic token of every request in every layer, on the
+        GPU (kvd_append_token) and in the oracle (O13, with the layer's last select scores)."""
+        import torch as _t
+        for l in range(self.L):
+            src_l = l % self.alias if self.alias else l
+            knew = np.empty((self.B, self.Hkv, 128), np.uint16)
+            vnew = np.empty_like(knew)
+            for bi, r in enumerate(self.reqs):
+                n = self.nl[(l, r)]
+                Kf, Vf = synth.request_kv(self.seed, src_l, r, self.Hkv, n + 1)
+                knew[bi], vnew[bi] = Kf[:, n], Vf[:, n]
+            self.cache.append_token(l, self.reqs, _t.from_numpy(knew.view(np.int16)).to(self.dev),
+                                    _t.from_numpy(vnew.view(np.int16)).to(self.dev), step)
+            for bi, r in enumerate(self.reqs):
+                n = self.nl[(l, r)]
+                for h in range(self.Hkv):
+                    K, V = self.kv[(l, r, h)]
+                    nb = (n + self.P - 1) // self.P
+                    sc = self.last_scores.get((l, r, h), np.zeros(nb, np.float32))
+                    K, V, S, _ = oracle.append_token(self.oc[(l, r, h)], K, V, self.S[(l, r, h)], n, self.P,
+                                                     knew[bi, h], vnew[bi, h], step, self.pol, sc, self.sink,
+                                                     self.local, self.summary)
+                    self.kv[(l, r, h)] = (K, V)
+                    self.S[(l, r, h)] = S
+                self.nl[(l, r)] = n + 1
 
     def compare_layer(self, l, g, o, check_state=True, check_slots=False):
         """Assert parity for one layer's outputs; returns the max attention error."""
@@ -152,7 +183,7 @@ class Case:
         """O7 invariant: every occupied slot holds exactly its block's K/V (from the generator)."""
         K, V = self.kv[(l, r, h)]
         st = self.cache.read_segment(l, r, h)
-        n, P = self.n[r], self.P
+        n, P = self.nl[(l, r)], self.P
         for s, b in enumerate(st["slot_block"]):
             if b < 0:
                 continue
@@ -162,9 +193,11 @@ class Case:
             assert np.array_equal(vv[:cnt], V[P * b:P * b + cnt]), (l, r, h, s, b, "slot V bytes")
             assert not kk[cnt:].any() and not vv[cnt:].any()
 
-    def run(self, steps, t0=0, check_state=True, check_slots_every=0):
+    def run(self, steps, t0=0, check_state=True, check_slots_every=0, append_every=0):
         worst = 0.0
         for t in range(t0, t0 + steps):
+            if append_every and t % append_every == 0:
+                self.append(t + 1)
             for l in range(self.L):
                 q = self.queries(l, t)
                 g = self.gpu_layer(l, q, t + 1)

@@ -309,3 +309,23 @@ def test_minmax_select_parity(n, P, C, policy, fused):
     c = Case(L=1, B=2, Hq=8, Hkv=2, n=n, P=P, k=32, C=C, policy=policy, seed=71, ragged=True, fused=fused,
              summary="minmax")
     c.run(steps=4, check_slots_every=2)
+
+
+# ---- decode-time append (R16, O13): tokens join the local window, new blocks are admitted,
+# summaries follow; selection / slot maps / attention stay bit-exact with the oracle
+@pytest.mark.parametrize("C,policy,fused,summary", [(None, "la", True, "mean"), (60, "la", True, "mean"),
+                                                   (60, "lru", False, "mean"), (70, "lfu", True, "minmax")])
+def test_append_tokens(C, policy, fused, summary):
+    c = Case(L=2, B=2, Hq=8, Hkv=2, n=1000, P=16, k=24, C=C, policy=policy, seed=81, ragged=True, fused=fused,
+             summary=summary, extra=48)
+    c.run(steps=40, append_every=1, check_slots_every=5)
+    assert all(v == c.n[r] + 40 for (l, r), v in c.nl.items())
+
+
+def test_append_errors():
+    c = Case(L=1, B=1, Hq=8, Hkv=2, n=500, P=16, k=8, C=40, seed=82, extra=1)
+    c.append(1)
+    k = torch.zeros((1, 2, 128), dtype=torch.int16, device="cuda")
+    with pytest.raises(KVDError) as e:
+        c.cache.append_token(0, [0], k, k, 2)                    # context full
+    assert e.value.status == "KVD_ERANGE"
