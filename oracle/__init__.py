@@ -206,6 +206,48 @@ def append_token(cache, K, V, S, n, P, k_new, v_new, step, policy, scores, sink=
     return K, V, S, pinned
 
 
+def warm_importance(q_obs, K, P):
+    """O14: importance of every block of a segment from the prompt's final
+    observation window -- "for each query within this window, we compute its attention weights
+    over all prefix keys and aggregate them across heads" -- in fp64 from the bf16 inputs:
+    I_b = sum over the G x n_obs queries q of sum over tokens t of block b of softmax_t(q.K_t / sqrt(d)).
+    q_obs [G][n_obs][d], K [n][d] bf16 bits -> I [nb] float64."""
+    Q = _f64(q_obs).reshape(-1, q_obs.shape[-1])
+    Kf = _f64(K)
+    z = Q @ Kf.T / np.sqrt(Kf.shape[1])
+    w = np.exp(z - z.max(axis=1, keepdims=True))
+    w /= w.sum(axis=1, keepdims=True)
+    tok = w.sum(axis=0)
+    nb = (Kf.shape[0] + P - 1) // P
+    return np.array([tok[P * b:P * b + P].sum() for b in range(nb)])
+
+
+def warm_start(cache, importance):
+    """O14 placement (reading R29): a host-backed segment cache starts with its C - pinned most
+    important non-pinned blocks resident (importance desc, block id asc), in the slots after the
+    pinned blocks, ascending by block id; last use 0, phase 1, count 1.  A fully resident cache is
+    unchanged."""
+    nb, C = cache.nb, cache.C
+    if C >= nb:
+        return np.zeros(0, np.int32)
+    pin = cache.is_pinned.astype(bool)
+    cand = np.nonzero(~pin)[0]
+    room = C - int(pin.sum())
+    order = np.lexsort((cand, -importance[cand]))
+    chosen = np.sort(cand[order[:room]]).astype(np.int32)
+    s = int(pin.sum())
+    for b in chosen:
+        cache.table[b] = s
+        cache.slot_block[s] = b
+        cache.last_use[s], cache.phase[s], cache.use_count[s] = 0, 1, 1
+        s += 1
+    return chosen
+
+
+def _f64(bits):
+    return (np.asarray(bits, np.uint16).astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+
+
 def fetch(host_records, slot_pool, miss, n_miss):
     """O7: slot_pool[slot] := host_records[block] for each miss (in place)."""
     assert host_records.flags.c_contiguous and slot_pool.flags.c_contiguous
