@@ -160,6 +160,16 @@ kvd_status kvd_load_prefix(kvd_cache* c, int32_t layer, int32_t req,
                            const uint16_t* k, const uint16_t* v, int64_t n_tokens,
                            kvd_stream stream);
 
+/* Importance-guided warm-up (R29): kvd_load_prefix, then for a
+ * host-backed cache the C - pinned non-pinned blocks with the highest attention mass from the
+ * prompt's final observation window start resident (instead of a cold cache): importance of block
+ * b = sum over the G x n_obs observation queries of its tokens' softmax weights over the whole
+ * prefix (fp32); ties -> lower block; placed after the pinned blocks, ascending by block, as
+ * admitted at step 0 (last use 0, phase 1, count 1).  q_obs: bf16 [Hq][n_obs][128] (host or
+ * device), n_obs <= 16 and G x n_obs <= 128.  A fully resident cache ignores it. */
+kvd_status kvd_load_prefix_obs(kvd_cache* c, int32_t layer, int32_t req, const uint16_t* k, const uint16_t* v,
+                               int64_t n_tokens, const uint16_t* q_obs, int32_t n_obs, kvd_stream stream);
+
 /* (1) Select.  q: device bf16 [B][Hq][128].  req_ids: host int32 [B] (distinct,
  * loaded).  For each request b and KV head h: qbar = fp32 sum of the group's
  * G query heads (g ascending); score_j = sequential fp32 FMA chain over the 128
@@ -251,6 +261,8 @@ kvd_status kvd_read_host_record(kvd_cache* c, int32_t layer, int32_t req, int32_
 /* Copy a segment's summaries as [nb][128] bf16 (block-major, unpadded). */
 kvd_status kvd_read_summaries(kvd_cache* c, int32_t layer, int32_t req, int32_t head,
                               uint16_t* out);
+/* Block importances [nb] of `head` computed by the last kvd_load_prefix_obs (setup scratch). */
+kvd_status kvd_read_warm_importance(kvd_cache* c, int32_t head, int64_t nb, float* out);
 /* Quest min/max summaries of a segment (summary_kind 1): mn, mx [nb][128] bf16, block-major. */
 kvd_status kvd_read_minmax(kvd_cache* c, int32_t layer, int32_t req, int32_t head, uint16_t* mn, uint16_t* mx);
 /* Hierarchical index of one segment (index_ratio > 0): *nc receives the centroid count;

@@ -92,6 +92,7 @@ struct kvd_cache {
     int32_t* csel = nullptr;               // [R][Hkv][m_max] stage-1 selection (scratch)
     uint32_t* cand_bits = nullptr;         // [L][R][Hkv][nb_pad / 32] last step's stage-2 candidates
     uint8_t* idx_stage = nullptr;          // setup scratch of the index build
+    float* warm_imp = nullptr;             // setup scratch of the importance warm-up [Hkv][nb_max]
     // 2D window scaling (R28): per layer-head capacity; per layer-head selection / miss counters
     std::vector<int64_t> cap_host;         // [L][Hkv]
     int32_t* cap_dev = nullptr;            // [L][Hkv]
@@ -107,6 +108,7 @@ struct kvd_cache {
     // setup staging (lazily allocated)
     uint16_t* stage_kv = nullptr;
     uint8_t* stage_rec = nullptr;
+    uint16_t* stage_q = nullptr;                 // observation-window queries (warm-up)
     // host
     uint8_t* host_store = nullptr;          // pinned, mapped (UVA: same pointer on device)
     std::vector<int64_t> ntok;              // host copy of the token counts [L][R] (kvd_append_token grows them)
@@ -115,7 +117,9 @@ struct kvd_cache {
 namespace kvd {
 // launchers (return cudaGetLastError())
 cudaError_t launch_prefix(kvd_cache* c, int layer, int req, const uint16_t* dk, const uint16_t* dv, int64_t n,
-                          cudaStream_t s);
+                          cudaStream_t s, const uint16_t* dq_obs = nullptr, int n_obs = 0);
+cudaError_t launch_warm(kvd_cache* c, int layer, int req, const uint16_t* dk, const uint16_t* dq, int n_obs, int64_t n,
+                        int32_t* slot_of, cudaStream_t s);                                  // k_warm.cu
 cudaError_t launch_select(kvd_cache* c, const StepParams& p, const uint16_t* q, int32_t* out_ids, float* out_scores,
                           cudaStream_t s);
 size_t resolve_smem_bytes(int64_t nkeys, int64_t kmax, int64_t nb_pad);   // k_resolve.cu

@@ -129,7 +129,7 @@ __global__ void table_init_kernel(int32_t* __restrict__ table_lr, int32_t* __res
 __global__ void set_ntok_kernel(int32_t* ntok, int req, int32_t n) { ntok[req] = n; }
 
 cudaError_t launch_prefix(kvd_cache* c, int layer, int req, const uint16_t* dk, const uint16_t* dv, int64_t n,
-                          cudaStream_t s) {
+                          cudaStream_t s, const uint16_t* dq_obs, int n_obs) {
     const int64_t sl = ((int64_t)layer * c->R + req) * c->Hkv;      // first segment of (layer, req)
     SegGeom g = seg_geom(n, c->P, c->cfg.sink_tokens, c->cfg.local_tokens);
     summary_kernel<<<dim3((unsigned)(c->nb_pad / 32), c->Hkv), 128, 0, s>>>(
@@ -141,6 +141,10 @@ cudaError_t launch_prefix(kvd_cache* c, int layer, int req, const uint16_t* dk, 
                                              c->last_use + sl * c->C, c->phase + sl * c->C,
                                              c->use_count + sl * c->C, slot_of, c->nb_pad, c->C, g,
                                              c->resident ? 1 : 0);
+    if (dq_obs && n_obs > 0 && !c->resident) {    // importance-guided warm-up (k_warm.cu, R29)
+        cudaError_t e = launch_warm(c, layer, req, dk, dq_obs, n_obs, n, slot_of, s);
+        if (e != cudaSuccess) return e;
+    }
     dim3 rg((unsigned)g.nb, c->Hkv);
     // resident blocks / pinned blocks -> their slots
     record_kernel<<<rg, 128, 0, s>>>(dk, dv, n, c->P, c->slots + sl * c->C * c->rec_bytes, c->C, (int)c->rec_bytes,

@@ -351,7 +351,7 @@ void kvd_destroy_cache(kvd_cache* c) {
     cudaDeviceSynchronize();
     void* dev[] = {c->slots, c->summ, c->scores, c->table, c->slot_block, c->last_use, c->phase,
                    c->use_count, c->miss, c->miss_count, c->kt_slots, c->kt_acc, c->summ2, c->cap_dev, c->seg_stats, c->cent, c->cscores, c->ncent, c->cent_of, c->memb, c->moff, c->csel, c->cand_bits, c->idx_stage, c->stats,
-                   c->err, c->ntok_dev, c->zero_rec, c->stage_kv, c->stage_rec};
+                   c->err, c->ntok_dev, c->zero_rec, c->stage_kv, c->stage_rec, c->stage_q, c->warm_imp};
     for (void* p : dev)
         if (p) cudaFree(p);
     if (c->host_store) cudaFreeHost(c->host_store);
@@ -378,8 +378,8 @@ kvd_status kvd_get_info(const kvd_cache* c, kvd_cache_info* out) {
 
 int32_t kvd_attn_width(const kvd_cache* c, int32_t k_blocks) { return c ? k_blocks + c->pmax : -1; }
 
-kvd_status kvd_load_prefix(kvd_cache* c, int32_t layer, int32_t req, const uint16_t* k, const uint16_t* v,
-                           int64_t n_tokens, kvd_stream stream) {
+static kvd_status load_prefix_impl(kvd_cache* c, int32_t layer, int32_t req, const uint16_t* k, const uint16_t* v,
+                                   int64_t n_tokens, const uint16_t* q_obs, int32_t n_obs, kvd_stream stream) {
     if (!c || !k || !v) return fail(KVD_EINVAL, "NULL argument");
     if (layer < 0 || layer >= c->L) return fail(KVD_EINVAL, "layer %d out of range", layer);
     if (req < 0 || req >= c->R) return fail(KVD_EINVAL, "req %d out of range", req);
@@ -405,7 +405,21 @@ kvd_status kvd_load_prefix(kvd_cache* c, int32_t layer, int32_t req, const uint1
         KVD_CUDA(cudaMemcpyAsync(c->stage_kv + kv_elems, v, kv_elems * 2, cudaMemcpyHostToDevice, s));
         dv = c->stage_kv + kv_elems;
     }
-    KVD_CUDA(launch_prefix(c, layer, req, dk, dv, n_tokens, s));
+    const uint16_t* dq = nullptr;
+    if (q_obs && n_obs > 0 && !c->resident) {
+        if (n_obs > 16 || c->G * n_obs > 128) return fail(KVD_EINVAL, "n_obs=%d: at most 16 (and G x n_obs <= 128)", n_obs);
+        const size_t qbytes = (size_t)c->Hq * n_obs * kHeadDim * 2;
+        if (!c->stage_q) KVD_CUDA(dalloc(&c->stage_q, (size_t)c->Hq * 16 * kHeadDim * 2));
+        cudaPointerAttributes aq{};
+        KVD_CUDA(cudaPointerGetAttributes(&aq, q_obs));
+        if (aq.type != cudaMemoryTypeDevice && aq.type != cudaMemoryTypeManaged) {
+            KVD_CUDA(cudaMemcpyAsync(c->stage_q, q_obs, qbytes, cudaMemcpyHostToDevice, s));
+            dq = c->stage_q;
+        } else {
+            dq = q_obs;
+        }
+    }
+    KVD_CUDA(launch_prefix(c, layer, req, dk, dv, n_tokens, s, dq, dq ? n_obs : 0));
     if (c->index_ratio > 0) {                     // hierarchical index over the new summaries (R27)
         if (!c->idx_stage) KVD_CUDA(dalloc(&c->idx_stage, index_stage_bytes(c->Hkv, c->nb_pad)));
         KVD_CUDA(launch_index_build(c, layer, req, n_tokens, s));
@@ -413,6 +427,17 @@ kvd_status kvd_load_prefix(kvd_cache* c, int32_t layer, int32_t req, const uint1
     KVD_CUDA(cudaStreamSynchronize(s));
     c->ntok[(size_t)layer * c->R + req] = n_tokens;
     return KVD_OK;
+}
+
+kvd_status kvd_load_prefix(kvd_cache* c, int32_t layer, int32_t req, const uint16_t* k, const uint16_t* v,
+                           int64_t n_tokens, kvd_stream stream) {
+    return load_prefix_impl(c, layer, req, k, v, n_tokens, nullptr, 0, stream);
+}
+
+kvd_status kvd_load_prefix_obs(kvd_cache* c, int32_t layer, int32_t req, const uint16_t* k, const uint16_t* v,
+                               int64_t n_tokens, const uint16_t* q_obs, int32_t n_obs, kvd_stream stream) {
+    if (!q_obs || n_obs < 1) return fail(KVD_EINVAL, "q_obs / n_obs");
+    return load_prefix_impl(c, layer, req, k, v, n_tokens, q_obs, n_obs, stream);
 }
 
 kvd_status kvd_select_topk(kvd_cache* c, int32_t layer, const uint16_t* q, const int32_t* req_ids, int32_t B,
@@ -560,6 +585,14 @@ kvd_status kvd_read_index(kvd_cache* c, int32_t layer, int32_t req, int32_t head
         const int64_t nb = (c->ntok[(size_t)layer * c->R + req] + c->P - 1) / c->P;
         KVD_CUDA(cudaMemcpy(cent_of, c->cent_of + seg * c->nb_pad, (size_t)nb * 4, cudaMemcpyDeviceToHost));
     }
+    return KVD_OK;
+}
+
+kvd_status kvd_read_warm_importance(kvd_cache* c, int32_t head, int64_t nb, float* out) {
+    if (!c || !out || head < 0 || head >= c->Hkv || nb < 1 || nb > c->nb_max) return fail(KVD_EINVAL, "bad arguments");
+    if (!c->warm_imp) return fail(KVD_ESTATE, "no warm-up has run");
+    KVD_CUDA(cudaDeviceSynchronize());
+    KVD_CUDA(cudaMemcpy(out, c->warm_imp + (int64_t)head * nb, (size_t)nb * 4, cudaMemcpyDeviceToHost));
     return KVD_OK;
 }
 

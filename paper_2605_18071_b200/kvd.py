@@ -60,7 +60,8 @@ EXPORTS = ["kvd_required_bytes", "kvd_create_cache", "kvd_destroy_cache", "kvd_g
            "kvd_version", "kvd_set_device_step", "kvd_launch_count",
            "kvd_select_resolve_fetch", "kvd_enable_kernel_timer", "kvd_read_kernel_timer",
            "kvd_probe_zero_copy", "kvd_read_index", "kvd_set_segment_capacity", "kvd_get_segment_stats",
-           "kvd_plan_window_scaling", "kvd_read_minmax", "kvd_append_token"]
+           "kvd_plan_window_scaling", "kvd_read_minmax", "kvd_append_token", "kvd_load_prefix_obs",
+           "kvd_read_warm_importance"]
 
 
 def lib():
@@ -103,6 +104,8 @@ def lib():
             "kvd_plan_window_scaling": ([p, p, i32, i32, ctypes.c_double, p], i32),
             "kvd_read_minmax": ([p, i32, i32, i32, p, p], i32),
             "kvd_append_token": ([p, i32, p, i32, p, p, u32, p], i32),
+            "kvd_load_prefix_obs": ([p, i32, i32, p, p, i64, p, i32, p], i32),
+            "kvd_read_warm_importance": ([p, i32, i64, p], i32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -118,13 +121,18 @@ def _check(code):
 
 
 def ptr(x):
-    """Raw address of a torch tensor, numpy array, int or None."""
+    """Raw address of a C-contiguous torch tensor or numpy array, an int, or None (a strided
+    view raises: the C ABI takes dense arrays)."""
     if x is None:
         return None
     if isinstance(x, int):
         return x
     if isinstance(x, np.ndarray):
+        if not x.flags["C_CONTIGUOUS"]:
+            raise ValueError("array is not C-contiguous (np.ascontiguousarray it)")
         return x.ctypes.data
+    if not x.is_contiguous():
+        raise ValueError("tensor is not contiguous")
     return x.data_ptr()
 
 
@@ -193,8 +201,14 @@ class KVCache:
         _check(lib().kvd_set_device_step(self.h, ptr(dev_step)))
 
     # ------------------------------------------------------------ setup
-    def load_prefix(self, layer, req, k, v, n_tokens, stream=None):
-        _check(lib().kvd_load_prefix(self.h, layer, req, ptr(k), ptr(v), n_tokens, _stream(stream)))
+    def load_prefix(self, layer, req, k, v, n_tokens, stream=None, q_obs=None):
+        """kvd_load_prefix; with q_obs [Hq][n_obs][128] the importance-guided warm-up
+        (kvd_load_prefix_obs)."""
+        if q_obs is None:
+            _check(lib().kvd_load_prefix(self.h, layer, req, ptr(k), ptr(v), n_tokens, _stream(stream)))
+        else:
+            _check(lib().kvd_load_prefix_obs(self.h, layer, req, ptr(k), ptr(v), n_tokens, ptr(q_obs),
+                                             int(q_obs.shape[1]), _stream(stream)))
 
     # ------------------------------------------------------------ step
     def select_topk(self, layer, q, req_ids, k_blocks, out_ids, out_scores=None, stream=None):
@@ -247,6 +261,12 @@ class KVCache:
     def read_summaries(self, layer, req, head, nb):
         out = np.empty((nb, 128), np.uint16)
         _check(lib().kvd_read_summaries(self.h, layer, req, head, ptr(out)))
+        return out
+
+    def read_warm_importance(self, head, nb):
+        """Block importances of the last warm-up (kvd_read_warm_importance)."""
+        out = np.empty(nb, np.float32)
+        _check(lib().kvd_read_warm_importance(self.h, head, nb, ptr(out)))
         return out
 
     def read_minmax(self, layer, req, head, nb):

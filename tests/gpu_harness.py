@@ -27,7 +27,7 @@ def row_normwise_err(o, ref):
 class Case:
     def __init__(self, *, L=1, B=1, Hq=8, Hkv=2, n=4096, P=16, k=32, C=None, policy="lru", seed=0,
                  alpha=0.9, ragged=False, sink=4, local=64, alias=0, reqs=None, R=None, device=0,
-                 fused=False, index_ratio=0, caps=None, summary="mean", extra=0):
+                 fused=False, index_ratio=0, caps=None, summary="mean", extra=0, warm_obs=0):
         self.fused = fused            # kvd_select_resolve_fetch instead of select_topk + resolve_and_fetch
         self.index_ratio = index_ratio  # hierarchical centroid index (R27); 0 = flat
         self.L, self.B, self.Hq, self.Hkv, self.P, self.k = L, B, Hq, Hkv, P, k
@@ -59,7 +59,14 @@ class Case:
             for r in self.reqs:
                 src_l = l % alias if alias else l
                 K, V = synth.request_kv(seed, src_l, r, Hkv, self.n[r])
-                self.cache.load_prefix(l, r, K, V, self.n[r])
+                qobs = None
+                if warm_obs:
+                    # the prompt's observation window: the query stream's first n_obs steps (the
+                    # decode queries continue that stream, AR(1) temporal locality)
+                    qobs = np.ascontiguousarray(np.concatenate(
+                        [synth.queries(seed, l, r, h, self.G, nsteps=warm_obs, alpha=alpha).transpose(1, 0, 2)
+                         for h in range(Hkv)], axis=0))                           # [Hq][n_obs][128]
+                self.cache.load_prefix(l, r, K, V, self.n[r], q_obs=qobs)
                 for h in range(Hkv):
                     self.kv[(l, r, h)] = (K[h], V[h])
                     self.S[(l, r, h)] = (oracle.block_summaries(K[h], P) if summary == "mean"
@@ -69,6 +76,9 @@ class Case:
                         self.index[(l, r, h)] = (cent, cent_of, index_ratio)
                     pinned = oracle.pinned_blocks(self.n[r], P, sink, local)
                     self.oc[(l, r, h)] = oracle.SegmentCache(len(pinned), self.caps.get((l, h), self.C), pinned)
+                    if warm_obs:
+                        imp = oracle.warm_importance(qobs[h * self.G:(h + 1) * self.G], K[h], P)
+                        oracle.warm_start(self.oc[(l, r, h)], imp)
         self.nl = {(l, r): self.n[r] for l in range(L) for r in self.reqs}   # tokens per (layer, request)
         self.last_scores = {}
         self.ids = torch.empty((B, Hkv, max(k, 1)), dtype=torch.int32, device=self.dev)

@@ -329,3 +329,20 @@ def test_append_errors():
     with pytest.raises(KVDError) as e:
         c.cache.append_token(0, [0], k, k, 2)                    # context full
     assert e.value.status == "KVD_ERANGE"
+
+
+# ---- importance-guided warm-up (R29, O14): the initial residency is the oracle's (slot map
+# bit-exact right after the prefix load), then every step as usual; warm starts miss less
+@pytest.mark.parametrize("policy,fused,caps", [("la", True, None), ("lru", False, {(0, 1): 40})])
+def test_warm_start(policy, fused, caps):
+    c = Case(L=1, B=2, Hq=8, Hkv=2, n=6000, P=16, k=24, C=69, policy=policy, seed=91, ragged=True, fused=fused,
+             warm_obs=16, caps=caps)
+    for (l, r, h), oc in c.oc.items():
+        st = c.cache.read_segment(l, r, h)
+        assert np.array_equal(st["slot_block"][:len(oc.slot_block)], oc.slot_block), (l, r, h, "warm slot map")
+        assert np.array_equal(st["table"][:oc.nb], oc.table), (l, r, h, "warm table")
+    c.run(steps=6, check_slots_every=3)
+    cold = Case(L=1, B=2, Hq=8, Hkv=2, n=6000, P=16, k=24, C=69, policy=policy, seed=91, ragged=True, fused=fused,
+                caps=caps)
+    cold.run(steps=6, check_state=False)
+    assert c.cache.stats()["misses"] < cold.cache.stats()["misses"]
