@@ -400,6 +400,9 @@ static cudaError_t launch_attn_s(kvd_cache* c, const StepParams& p, const uint16
     Work wk;
     wk.TS = (p.W + p.E - 1) / p.E;
     wk.NP = attn_pieces(wk.TS);
+#ifdef KVD_EXPERIMENTS
+    if (const char* e = getenv("KVD_ATTN_NP")) wk.NP = std::max(4, std::min(kMaxPieces, atoi(e) / 4 * 4));   // tuning only
+#endif
     AttnBufs ab{c->slots, c->ntok_dev + (int64_t)p.layer * c->R, c->zero_rec};   // token counts of this layer
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(wk.NP / kAttnWarpsPerCta), (unsigned)(p.B * p.Hkv));

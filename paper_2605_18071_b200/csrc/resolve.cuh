@@ -117,6 +117,34 @@ __device__ inline int resolve_main(const StepParams& p, const ResolveBufs& rb, i
         if (tid == 0) rb.miss_count[rs] = 0;
         return 0;
     }
+    if (rb.nkeys == 0) {
+        // ---- fully resident (R14): block b lives in slot b and every selected block hits -- no
+        //      scans: metadata stores, counters, then the attention list
+        const uint32_t step = p.step_dev ? *p.step_dev : p.step;
+        for (int i = tid; i < k; i += blockDim.x) {
+            const int32_t s = S[i];
+            lu[s] = step;
+            ph[s] = 0;
+            atomicAdd(&uc[s], 1u);
+        }
+        if (tid == 0) {
+            rb.miss_count[rs] = 0;
+            atomicAdd(&rb.stats[0], (unsigned long long)k);
+            atomicAdd(&rb.stats[1], (unsigned long long)k);
+            atomicAdd(&rb.stats[3], (unsigned long long)(ns + nl));
+            if (rb.seg_stats) atomicAdd(&rb.seg_stats[((int64_t)p.layer * p.Hkv + h) * 2], (unsigned long long)k);
+        }
+        if (launch_dependents) griddep_launch();
+        for (int i = tid; i < p.W; i += blockDim.x) {
+            int32_t b = -1;
+            if (i < ns) b = i;
+            else if (i < ns + k) b = S[i - ns];
+            else if (i < ns + k + nl) b = g.local_begin + (i - ns - k);
+            attn[2 * i] = b;
+            attn[2 * i + 1] = b;
+        }
+        return 0;
+    }
     // ---- 2. hits / misses (misses compacted in ascending order)
     int nm_total = 0;
     for (int base = 0; base < k; base += blockDim.x) {
