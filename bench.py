@@ -75,9 +75,9 @@ CONFIGS = {
 METRIC = "decode tokens/s at 128k ctx; sparse-attn HBM GB/s % peak; fetch GB/s, 1-8 GPU"
 RECORD = 8192           # bytes of one 16-token K||V block record (bf16)
 SUMMARY = 256           # bytes of one block summary (128 bf16)
-KINDS = ("select", "resolve", "gather", "attn")
-KIND_NAMES = {"select": "select_kernel (a1+a2; fused: +a3+a4)", "resolve": "resolve_kernel (a3)",
-              "gather": "gather_kernel (a4)", "attn": "attn_kernel (a5+a6)"}
+KINDS = ("score", "select", "resolve", "gather", "attn")
+KIND_NAMES = {"score": "score_kernel (a1)", "select": "select_kernel (a2; fused: +a3+a4)",
+              "resolve": "resolve_kernel (a3)", "gather": "gather_kernel (a4)", "attn": "attn_kernel (a5+a6)"}
 
 
 def parse(argv=None):
@@ -148,6 +148,10 @@ def per_segment_bytes(cfg, misses_per_seg=0.0, victims=True):
     resident = C >= nb
     return dict(
         select=SUMMARY * sel_blocks + 2 * G * 128 + 8 * k,  # summaries (or centroids + members) + q + ids
+        # the kernels of the select call: score_kernel streams the summaries and writes fp32 scores;
+        # select_kernel ranks them from L2 and writes the ids
+        score=SUMMARY * sel_blocks + 2 * G * 128 + 4 * nb,
+        topk=8 * k,
         resolve=4 * k + (0 if resident or not victims else 13 * C + 4 * C),   # table probes + victim scan (LA)
         attn=RECORD * (k + p) + 2 * G * 128 + 4 * G * 128 + 4 * G,   # K/V pages + q + o + lse
         fetch=RECORD * misses_per_seg,                     # host link read (and HBM write)
@@ -280,7 +284,9 @@ class Runner:
         # queries for every step of the run: [T][L][B][Hq][128]; layer l follows the key topics
         # of its K/V (synthetic layer l % A) with its own random streams (stream layer l)
         self.fill = max(1, args.fill if args.fill is not None else (1 if self.resident else max(4, 2 * C // k)))
-        self.T = min(self.fill + args.warmup + 3 * args.steps + 2, 256)
+        # one query row per step of the whole run (fill, warm-up, timed, kernel-timer, isolated and
+        # e2e passes): no step replays an earlier step's queries, so no pass sees an artificial hit
+        self.T = self.fill + args.warmup + 4 * args.steps + 8
         Hkv_all = cfg["Hkv"]
         qh = np.stack([synth.batch_queries(args.seed, l % self.A, self.greqs, Hkv_all, G, t0=0, nsteps=self.T,
                                            alpha=args.alpha, stream_layer=l)[:, :, self.h0 * G:(self.h0 + Hkv) * G]
@@ -496,9 +502,12 @@ def run_gpu(args):
         e = {"kernel": KIND_NAMES[kind], "launches_per_step": nl / args.steps, "avg_launch_us": avg_ms * 1e3,
              "busy_ms_per_step": ns * 1e-6 / args.steps, "segments_per_launch": segs_per_launch}
         e["busy_share"] = e["busy_ms_per_step"] / ms_timer         # > 1 when launches of chains overlap
-        if kind == "select":
-            by = b["select"] + (b["resolve"] if R.fused else 0)
+        if kind == "score":
+            e["hbm_bytes_per_launch"] = b["score"] * segs_per_launch
+        elif kind == "select":
+            by = b["topk"] + (b["resolve"] if R.fused else 0)
             e["hbm_bytes_per_launch"] = by * segs_per_launch
+            e["note"] = "ranks the scores from L2 (4 B per block); HBM bytes: ids (+ resolve)"
             if R.fused and link:
                 e["host_bytes_per_launch"] = RECORD * misses_per_seg * segs_per_launch
         elif kind == "attn":
@@ -581,7 +590,8 @@ def run_gpu(args):
         R.chains, R.chain_streams = saved
         R.prepare_graph(s)
         iso = {"ms_per_step": ms_iso, "chains": 1}
-        for kind, by in (("select", b["select"] + (b["resolve"] if R.fused else 0)), ("attn", b["attn"])):
+        for kind, by in (("score", b["score"]), ("select", b["topk"] + (b["resolve"] if R.fused else 0)),
+                         ("attn", b["attn"])):
             ns, nl = kti[kind]
             if nl:
                 us = ns / nl * 1e-3

@@ -302,8 +302,8 @@ kvd_status kvd_plan_window_scaling(const double* benefit, const double* cost, in
  * atomics per CTA (per warp for attention).  kvd_enable_kernel_timer synchronises and zeroes
  * the accumulators (allocating on first use); enable = 0 stops recording.  Step calls capture
  * the on/off state when they are issued (or captured into a graph).
- * kvd_read_kernel_timer synchronises and copies ns[4] (summed launch durations) and
- * launches[4] (counts). */
+ * kvd_read_kernel_timer synchronises and copies ns[5] (summed launch durations) and
+ * launches[5] (counts), by kernel kind: select, resolve, gather, attention, score. */
 kvd_status kvd_enable_kernel_timer(kvd_cache* c, int32_t enable);
 /* Host-link probe (measurement; the gather's denominator): copy `bytes` (a
  * multiple of 16) from pinned host memory `host` to device memory `dev` with the miss gather's

@@ -198,7 +198,7 @@ constexpr int kExpUnits = 16384, kExpPhases = 8;
     do {                        \
     } while (0)
 #endif
-enum { kKtSelect = 0, kKtResolve = 1, kKtGather = 2, kKtAttn = 3, kKtKinds = 4 };
+enum { kKtSelect = 0, kKtResolve = 1, kKtGather = 2, kKtAttn = 3, kKtScore = 4, kKtKinds = 5 };
 
 // Process-wide count of step-kernel launches issued by libkvd (kvd_launch_count;
 // a launch recorded into a CUDA graph counts once, at capture).

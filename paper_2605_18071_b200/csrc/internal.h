@@ -53,6 +53,7 @@ struct StepParams {
     int32_t sel_stride;               // stage 1: output stride per segment (m_max)
     const int32_t* sel_count;         // stage 1: centroids per segment [L][R][Hkv]
     const uint16_t* summ2;            // Quest min/max summaries (sel_mode 2): the maximum matrix
+    int32_t prescored;                // select_kernel: scores come from score_kernel (k_score.cu) via L2
     int32_t req[KVD_MAX_BATCH];
 };
 
@@ -125,7 +126,8 @@ cudaError_t launch_select(kvd_cache* c, const StepParams& p, const uint16_t* q, 
 size_t resolve_smem_bytes(int64_t nkeys, int64_t kmax, int64_t nb_pad);   // k_resolve.cu
 size_t resolve_static_smem();                                               // k_resolve.cu
 void select_geometry(int64_t nb_pad, int segs, bool resident, int* nt, int* cl, int* kpt, int* v);   // k_select.cu
-size_t select_smem_bytes(int nt, int kpt);                                  // k_select.cu (dynamic)
+size_t select_smem_bytes(int nt, int kpt, int cl, int64_t kb);              // k_select.cu (dynamic)
+bool select_fast_ok(int cl, int64_t span, int64_t kb);                      // k_select.cu
 size_t select_static_smem();                                                // k_select.cu
 constexpr size_t kMaxSmemBytes = 227 * 1024;
 cudaError_t launch_resolve(kvd_cache* c, const StepParams& p, const int32_t* ids, int32_t* out_attn, cudaStream_t s);
@@ -144,6 +146,8 @@ cudaError_t launch_shrink_capacity(kvd_cache* c, int layer, int head, int64_t ca
 cudaError_t launch_append(kvd_cache* c, const StepParams& p, const uint16_t* k, const uint16_t* v, const int32_t* n,
                           cudaStream_t s);                                                  // k_append.cu
 cudaError_t launch_zero_copy(const void* host, void* dev, size_t bytes, int ctas, cudaStream_t s);
+cudaError_t launch_score(kvd_cache* c, const StepParams& p, const uint16_t* q, const uint16_t* mat,
+                         const uint16_t* mat2, float* scores, cudaStream_t s);                // k_score.cu
 cudaError_t launch_select_resolve(kvd_cache* c, const StepParams& p, const uint16_t* q, int32_t* out_ids,
                                   float* out_scores, int32_t* out_attn, cudaStream_t s);
 cudaError_t launch_attention(kvd_cache* c, const StepParams& p, const uint16_t* q, const int32_t* attn, float* out,

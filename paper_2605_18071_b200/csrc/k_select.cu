@@ -47,29 +47,78 @@ void select_geometry(int64_t nb_pad, int segs, bool resident, int* nt, int* cl, 
     *v = vw;
 }
 
-// dynamic shared memory: [span] keys | [kListCap] compacted pairs | [span] first-digit bins
-size_t select_smem_bytes(int nt, int kpt) { return (size_t)nt * kpt * 5 + (size_t)kListCap * 8; }
+// Geometry of the select kernel behind score_kernel (p.prescored): it only ranks scores from L2,
+// so a segment takes the fewest CTAs whose shared memory holds its keys (<= kMaxKpt per thread;
+// KVD_SELECT_PRE_SPAN in experiment builds caps the span), 512 threads up to 2048 blocks.
+void select_geometry_pre(int64_t nb_pad, int* nt, int* cl, int* kpt, int* v) {
+    static const int max_span = tune("KVD_SELECT_PRE_SPAN", 1024 * kMaxKpt),
+                     nt_small = tune("KVD_SELECT_NT_SMALL", 512), nt_large = tune("KVD_SELECT_NT_LARGE", 1024);
+    int c = 1;
+    while (c < 8 && (nb_pad + c - 1) / c > max_span) c <<= 1;
+    const int64_t span = (nb_pad + c - 1) / c;
+    const int threads = span <= 2048 ? nt_small : nt_large;
+    int64_t per = (span + threads - 1) / threads;
+    per = (per + 1) / 2 * 2;
+    *nt = threads;
+    *cl = c;
+    *kpt = (int)(per < 2 ? 2 : per);
+    *v = 2;
+}
 
-size_t select_static_smem() { return sizeof(TopkShared) + sizeof(ResolveShared) + sizeof(float) * kHeadDim; }
+// The default selection (select_fast) gathers up to min(K, span) candidates per CTA on rank 0 of
+// a cluster: at most kCandMax rank keys (64 KiB).  Larger K x cluster products take the general
+// path.
+constexpr int64_t kCandMax = 8192;
+size_t select_static_smem();
+bool select_fast_ok(int cl, int64_t span, int64_t kb) {
+    if (cl > 1 && cl * std::min(kb, span) > kCandMax) return false;
+    const size_t fast = (size_t)span * 4 + (size_t)kRankList * 8 + (cl > 1 ? 8 * (size_t)cl * std::min(kb, span) : 0);
+    return fast + 16 + 4 * (size_t)kb + select_static_smem() <= kMaxSmemBytes;
+}
 
+// dynamic shared memory: general path [span] keys | [kListCap] compacted pairs | [span] first-digit
+// bins; default path [span] keys | [kRankList] rank keys | [CL * min(K, span)] candidates (CL > 1).
+// (The fused kernel adds the selection, 4 B per id, past the larger of this and the resolve's set.)
+size_t select_smem_bytes(int nt, int kpt, int cl, int64_t kb) {
+    const int64_t span = (int64_t)nt * kpt;
+    const size_t general = (size_t)span * 5 + (size_t)kListCap * 8;
+    const size_t fast = select_fast_ok(cl, span, kb)
+                            ? (size_t)span * 4 + (size_t)kRankList * 8 + (cl > 1 ? 8 * (size_t)cl * std::min(kb, span) : 0)
+                            : 0;
+    return std::max(general, fast);
+}
+
+size_t select_static_smem() {
+    return sizeof(TopkShared) + sizeof(KthShared) + sizeof(ResolveShared) + sizeof(float) * kHeadDim;
+}
+
+// score_kernel over the launch's segments, then the select kernel ranking those scores (PDL).
 template <bool RESOLVE>
 static cudaError_t launch_select_any(kvd_cache* c, const StepParams& p, const uint16_t* q, int32_t* out_ids,
                                      float* out_scores, const FuseArgs& fa, cudaStream_t s) {
+    cudaError_t e = launch_score(c, p, q, c->summ, c->summ2, c->scores, s);
+    if (e != cudaSuccess) return e;
+    StepParams p2 = p;
+    p2.prescored = 1;
     int nt, cl, kpt, v;
-    select_geometry(c->nb_pad, p.B * p.Hkv, c->resident, &nt, &cl, &kpt, &v);
-    return nt == 512 ? launch_select_nt<512, RESOLVE>(c, p, q, c->summ, c->scores, cl, kpt, v, out_ids, out_scores, fa, s)
-                     : launch_select_nt<1024, RESOLVE>(c, p, q, c->summ, c->scores, cl, kpt, v, out_ids, out_scores, fa, s);
+    select_geometry_pre(c->nb_pad, &nt, &cl, &kpt, &v);
+    return nt == 512 ? launch_select_nt<512, RESOLVE>(c, p2, q, c->summ, c->scores, cl, kpt, v, out_ids, out_scores, fa, s)
+                     : launch_select_nt<1024, RESOLVE>(c, p2, q, c->summ, c->scores, cl, kpt, v, out_ids, out_scores, fa, s);
 }
 
 // Stage 1 of the hierarchical index (R27): the same kernel over the segment's centroid matrix
 // (p.nb_pad = nc_pad, p.sel_mode = 1), selected centroid ids -> c->csel.  No fetch inside, so the
 // resident geometry (spread over SMs) applies.
 cudaError_t launch_select_centroids(kvd_cache* c, const StepParams& p, const uint16_t* q, cudaStream_t s) {
+    cudaError_t e = launch_score(c, p, q, c->cent, nullptr, c->cscores, s);
+    if (e != cudaSuccess) return e;
+    StepParams p2 = p;
+    p2.prescored = 1;
     int nt, cl, kpt, v;
-    select_geometry(c->nc_pad, p.B * p.Hkv, true, &nt, &cl, &kpt, &v);
+    select_geometry_pre(c->nc_pad, &nt, &cl, &kpt, &v);
     const FuseArgs fa{};
-    cudaError_t e = nt == 512 ? launch_select_nt<512, false>(c, p, q, c->cent, c->cscores, cl, kpt, v, c->csel, nullptr, fa, s)
-                              : launch_select_nt<1024, false>(c, p, q, c->cent, c->cscores, cl, kpt, v, c->csel, nullptr, fa, s);
+    e = nt == 512 ? launch_select_nt<512, false>(c, p2, q, c->cent, c->cscores, cl, kpt, v, c->csel, nullptr, fa, s)
+                  : launch_select_nt<1024, false>(c, p2, q, c->cent, c->cscores, cl, kpt, v, c->csel, nullptr, fa, s);
     return e != cudaSuccess ? e : cudaGetLastError();
 }
 

@@ -86,9 +86,10 @@ kvd_status check_config(const kvd_config* cfg, Geometry* g) {
         // on-chip working sets (dynamic + static shared memory of the step kernels, kvd.h)
         int nt, cl, kpt, v;
         select_geometry(g->nb_pad, 1 << 30, g->resident, &nt, &cl, &kpt, &v);   // fewest CTAs: most keys each
-        const size_t sel = select_smem_bytes(nt, kpt);
+        const size_t sel = select_smem_bytes(nt, kpt, cl, g->kmax);
         const size_t res = resolve_smem_bytes(g->resident ? 0 : g->C, g->kmax, g->nb_pad);
-        if (std::max(sel, res) + select_static_smem() > kMaxSmemBytes ||
+        // the fused kernel keeps the selection (4 B per id) past the larger of the two
+        if ((std::max(sel, res) + 15) / 16 * 16 + 4 * (size_t)g->kmax + select_static_smem() > kMaxSmemBytes ||
             res + resolve_static_smem() > kMaxSmemBytes)
             return fail(KVD_EINVAL, "slots_per_segment=%lld too large for on-chip victim selection (host-backed cache)",
                         (long long)g->C);
@@ -217,6 +218,7 @@ kvd_status check_step(kvd_cache* c, int32_t layer, const int32_t* req_ids, int32
     p->sel_stride = 0;
     p->sel_count = nullptr;
     p->summ2 = c->summ2;
+    p->prescored = 0;
 #ifdef KVD_EXPERIMENTS
     if (getenv("KVD_EXP_TRACE")) {
         if (!g_exp_trace) {

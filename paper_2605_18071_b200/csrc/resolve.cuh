@@ -328,6 +328,8 @@ struct FuseArgs {
     int32_t* out_attn;
     const uint8_t* host_store;    // NULL: fully resident (no misses)
     uint8_t* slots;
+    int32_t fast;                 // select_kernel: per-CTA thresholds + rank-0 merge (select_fast)
+    uint32_t sel_off;             // select_kernel (fused): byte offset of the selection in shared memory
 };
 
 // (a4) inside a segment's CTA: all threads copy the nm missed 8 KiB records host -> slot.

@@ -34,6 +34,7 @@
 #include <vector>
 
 #include "resolve.cuh"
+#include "topk.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -109,12 +110,6 @@ __device__ __forceinline__ T* cl_remote(T* p, int rank) {
 
 enum { kModeWhole = 0, kModeList = 1, kModeEqual = 2 };
 
-// inverse of score_key32 for non-NaN keys (key 0 = NaN -> -inf here)
-__device__ __forceinline__ float key_to_score(uint32_t key) {
-    if (key == 0u) return -INFINITY;
-    return __uint_as_float((key >> 31) ? (key & 0x7FFFFFFFu) : ~key);
-}
-
 // cluster-wide min / max of (kmn, kmx); every thread returns the cluster values
 template <int CL>
 __device__ __forceinline__ void cta_minmax(uint32_t& kmn, uint32_t& kmx, TopkShared& sm) {
@@ -189,6 +184,97 @@ __device__ __forceinline__ void pick_digit(TopkShared& sm, int nbins, int kk, in
 // cache (a3, resolve.cuh) and copies its misses from the host store (a4) in the same CTA,
 // reusing the dynamic shared memory: select -> resolve -> fetch without kernel boundaries.
 
+// Selection after scoring, the default path (fa.fast): every CTA finds the K-th largest rank key
+// of its own candidates (topk.cuh, CTA barriers only) and emits its top min(K, candidates) in id
+// order -- straight to the output when the segment has one CTA; otherwise as rank keys into
+// rank 0's candidate area (distributed shared memory), whose offset every rank derives from the
+// geometry.  One cluster barrier; rank 0 then selects K of the <= CL*K candidates (already in
+// ascending id order: rank c's span precedes rank c+1's) and emits them.  The global top-k is
+// contained in the union of the per-CTA top-k sets, so the result is the exact top-k.
+template <int CL, bool RESOLVE>
+__device__ __forceinline__ void select_fast(const FuseArgs& fa, const StepParams& p, const SegGeom& g, int K,
+                                            int ostride, int64_t base, int span, int crank, int c_lo, int c_hi,
+                                            uint32_t kmn, uint32_t kmx, uint32_t* skey, int64_t seg, int bi, int h,
+                                            int r, const float* __restrict__ scores, int32_t* __restrict__ out_ids,
+                                            float* __restrict__ out_scores, ResolveShared& rsm) {
+    __shared__ KthShared ks;
+    const int tid = threadIdx.x;
+    uint64_t* list = reinterpret_cast<uint64_t*>(skey + span);      // [kRankList] threshold-bin members
+    uint64_t* cand = list + kRankList;                              // [CL * min(K, span)] (rank 0)
+    uint8_t* smraw = reinterpret_cast<uint8_t*>(skey);
+    int32_t* sel = reinterpret_cast<int32_t*>(smraw + fa.sel_off);  // fused: the selection, past everything
+    // stage 1 (index) writes per request id: concurrent chains of one step never share rows
+    int32_t* ids_out = out_ids + ((int64_t)(p.sel_mode == 1 ? r : bi) * p.Hkv + h) * ostride;
+    float* sc_out = out_scores ? out_scores + ((int64_t)bi * p.Hkv + h) * ostride : nullptr;
+    const float* sc_seg = scores + seg * p.nb_pad;
+    auto put = [&](uint32_t id, int pos) {
+        ids_out[pos] = (int32_t)id;
+        if (sc_out) sc_out[pos] = __ldcg(sc_seg + id);
+        if (RESOLVE) sel[pos] = (int32_t)id;
+    };
+    const int unit = (bi * gridDim.y + h) * CL + crank;
+    (void)unit;
+    if (tid == 0) EXP_STAMP(p.exp_trace, unit, 2);
+    const SpanView sv{skey, c_lo, c_hi, (uint32_t)base};
+    uint64_t T = 0ull;                                              // 0: every candidate
+    if (K > 0 && c_hi - c_lo > K) T = kth_largest(sv, K, kmn, kmx, list, ks, p.exp_trace, unit);
+    if (tid == 0) EXP_STAMP(p.exp_trace, unit, 5);
+    if constexpr (CL == 1) {
+        if (K > 0) emit_ordered(sv, T, ks, [&](int i, int pos) { put((uint32_t)(base + i), pos); });
+    } else {
+        auto ncand_of = [&](int c) {
+            const int64_t b0 = (int64_t)c * span;
+            const int64_t nbv = min(max((int64_t)g.nb - b0, (int64_t)0), (int64_t)span);
+            const int64_t lo = min(max((int64_t)g.sink_end - b0, (int64_t)0), nbv);
+            const int64_t hi = min(max((int64_t)g.local_begin - b0, (int64_t)0), nbv);
+            return (int)(hi - lo);
+        };
+        int off = 0, n = 0;
+#pragma unroll
+        for (int c = 0; c < CL; ++c) {
+            const int m = min(K, ncand_of(c));
+            off += c < crank ? m : 0;
+            n += m;
+        }
+        uint64_t* cand0 = cg::this_cluster().map_shared_rank(cand, 0);
+        if (K > 0)
+            emit_ordered(sv, T, ks, [&](int i, int pos) { cand0[off + pos] = rank_key(skey[i], (uint32_t)(base + i)); });
+        cl_sync<CL>();              // release / acquire: every CTA's candidates and scores reach rank 0
+        if (crank != 0) {
+            if constexpr (!RESOLVE) griddep_launch();
+            return;
+        }
+        const ListView lv{cand, 0, n};
+        uint64_t T2 = 0ull;
+        if (K > 0 && n > K) {
+            uint32_t mn = 0xFFFFFFFFu, mx = 0u;
+            for (int i = tid; i < n; i += blockDim.x) {
+                const uint32_t k = lv.k32(i);
+                if (k) {
+                    mn = min(mn, k);
+                    mx = max(mx, k);
+                }
+            }
+            T2 = kth_largest(lv, K, mn, mx, list, ks);
+        }
+        if (K > 0) emit_ordered(lv, T2, ks, [&](int i, int pos) { put(rank_id(cand[i]), pos); });
+    }
+    if (tid == 0) EXP_STAMP(p.exp_trace, unit, 6);
+    if constexpr (!RESOLVE) {
+        griddep_launch();
+    } else {
+        // the sorted selection -> the resolve's S[] (sel lies past the resolve's working set);
+        // resolve_main starts with a barrier
+        int32_t* S = reinterpret_cast<int32_t*>(reinterpret_cast<uint64_t*>(smraw) + fa.rb.nkeys);
+        for (int j = tid; j < K; j += blockDim.x) S[j] = sel[j];
+        const int nm = resolve_main(p, fa.rb, bi, h, out_ids, fa.out_attn, smraw, rsm, true, true);
+        if (nm > 0 && fa.host_store) {
+            const int32_t* Sx = reinterpret_cast<const int32_t*>(reinterpret_cast<uint64_t*>(smraw) + fa.rb.nkeys);
+            gather_segment(p, bi, h, Sx + 2 * fa.rb.kmax, Sx + 3 * fa.rb.kmax, nm, fa.host_store, fa.slots, 0, 1);
+        }
+    }
+}
+
 template <int CL, int NT, int V, bool RESOLVE>
 __device__ __forceinline__ void select_body(const FuseArgs& fa, const StepParams& p, const uint16_t* __restrict__ q,
                                             const uint16_t* __restrict__ summ, float* __restrict__ scores,
@@ -247,8 +333,31 @@ __device__ __forceinline__ void select_body(const FuseArgs& fa, const StepParams
     const Vec* srow = reinterpret_cast<const Vec*>(summ + seg * kHeadDim * p.nb_pad + base);
     const int64_t rstride = p.nb_pad / V;         // Vec elements per dim row (nb_pad % 128 == 0)
     uint32_t kmn = 0xFFFFFFFFu, kmx = 0u;
+    if (p.prescored) {
+        // ---- the scores of this CTA's span from score_kernel (L2): 16-byte loads, keys to smem
+        griddep_wait();
+        if (tid == 0) kt_begin(p.kt_slots, p.kt_base + kKtSelect);
+        if (tid == 0) EXP_STAMP(p.exp_trace, ((bi * gridDim.y + h) * CL + crank), 1);
+        const float4* s4 = reinterpret_cast<const float4*>(sc);       // base, nb_pad: multiples of 4
+        for (int i4 = tid; 4 * i4 < nbv; i4 += NT) {
+            const float4 x = __ldcg(s4 + i4);
+            const float xs[4] = {x.x, x.y, x.z, x.w};
+            uint32_t key[4];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                const int i = 4 * i4 + v;
+                key[v] = score_key32(xs[v]);
+                if (i >= c_lo && i < c_hi && key[v] != 0u) {
+                    kmn = min(kmn, key[v]);
+                    kmx = max(kmx, key[v]);
+                }
+            }
+            *reinterpret_cast<uint4*>(&skey[4 * i4]) = make_uint4(key[0], key[1], key[2], key[3]);
+        }
+        __syncthreads();
+    }
 #pragma unroll 1
-    for (int gi = 0; gi * V < kpt; ++gi) {
+    for (int gi = 0; !p.prescored && gi * V < kpt; ++gi) {
         const int i0 = (gi * NT + tid) * V;
         const bool ld = i0 < nbv;                 // V-groups never straddle nb_pad
         const Vec* src = srow + (ld ? i0 / V : 0);
@@ -348,6 +457,12 @@ __device__ __forceinline__ void select_body(const FuseArgs& fa, const StepParams
             }
         }
     }
+    if (fa.fast) {
+        select_fast<CL, RESOLVE>(fa, p, g, K, ostride, base, span, crank, c_lo, c_hi, kmn, kmx, skey, seg, bi, h, r,
+                                 scores, out_ids, out_scores, rsm);
+        return;
+    }
+    // ---- general path (a cluster whose candidates do not fit rank 0's candidate area: K large)
     cta_minmax<CL>(kmn, kmx, sm);
     if (tid == 0) EXP_STAMP(p.exp_trace, ((bi * gridDim.y + h) * CL + crank), 2);
     if (K == 0) {
@@ -753,8 +868,15 @@ template <int CL, int NT, int V, bool RESOLVE>
 inline cudaError_t launch_select_k(kvd_cache* c, const StepParams& p, const uint16_t* q, const uint16_t* mat,
                                    float* scores, int kpt, int32_t* out_ids, float* out_scores, const FuseArgs& fa,
                                    cudaStream_t s) {
-    size_t smem = select_smem_bytes(NT, kpt);
-    if (RESOLVE) smem = std::max(smem, resolve_smem_bytes(fa.rb.nkeys, c->kmax, c->nb_pad));
+    const int64_t kb = p.sel_mode == 1 ? c->m_max : p.k;          // most ids a segment selects
+    FuseArgs f2 = fa;
+    f2.fast = select_fast_ok(CL, (int64_t)NT * kpt, kb) ? 1 : 0;
+    size_t smem = select_smem_bytes(NT, kpt, CL, kb);
+    if (RESOLVE) {
+        smem = std::max(smem, resolve_smem_bytes(fa.rb.nkeys, c->kmax, c->nb_pad));
+        f2.sel_off = (uint32_t)((smem + 15) / 16 * 16);
+        smem = f2.sel_off + 4 * (size_t)kb;
+    }
     // opt in to the largest dynamic size this instantiation has been launched with (per device
     // ordinal: the attribute is per device)
     static size_t smem_set[64] = {};
@@ -787,7 +909,7 @@ inline cudaError_t launch_select_k(kvd_cache* c, const StepParams& p, const uint
     cfg.attrs = attr;
     cfg.numAttrs = na;
     count_launch();
-    return cudaLaunchKernelEx(&cfg, select_kernel<CL, NT, V, RESOLVE>, fa, p, q, mat, scores,
+    return cudaLaunchKernelEx(&cfg, select_kernel<CL, NT, V, RESOLVE>, f2, p, q, mat, scores,
                               (const int32_t*)c->ntok_dev + (int64_t)p.layer * c->R, kpt, out_ids, out_scores);
 }
 

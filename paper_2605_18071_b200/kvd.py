@@ -313,7 +313,7 @@ class KVCache:
         _check(lib().kvd_get_segment_stats(self.h, ptr(sel), ptr(mis)))
         return sel, mis
 
-    KERNEL_KINDS = ("select", "resolve", "gather", "attn")
+    KERNEL_KINDS = ("select", "resolve", "gather", "attn", "score")
 
     def enable_kernel_timer(self, enable=True):
         """Device-side launch timing of every step kernel (kvd.h); zeroes the accumulators."""
@@ -321,8 +321,8 @@ class KVCache:
 
     def read_kernel_timer(self):
         """{kind: (summed launch ns, launches)} since the last enable."""
-        ns = np.zeros(4, np.uint64)
-        n = np.zeros(4, np.uint64)
+        ns = np.zeros(len(self.KERNEL_KINDS), np.uint64)
+        n = np.zeros(len(self.KERNEL_KINDS), np.uint64)
         _check(lib().kvd_read_kernel_timer(self.h, ptr(ns), ptr(n)))
         return {k: (int(ns[i]), int(n[i])) for i, k in enumerate(self.KERNEL_KINDS)}
 

@@ -1,8 +1,10 @@
 #!/bin/bash
-# ncu --set full of chain-sized select / attention launches (c2, eager, 2 layers).  usage: tools/gpu_ncu_sel.sh <tag>
-tag=${1:-ns}; mkdir -p gpurun_out
-K="regex:select_kernel|attn_kernel|merge_kernel"
-timeout 900 /usr/local/cuda/bin/ncu --set full --clock-control none --import-source on -k "$K" -s 48 -c 6 -o gpurun_out/${tag}_c2 -f \
-  python bench.py --config c2 --layers 2 --no-graph --fill 3 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/${tag}_c2.out 2>&1
-echo "ncu c2 rc $?"
-python tools/ncu_details.py gpurun_out/${tag}_c2.ncu-rep | head -60
+# ncu --set full of the select kernel (whole-batch launches, eager): per-source-line stall samples.
+# usage: tools/gpu_ncu_sel.sh <tag> [configs...]
+tag=${1:-ns}; shift; cfgs=${@:-c3}; mkdir -p gpurun_out
+for c in $cfgs; do
+  timeout 900 /usr/local/cuda/bin/ncu --set full --clock-control none --import-source on -k regex:select_kernel -s 64 -c 2 \
+    -o gpurun_out/${tag}_sel_$c -f python bench.py --config $c --layers 2 --chains 1 --no-graph --fill 32 --steps 1 --warmup 1 \
+    --no-e2e --no-cpu-baseline --no-isolated > gpurun_out/${tag}_sel_$c.out 2>&1
+  echo "ncu $c rc $?"
+done

@@ -1,32 +1,38 @@
-"""Write profiles/<tag>_ncu_traffic.json from `ncu --set full` captures of one eager layer step
-(whole batch, one chain): DRAM bytes (read + write) per ABI call, per config, for bench.py's
-roofline "traffic" field.  usage: python tools/ncu_traffic.py <tag> c2=<rep> c3=<rep> ...
+"""Write profiles/<tag>_ncu_traffic.json from `ncu --set full` captures of eager layer steps:
+DRAM bytes (read + write) and PCIe read bytes per launch and per segment, per ABI call and
+config, for bench.py's roofline "traffic" field.
+usage: python tools/ncu_traffic.py <tag> c2=<rep>:<segments per launch> c3=<rep>:<segs> ...
 
-Per ABI call: select = score_kernel (+ topk_kernel when unfused), attn = attn_kernel +
-merge_kernel.  Averaged over the captured layers."""
+Per ABI call: select = score_kernel + select_kernel (kvd_select_resolve_fetch: top-k + resolve +
+fetch; + cand_kernel with the hierarchical index), attn = attn_kernel (attention + LSE merge).
+Averaged over the captured launches."""
 import csv
 import io
 import json
 import subprocess
 import sys
 
-SEGMENTS = {"c2": 64, "c3": 128, "c4": 16, "c5": 512}
-CALLS = {"select": ("score_kernel", "topk_kernel"), "attn": ("attn_kernel", "merge_kernel")}
+CALLS = {"select": ("select_kernel", "score_kernel", "cand_kernel"), "attn": ("attn_kernel",)}
+METRICS = ("dram__bytes_read.sum", "dram__bytes_write.sum", "pcie__read_bytes.sum")
 
 
 def kernels(rep):
     txt = subprocess.run(["/usr/local/cuda/bin/ncu", "-i", rep, "--page", "raw", "--csv", "--metrics",
-                          "dram__bytes_read.sum,dram__bytes_write.sum"], capture_output=True, text=True).stdout
+                          ",".join(METRICS)], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
     h, units = rows[0], rows[1]
     ki = h.index("Kernel Name")
-    ri, wi = h.index("dram__bytes_read.sum"), h.index("dram__bytes_write.sum")
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+
+    def val(r, m):
+        if m not in h:
+            return None
+        i = h.index(m)
+        return float(r[i].replace(",", "")) * scale.get(units[i], 1)
     out = []
     for r in rows[2:]:
-        name = r[ki].split("(")[0].replace("void ", "").split("<")[0]
-        b = float(r[ri]) * scale[units[ri]] + float(r[wi]) * scale[units[wi]]
-        out.append((name, b))
+        name = r[ki].split("(")[0].replace("void ", "").replace("kvd::", "").split("<")[0]
+        out.append((name, val(r, METRICS[0]) + val(r, METRICS[1]), val(r, METRICS[2])))
     return out
 
 
@@ -34,15 +40,23 @@ def main():
     tag = sys.argv[1]
     res = {}
     for a in sys.argv[2:]:
-        cfg, rep = a.split("=", 1)
+        cfg, spec = a.split("=", 1)
+        rep, segs = spec.rsplit(":", 1)
+        segs = int(segs)
         ks = kernels(rep)
         res[cfg] = {}
         for call, names in CALLS.items():
-            per = {n: [b for k, b in ks if k == n] for n in names}
+            per = {n: [(b, pc) for k, b, pc in ks if k == n] for n in names}
             if not per[names[0]]:
                 continue
-            tot = sum(sum(v) / len(v) for v in per.values() if v)
-            res[cfg][call] = {"dram_bytes_per_call": tot, "segments": SEGMENTS[cfg],
+            dram = sum(sum(b for b, _ in v) / len(v) for v in per.values() if v)
+            pcie = [pc for v in per.values() for _, pc in v]
+            pcie = sum(pcie) / len(per[names[0]]) if pcie and None not in pcie else None
+            res[cfg][call] = {"dram_bytes_per_launch": dram, "segments_per_launch": segs,
+                              "dram_bytes_per_segment": dram / segs,
+                              "pcie_read_bytes_per_launch": pcie,
+                              "pcie_read_bytes_per_segment": None if pcie is None else pcie / segs,
+                              "launches": len(per[names[0]]),
                               "kernels": " + ".join(n for n in names if per[n]) + f" ({rep.split('/')[-1]})"}
     path = f"profiles/{tag}_ncu_traffic.json"
     json.dump(res, open(path, "w"), indent=1)
