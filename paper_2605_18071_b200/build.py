@@ -11,7 +11,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libkvd.so")
 SOURCES = ["kvd_abi.cu", "k_prefix.cu", "k_select.cu", "k_select_nt512.cu", "k_select_nt1024.cu",
-           "k_resolve.cu", "k_attn.cu", "k_score.cu", "k_index.cu", "k_append.cu", "k_warm.cu"]
+           "k_resolve.cu", "k_attn.cu", "k_score.cu", "k_rank.cu", "k_index.cu", "k_append.cu", "k_warm.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2",

@@ -53,7 +53,6 @@ struct StepParams {
     int32_t sel_stride;               // stage 1: output stride per segment (m_max)
     const int32_t* sel_count;         // stage 1: centroids per segment [L][R][Hkv]
     const uint16_t* summ2;            // Quest min/max summaries (sel_mode 2): the maximum matrix
-    int32_t prescored;                // select_kernel: scores come from score_kernel (k_score.cu) via L2
     int32_t req[KVD_MAX_BATCH];
 };
 

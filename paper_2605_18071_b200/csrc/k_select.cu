@@ -47,7 +47,7 @@ void select_geometry(int64_t nb_pad, int segs, bool resident, int* nt, int* cl, 
     *v = vw;
 }
 
-// Geometry of the select kernel behind score_kernel (p.prescored): it only ranks scores from L2,
+// Geometry of rank_kernel (behind score_kernel): it only ranks scores from L2,
 // so a segment takes the fewest CTAs whose shared memory holds its keys (<= kMaxKpt per thread;
 // KVD_SELECT_PRE_SPAN in experiment builds caps the span), 512 threads up to 2048 blocks.
 void select_geometry_pre(int64_t nb_pad, int* nt, int* cl, int* kpt, int* v) {
@@ -92,33 +92,43 @@ size_t select_static_smem() {
     return sizeof(TopkShared) + sizeof(KthShared) + sizeof(ResolveShared) + sizeof(float) * kHeadDim;
 }
 
-// score_kernel over the launch's segments, then the select kernel ranking those scores (PDL).
+// score_kernel over the launch's segments, then rank_kernel ranking those scores from L2 (PDL).
+// A cluster whose candidates do not fit rank 0 (K x cluster size > kCandMax) takes the
+// self-scoring select_kernel with the general top-k instead.
 template <bool RESOLVE>
 static cudaError_t launch_select_any(kvd_cache* c, const StepParams& p, const uint16_t* q, int32_t* out_ids,
                                      float* out_scores, const FuseArgs& fa, cudaStream_t s) {
-    cudaError_t e = launch_score(c, p, q, c->summ, c->summ2, c->scores, s);
-    if (e != cudaSuccess) return e;
-    StepParams p2 = p;
-    p2.prescored = 1;
     int nt, cl, kpt, v;
     select_geometry_pre(c->nb_pad, &nt, &cl, &kpt, &v);
-    return nt == 512 ? launch_select_nt<512, RESOLVE>(c, p2, q, c->summ, c->scores, cl, kpt, v, out_ids, out_scores, fa, s)
-                     : launch_select_nt<1024, RESOLVE>(c, p2, q, c->summ, c->scores, cl, kpt, v, out_ids, out_scores, fa, s);
+    if (!select_fast_ok(cl, (int64_t)nt * kpt, p.k)) {
+        select_geometry(c->nb_pad, p.B * p.Hkv, c->resident, &nt, &cl, &kpt, &v);
+        return nt == 512 ? launch_select_nt<512, RESOLVE>(c, p, q, c->summ, c->scores, cl, kpt, v, out_ids, out_scores, fa, s)
+                         : launch_select_nt<1024, RESOLVE>(c, p, q, c->summ, c->scores, cl, kpt, v, out_ids, out_scores, fa, s);
+    }
+    cudaError_t e = launch_score(c, p, q, c->summ, c->summ2, c->scores, s);
+    if (e != cudaSuccess) return e;
+    return nt == 512 ? launch_rank_nt<512, RESOLVE>(c, p, c->scores, cl, kpt, out_ids, out_scores, fa, s)
+                     : launch_rank_nt<1024, RESOLVE>(c, p, c->scores, cl, kpt, out_ids, out_scores, fa, s);
 }
 
 // Stage 1 of the hierarchical index (R27): the same kernel over the segment's centroid matrix
 // (p.nb_pad = nc_pad, p.sel_mode = 1), selected centroid ids -> c->csel.  No fetch inside, so the
 // resident geometry (spread over SMs) applies.
 cudaError_t launch_select_centroids(kvd_cache* c, const StepParams& p, const uint16_t* q, cudaStream_t s) {
-    cudaError_t e = launch_score(c, p, q, c->cent, nullptr, c->cscores, s);
-    if (e != cudaSuccess) return e;
-    StepParams p2 = p;
-    p2.prescored = 1;
     int nt, cl, kpt, v;
     select_geometry_pre(c->nc_pad, &nt, &cl, &kpt, &v);
     const FuseArgs fa{};
-    e = nt == 512 ? launch_select_nt<512, false>(c, p2, q, c->cent, c->cscores, cl, kpt, v, c->csel, nullptr, fa, s)
-                  : launch_select_nt<1024, false>(c, p2, q, c->cent, c->cscores, cl, kpt, v, c->csel, nullptr, fa, s);
+    cudaError_t e;
+    if (!select_fast_ok(cl, (int64_t)nt * kpt, c->m_max)) {
+        select_geometry(c->nc_pad, p.B * p.Hkv, true, &nt, &cl, &kpt, &v);
+        e = nt == 512 ? launch_select_nt<512, false>(c, p, q, c->cent, c->cscores, cl, kpt, v, c->csel, nullptr, fa, s)
+                      : launch_select_nt<1024, false>(c, p, q, c->cent, c->cscores, cl, kpt, v, c->csel, nullptr, fa, s);
+    } else {
+        e = launch_score(c, p, q, c->cent, nullptr, c->cscores, s);
+        if (e == cudaSuccess)
+            e = nt == 512 ? launch_rank_nt<512, false>(c, p, c->cscores, cl, kpt, c->csel, nullptr, fa, s)
+                          : launch_rank_nt<1024, false>(c, p, c->cscores, cl, kpt, c->csel, nullptr, fa, s);
+    }
     return e != cudaSuccess ? e : cudaGetLastError();
 }
 

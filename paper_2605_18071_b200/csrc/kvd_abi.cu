@@ -218,7 +218,6 @@ kvd_status check_step(kvd_cache* c, int32_t layer, const int32_t* req_ids, int32
     p->sel_stride = 0;
     p->sel_count = nullptr;
     p->summ2 = c->summ2;
-    p->prescored = 0;
 #ifdef KVD_EXPERIMENTS
     if (getenv("KVD_EXP_TRACE")) {
         if (!g_exp_trace) {

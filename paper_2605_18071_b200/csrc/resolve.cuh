@@ -200,6 +200,7 @@ __device__ inline int resolve_main(const StepParams& p, const ResolveBufs& rb, i
         // radix select: the nv-th smallest key, T (keys are unique among candidates)
         uint64_t prefix = 0, mask = 0;
         int kk = nv;
+#pragma unroll 1
         for (int shift = 56; shift >= 0; shift -= 8) {
             for (int i = tid; i < 256; i += blockDim.x) rsm.hist[i] = 0;
             __syncthreads();

@@ -333,31 +333,8 @@ __device__ __forceinline__ void select_body(const FuseArgs& fa, const StepParams
     const Vec* srow = reinterpret_cast<const Vec*>(summ + seg * kHeadDim * p.nb_pad + base);
     const int64_t rstride = p.nb_pad / V;         // Vec elements per dim row (nb_pad % 128 == 0)
     uint32_t kmn = 0xFFFFFFFFu, kmx = 0u;
-    if (p.prescored) {
-        // ---- the scores of this CTA's span from score_kernel (L2): 16-byte loads, keys to smem
-        griddep_wait();
-        if (tid == 0) kt_begin(p.kt_slots, p.kt_base + kKtSelect);
-        if (tid == 0) EXP_STAMP(p.exp_trace, ((bi * gridDim.y + h) * CL + crank), 1);
-        const float4* s4 = reinterpret_cast<const float4*>(sc);       // base, nb_pad: multiples of 4
-        for (int i4 = tid; 4 * i4 < nbv; i4 += NT) {
-            const float4 x = __ldcg(s4 + i4);
-            const float xs[4] = {x.x, x.y, x.z, x.w};
-            uint32_t key[4];
-#pragma unroll
-            for (int v = 0; v < 4; ++v) {
-                const int i = 4 * i4 + v;
-                key[v] = score_key32(xs[v]);
-                if (i >= c_lo && i < c_hi && key[v] != 0u) {
-                    kmn = min(kmn, key[v]);
-                    kmx = max(kmx, key[v]);
-                }
-            }
-            *reinterpret_cast<uint4*>(&skey[4 * i4]) = make_uint4(key[0], key[1], key[2], key[3]);
-        }
-        __syncthreads();
-    }
 #pragma unroll 1
-    for (int gi = 0; !p.prescored && gi * V < kpt; ++gi) {
+    for (int gi = 0; gi * V < kpt; ++gi) {
         const int i0 = (gi * NT + tid) * V;
         const bool ld = i0 < nbv;                 // V-groups never straddle nb_pad
         const Vec* src = srow + (ld ? i0 / V : 0);
@@ -864,6 +841,146 @@ __global__ void __launch_bounds__(NT, 1) select_kernel(FuseArgs fa, StepParams p
     }
 }
 
+
+// ------------------------------------------------------------------ rank_kernel
+// The select call's second kernel (behind score_kernel, PDL): one thread-block cluster of CL
+// CTAs x NT threads per segment ranks the segment's scores from L2 -- keys to shared memory,
+// select_fast (per-CTA thresholds, one cluster barrier, rank-0 merge), then, fused, the resolve
+// and the miss fetch on rank 0.  It carries only that path (no scoring loop, no general top-k):
+// every phase is latency-bound, and a kernel of this size keeps its code in the instruction
+// cache (the self-scoring select_kernel above is ~350 KiB of SASS; its phases stalled mostly on
+// instruction fetch, ncu).
+template <int CL, int NT, bool RESOLVE>
+__global__ void __launch_bounds__(NT, 1) rank_kernel(FuseArgs fa, StepParams p, float* __restrict__ scores,
+                                                     const int32_t* __restrict__ ntok, int kpt,
+                                                     int32_t* __restrict__ out_ids, float* __restrict__ out_scores) {
+    extern __shared__ __align__(16) uint32_t skey[];   // [span] keys | [kRankList] | [CL * K] candidates
+    __shared__ ResolveShared rsm;
+    const int crank = CL > 1 ? (int)cg::this_cluster().block_rank() : 0;
+    const int tid = threadIdx.x;
+    const int h = blockIdx.y, bi = blockIdx.z;
+    const int r = p.req[bi];
+    const int span = NT * kpt;
+    const int64_t base = (int64_t)crank * span;
+    const int64_t seg = ((int64_t)p.layer * p.R + r) * p.Hkv + h;
+    // the launch's view: the segment's blocks (pinned excluded, k = p.k), or -- stage 1 of the
+    // hierarchical index (R27) -- its centroids (no pinned; K = min(nc, max(ceil(4k/ratio),
+    // k + pinned)), ids written with stride sel_stride)
+    SegGeom g = seg_geom(ntok[r], p.P, p.sink_tokens, p.local_tokens);
+    int K = p.k, ostride = p.k;
+    if (p.sel_mode == 1) {
+        const int nc = p.sel_count[seg];
+        const int pin = g.sink_end + (g.nb - g.local_begin);
+        const int f = (kIdxFanout * p.k + p.sel_ratio - 1) / p.sel_ratio;
+        K = min(nc, max(f, p.k + pin));
+        ostride = p.sel_stride;
+        g.n = nc;
+        g.nb = nc;
+        g.sink_end = 0;
+        g.local_begin = nc;
+    }
+    auto clampi = [](int64_t x, int64_t lo_, int64_t hi_) { return (int)(x < lo_ ? lo_ : x > hi_ ? hi_ : x); };
+    const int nbv = clampi((int64_t)g.nb - base, 0, span);
+    const int c_lo = clampi(g.sink_end - base, 0, nbv);
+    const int c_hi = clampi(g.local_begin - base, 0, nbv);
+    const int unit = (bi * gridDim.y + h) * CL + crank;
+    (void)unit;
+    if (tid == 0) EXP_STAMP(p.exp_trace, unit, 0);
+    if (RESOLVE && crank == 0) resolve_pre(p, fa.rb, bi, h, rsm);
+    griddep_wait();                                // the scores come from score_kernel
+    if (tid == 0) kt_begin(p.kt_slots, p.kt_base + kKtSelect);
+    if (tid == 0) EXP_STAMP(p.exp_trace, unit, 1);
+    // ---- this CTA's scores -> monotone keys in shared memory (16-byte loads; base and the row
+    // pitch are multiples of 4), and the candidates' key range
+    const float4* s4 = reinterpret_cast<const float4*>(scores + seg * p.nb_pad + base);
+    uint32_t kmn = 0xFFFFFFFFu, kmx = 0u;
+#pragma unroll 1
+    for (int i4 = tid; 4 * i4 < nbv; i4 += NT) {
+        const float4 x = __ldcg(s4 + i4);
+        const uint4 k4 = make_uint4(score_key32(x.x), score_key32(x.y), score_key32(x.z), score_key32(x.w));
+        const uint32_t kv[4] = {k4.x, k4.y, k4.z, k4.w};
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const int i = 4 * i4 + v;
+            if (i >= c_lo && i < c_hi && kv[v] != 0u) {
+                kmn = min(kmn, kv[v]);
+                kmx = max(kmx, kv[v]);
+            }
+        }
+        *reinterpret_cast<uint4*>(&skey[4 * i4]) = k4;
+    }
+    __syncthreads();
+    select_fast<CL, RESOLVE>(fa, p, g, K, ostride, base, span, crank, c_lo, c_hi, kmn, kmx, skey, seg, bi, h, r,
+                             scores, out_ids, out_scores, rsm);   // CTA-uniform returns
+#ifdef KVD_EXPERIMENTS
+    __syncthreads();
+    if (tid == 0) EXP_STAMP(p.exp_trace, unit, 7);
+#endif
+    if (p.kt_slots) {
+        __syncthreads();
+        if (tid == 0)
+            kt_end(p.kt_slots, p.kt_acc, p.kt_base + kKtSelect, kKtSelect, (unsigned long long)gridDim.x * gridDim.y * gridDim.z);
+    }
+}
+
+template <int CL, int NT, bool RESOLVE>
+inline cudaError_t launch_rank_k(kvd_cache* c, const StepParams& p, float* scores, int kpt, int32_t* out_ids,
+                                 float* out_scores, const FuseArgs& fa, cudaStream_t s) {
+    const int64_t kb = p.sel_mode == 1 ? c->m_max : p.k;
+    const int64_t span = (int64_t)NT * kpt;
+    FuseArgs f2 = fa;
+    f2.fast = 1;
+    size_t smem = (size_t)span * 4 + (size_t)kRankList * 8 + (CL > 1 ? 8 * (size_t)CL * std::min(kb, span) : 0);
+    if (RESOLVE) {
+        smem = std::max(smem, resolve_smem_bytes(fa.rb.nkeys, c->kmax, c->nb_pad));
+        f2.sel_off = (uint32_t)((smem + 15) / 16 * 16);
+        smem = f2.sel_off + 4 * (size_t)kb;
+    }
+    static size_t smem_set[64] = {};
+    const int dev = c->cfg.device & 63;
+    if (smem > smem_set[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(rank_kernel<CL, NT, RESOLVE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        smem_set[dev] = smem;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CL, p.Hkv, p.B);
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[3];
+    int na = 0;
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na++].val.programmaticStreamSerializationAllowed = 1;
+    if (CL > 1) {
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = CL;
+        attr[na].val.clusterDim.y = 1;
+        attr[na++].val.clusterDim.z = 1;
+    }
+    if (RESOLVE && fa.host_store) {               // the host-link fetch is inside: schedule it first
+        attr[na].id = cudaLaunchAttributePriority;
+        attr[na++].val.priority = c->prio_hi;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
+    count_launch();
+    return cudaLaunchKernelEx(&cfg, rank_kernel<CL, NT, RESOLVE>, f2, p, scores,
+                              (const int32_t*)c->ntok_dev + (int64_t)p.layer * c->R, kpt, out_ids, out_scores);
+}
+
+template <int NT, bool RESOLVE>
+cudaError_t launch_rank_nt(kvd_cache* c, const StepParams& p, float* scores, int cl, int kpt, int32_t* out_ids,
+                           float* out_scores, const FuseArgs& fa, cudaStream_t s) {
+    switch (cl) {
+        case 1: return launch_rank_k<1, NT, RESOLVE>(c, p, scores, kpt, out_ids, out_scores, fa, s);
+        case 2: return launch_rank_k<2, NT, RESOLVE>(c, p, scores, kpt, out_ids, out_scores, fa, s);
+        case 4: return launch_rank_k<4, NT, RESOLVE>(c, p, scores, kpt, out_ids, out_scores, fa, s);
+        default: return launch_rank_k<8, NT, RESOLVE>(c, p, scores, kpt, out_ids, out_scores, fa, s);
+    }
+}
+
 template <int CL, int NT, int V, bool RESOLVE>
 inline cudaError_t launch_select_k(kvd_cache* c, const StepParams& p, const uint16_t* q, const uint16_t* mat,
                                    float* scores, int kpt, int32_t* out_ids, float* out_scores, const FuseArgs& fa,
@@ -941,5 +1058,14 @@ extern template cudaError_t launch_select_nt<1024, false>(kvd_cache*, const Step
     float*, int, int, int, int32_t*, float*, const FuseArgs&, cudaStream_t);
 extern template cudaError_t launch_select_nt<1024, true>(kvd_cache*, const StepParams&, const uint16_t*, const uint16_t*,
     float*, int, int, int, int32_t*, float*, const FuseArgs&, cudaStream_t);
+// k_rank.cu
+extern template cudaError_t launch_rank_nt<512, false>(kvd_cache*, const StepParams&, float*, int, int, int32_t*, float*,
+                                                      const FuseArgs&, cudaStream_t);
+extern template cudaError_t launch_rank_nt<512, true>(kvd_cache*, const StepParams&, float*, int, int, int32_t*, float*,
+                                                     const FuseArgs&, cudaStream_t);
+extern template cudaError_t launch_rank_nt<1024, false>(kvd_cache*, const StepParams&, float*, int, int, int32_t*, float*,
+                                                       const FuseArgs&, cudaStream_t);
+extern template cudaError_t launch_rank_nt<1024, true>(kvd_cache*, const StepParams&, float*, int, int, int32_t*, float*,
+                                                      const FuseArgs&, cudaStream_t);
 
 }  // namespace kvd

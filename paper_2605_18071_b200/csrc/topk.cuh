@@ -123,6 +123,7 @@ __device__ __forceinline__ uint64_t kth_largest(const View v, int K, uint32_t km
         sh.kmin[warp] = kmn;
         sh.kmax[warp] = kmx;
     }
+    #pragma unroll 1
     for (int i = tid; i < 512; i += NT) (&sh.hist[0][0])[i] = 0;
     if (tid == 0) {
         sh.nlist = 0;
@@ -131,6 +132,7 @@ __device__ __forceinline__ uint64_t kth_largest(const View v, int K, uint32_t km
     __syncthreads();
     kmn = 0xFFFFFFFFu;
     kmx = 0u;
+    #pragma unroll 1
     for (int w = 0; w < nw; ++w) {
         kmn = min(kmn, sh.kmin[w]);
         kmx = max(kmx, sh.kmax[w]);
@@ -148,6 +150,7 @@ __device__ __forceinline__ uint64_t kth_largest(const View v, int K, uint32_t km
     };
     int kk = K, cnt = v.hi - v.lo, bstar = 0;
     if (lin) {
+        #pragma unroll 1
         for (int i = v.lo + tid; i < v.hi; i += NT) atomicAdd(&sh.hist[0][bin_of(v.k32(i))], 1);
         __syncthreads();
         if (warp == 0) kth_pick(sh.hist[0], sh, 256, kk);
@@ -160,6 +163,7 @@ __device__ __forceinline__ uint64_t kth_largest(const View v, int K, uint32_t km
     // ---- the threshold bin's members: compacted as rank keys when they fit; their range
     const int s0 = v.lo & ~31;
     uint64_t gmn = ~0ull, gmx = 0ull;
+    #pragma unroll 1
     for (int i0 = s0 + warp * 32; i0 < v.hi; i0 += NT) {
         const int i = i0 + lane;
         const bool m = i >= v.lo && i < v.hi && bin_of(v.k32(i)) == bstar;
@@ -185,6 +189,7 @@ __device__ __forceinline__ uint64_t kth_largest(const View v, int K, uint32_t km
     __syncthreads();
     gmn = ~0ull;
     gmx = 0ull;
+    #pragma unroll 1
     for (int w = 0; w < nw; ++w) {
         gmn = min(gmn, sh.wmin[w]);
         gmx = max(gmx, sh.wmax[w]);
@@ -192,26 +197,49 @@ __device__ __forceinline__ uint64_t kth_largest(const View v, int K, uint32_t km
     if (tid == 0) EXP_STAMP(trace, unit, 4);
     const bool compacted = cnt <= kRankList;
     const int nl = compacted ? cnt : 0;
-    // visit every member (every lane of a warp iterates alike: warp-collective bodies allowed)
-    auto for_members = [&](auto&& f) {
-        if (compacted) {
-            for (int j0 = warp * 32; j0 < nl; j0 += NT) {
-                const int j = j0 + lane;
-                f(j < nl ? list[j] : 0ull, j < nl);
+    // one pass over the group {members : (rk & mask) == prefix}; every lane of a warp iterates
+    // alike (warp-collective bodies).  One loop body for every use keeps the code small.
+    enum { kOpMin = 0, kOpMinMax = 1, kOpHist = 2, kOpGather = 3 };
+    uint64_t mask = 0ull, prefix = 0ull;
+    auto group_pass = [&](int op, int* hb, int shift, int nbins, uint64_t& mn, uint64_t& mx) {
+        const int n = compacted ? nl : v.hi - s0;
+#pragma unroll 1
+        for (int j0 = warp * 32; j0 < n; j0 += NT) {
+            const int j = j0 + lane;
+            uint64_t r = 0ull;
+            bool in = false;
+            if (compacted) {
+                if (j < nl) {
+                    r = list[j];
+                    in = true;
+                }
+            } else {
+                const int i = s0 + j;
+                if (i >= v.lo && i < v.hi) {
+                    r = v.rk(i);
+                    in = bin_of((uint32_t)(r >> 32)) == bstar;
+                }
             }
-        } else {
-            for (int i0 = s0 + warp * 32; i0 < v.hi; i0 += NT) {
-                const int i = i0 + lane;
-                const bool inr = i >= v.lo && i < v.hi;
-                const uint64_t r = inr ? v.rk(i) : 0ull;
-                f(r, inr && bin_of((uint32_t)(r >> 32)) == bstar);
+            in = in && (r & mask) == prefix;
+            if (op == kOpHist) {
+                warp_hist_add(hb, (uint32_t)(r >> shift) & (uint32_t)(nbins - 1), in);
+            } else if (op == kOpGather) {
+                const uint32_t bal = __ballot_sync(0xffffffffu, in);
+                if (bal) {
+                    int wb = 0;
+                    if (lane == 0) wb = atomicAdd(&sh.nsmall, __popc(bal));
+                    wb = __shfl_sync(0xffffffffu, wb, 0);
+                    if (in) sh.small[wb + __popc(bal & lt)] = r;
+                }
+            } else if (in) {
+                mn = min(mn, r);
+                if (op == kOpMinMax) mx = max(mx, r);
             }
         }
     };
-    // ---- radix digits of the group {members : (rk & mask) == prefix}, from its highest
-    // differing bit down, until the kk-th largest is isolated: the group is taken whole (T = its
-    // minimum: known for the members, reduced otherwise) or holds <= 32 keys (ranked in a warp)
-    uint64_t mask = 0ull, prefix = 0ull;
+    // ---- radix digits of the group, from its highest differing bit down, until the kk-th
+    // largest is isolated: the group is taken whole (T = its minimum: known for the members,
+    // reduced otherwise) or holds <= 32 keys (ranked in a warp)
     int pass = 0, lo = 64 - __clzll((long long)(gmn ^ gmx));
     uint64_t T;
 #pragma unroll 1
@@ -220,34 +248,26 @@ __device__ __forceinline__ uint64_t kth_largest(const View v, int K, uint32_t km
             if (pass == 0) {
                 T = gmn;
             } else {
-                uint64_t mn = ~0ull;
-                for_members([&](uint64_t r, bool in) {
-                    if (in && (r & mask) == prefix) mn = min(mn, r);
-                });
+                uint64_t mn = ~0ull, mx = 0ull;
+                group_pass(kOpMin, nullptr, 0, 1, mn, mx);
                 mn = warp_min64(mn);
                 if (lane == 0) sh.wmin[warp] = mn;
                 __syncthreads();
                 T = ~0ull;
+#pragma unroll 1
                 for (int w = 0; w < nw; ++w) T = min(T, sh.wmin[w]);
                 __syncthreads();
             }
             break;
         }
         if (cnt <= 32) {
-            for_members([&](uint64_t r, bool in) {
-                const bool g = in && (r & mask) == prefix;
-                const uint32_t bal = __ballot_sync(0xffffffffu, g);
-                if (!bal) return;
-                int wb = 0;
-                if (lane == 0) wb = atomicAdd(&sh.nsmall, __popc(bal));
-                wb = __shfl_sync(0xffffffffu, wb, 0);
-                if (g) sh.small[wb + __popc(bal & lt)] = r;
-            });
+            uint64_t mn = 0ull, mx = 0ull;
+            group_pass(kOpGather, nullptr, 0, 1, mn, mx);
             __syncthreads();
             if (warp == 0) {
                 const uint64_t r = lane < cnt ? sh.small[lane] : 0ull;
                 int above = 0;
-#pragma unroll
+#pragma unroll 4
                 for (int u = 0; u < 32; ++u) above += (uint64_t)__shfl_sync(0xffffffffu, (unsigned long long)r, u) > r ? 1 : 0;
                 if (lane < cnt && above == kk - 1) sh.T = r;
             }
@@ -260,12 +280,15 @@ __device__ __forceinline__ uint64_t kth_largest(const View v, int K, uint32_t km
         if (lo < 64) mask |= ~0ull << lo;
         prefix = gmn & mask;
         int* hb = sh.hist[1 - (pass & 1)];       // cleared (pass 0: at the start; later: below)
-        for_members([&](uint64_t r, bool in) {
-            warp_hist_add(hb, (uint32_t)(r >> shift) & (uint32_t)(nbins - 1), in && (r & mask) == prefix);
-        });
+        {
+            uint64_t mn = 0ull, mx = 0ull;
+            group_pass(kOpHist, hb, shift, nbins, mn, mx);
+        }
         __syncthreads();
         if (warp == 0) kth_pick(hb, sh, nbins, kk);
-        else for (int i = tid - 32; i < 256; i += NT - 32) sh.hist[pass & 1][i] = 0;   // next pass's
+        else
+#pragma unroll 1
+            for (int i = tid - 32; i < 256; i += NT - 32) sh.hist[pass & 1][i] = 0;   // the next pass's
         __syncthreads();
         prefix |= (uint64_t)sh.digit << shift;
         mask |= (uint64_t)(nbins - 1) << shift;
@@ -291,6 +314,7 @@ __device__ __forceinline__ int emit_ordered(const View v, uint64_t T, KthShared&
     const int per = ((n + nw - 1) / nw + 31) & ~31;
     const int a = v.lo + warp * per, b = min(v.hi, a + per);
     int c = 0;
+    #pragma unroll 1
     for (int i0 = a; i0 < b; i0 += 32) {
         const int i = i0 + lane;
         c += __popc(__ballot_sync(0xffffffffu, i < b && v.rk(i) >= T));
@@ -312,6 +336,7 @@ __device__ __forceinline__ int emit_ordered(const View v, uint64_t T, KthShared&
     int pos = sh.wcnt[warp];
     const int tot = sh.wcnt[32];
     const uint32_t lt = (1u << lane) - 1u;
+    #pragma unroll 1
     for (int i0 = a; i0 < b; i0 += 32) {
         const int i = i0 + lane;
         const bool t = i < b && v.rk(i) >= T;

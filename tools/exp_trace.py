@@ -27,6 +27,9 @@ def read(lib, units):
 
 def show(name, tr, phases):
     used = tr[:, 0] > 0
+    if not used.any():
+        print(f"{name}: no stamps")
+        return
     tr = tr[used].astype(np.float64)
     t0 = tr[:, 0].min()
     print(f"{name}: {used.sum()} units")
@@ -74,7 +77,7 @@ def main():
         s.synchronize()
         tr = read(lib, 16384)
         show(f"[{rep}] select_kernel ({nb} requests)", tr[:8192],
-             ["entry", "after_wait", "scored", "first_digit", "compacted", "radix_done", "emitted", "end"])
+             ["entry", "after_wait", "keys", "first_digit", "compacted", "threshold", "emitted", "end"])
         if tr[8192:, 0].any():
             show(f"[{rep}] cand_kernel (index stage 2)", tr[8192:],
                  ["entry", "after_wait", "candidates", "la_scores", "scored", "radix", "emitted", "end"])
