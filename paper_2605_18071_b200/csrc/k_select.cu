@@ -47,11 +47,13 @@ void select_geometry(int64_t nb_pad, int segs, bool resident, int* nt, int* cl, 
     *v = vw;
 }
 
-// Geometry of rank_kernel (behind score_kernel): it only ranks scores from L2,
-// so a segment takes the fewest CTAs whose shared memory holds its keys (<= kMaxKpt per thread;
-// KVD_SELECT_PRE_SPAN in experiment builds caps the span), 512 threads up to 2048 blocks.
+// Geometry of rank_kernel (behind score_kernel): it only ranks scores from L2.  Its phases are
+// instruction-bound on one SM (a few dozen instructions per key and pass), so a segment is cut
+// into CTAs of at most 8192 keys (c4's 65,536 blocks: a cluster of 8; 1632 vs 1475 tok/s with
+// 2 CTAs of 32,768) -- up to the portable cluster size of 8 -- and the rank-0 merge takes the
+// rest.  512 threads up to 2048 blocks per CTA, else 1024.  (KVD_SELECT_PRE_SPAN: experiments.)
 void select_geometry_pre(int64_t nb_pad, int* nt, int* cl, int* kpt, int* v) {
-    static const int max_span = tune("KVD_SELECT_PRE_SPAN", 1024 * kMaxKpt),
+    static const int max_span = tune("KVD_SELECT_PRE_SPAN", 8192),
                      nt_small = tune("KVD_SELECT_NT_SMALL", 512), nt_large = tune("KVD_SELECT_NT_LARGE", 1024);
     int c = 1;
     while (c < 8 && (nb_pad + c - 1) / c > max_span) c <<= 1;

@@ -91,6 +91,8 @@ __device__ __forceinline__ void kth_pick(const int* hist, KthShared& sh, int nbi
     }
 }
 
+__device__ __forceinline__ uint32_t warp_min32(uint32_t x) { return __reduce_min_sync(0xffffffffu, x); }
+__device__ __forceinline__ uint32_t warp_max32(uint32_t x) { return __reduce_max_sync(0xffffffffu, x); }
 __device__ __forceinline__ uint64_t warp_min64(uint64_t x) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) x = min(x, (uint64_t)__shfl_xor_sync(0xffffffffu, (unsigned long long)x, o));
@@ -123,20 +125,15 @@ __device__ __forceinline__ uint64_t kth_largest(const View v, int K, uint32_t km
         sh.kmin[warp] = kmn;
         sh.kmax[warp] = kmx;
     }
-    #pragma unroll 1
+#pragma unroll 1
     for (int i = tid; i < 512; i += NT) (&sh.hist[0][0])[i] = 0;
     if (tid == 0) {
         sh.nlist = 0;
         sh.nsmall = 0;
     }
     __syncthreads();
-    kmn = 0xFFFFFFFFu;
-    kmx = 0u;
-    #pragma unroll 1
-    for (int w = 0; w < nw; ++w) {
-        kmn = min(kmn, sh.kmin[w]);
-        kmx = max(kmx, sh.kmax[w]);
-    }
+    kmn = warp_min32(lane < nw ? sh.kmin[lane] : 0xFFFFFFFFu);   // every warp reduces the partials
+    kmx = warp_max32(lane < nw ? sh.kmax[lane] : 0u);
     // ---- first digit: 256 bins linear in the score value (fp32 subtract, multiply by a positive
     // scale and truncate are monotone: equal scores share a bin; NaN -> bin 0).  Without a finite
     // non-empty range every block is in one bin.
@@ -150,7 +147,7 @@ __device__ __forceinline__ uint64_t kth_largest(const View v, int K, uint32_t km
     };
     int kk = K, cnt = v.hi - v.lo, bstar = 0;
     if (lin) {
-        #pragma unroll 1
+#pragma unroll 4
         for (int i = v.lo + tid; i < v.hi; i += NT) atomicAdd(&sh.hist[0][bin_of(v.k32(i))], 1);
         __syncthreads();
         if (warp == 0) kth_pick(sh.hist[0], sh, 256, kk);
@@ -163,7 +160,7 @@ __device__ __forceinline__ uint64_t kth_largest(const View v, int K, uint32_t km
     // ---- the threshold bin's members: compacted as rank keys when they fit; their range
     const int s0 = v.lo & ~31;
     uint64_t gmn = ~0ull, gmx = 0ull;
-    #pragma unroll 1
+#pragma unroll 2
     for (int i0 = s0 + warp * 32; i0 < v.hi; i0 += NT) {
         const int i = i0 + lane;
         const bool m = i >= v.lo && i < v.hi && bin_of(v.k32(i)) == bstar;
@@ -187,13 +184,8 @@ __device__ __forceinline__ uint64_t kth_largest(const View v, int K, uint32_t km
         sh.wmax[warp] = gmx;
     }
     __syncthreads();
-    gmn = ~0ull;
-    gmx = 0ull;
-    #pragma unroll 1
-    for (int w = 0; w < nw; ++w) {
-        gmn = min(gmn, sh.wmin[w]);
-        gmx = max(gmx, sh.wmax[w]);
-    }
+    gmn = warp_min64(lane < nw ? sh.wmin[lane] : ~0ull);
+    gmx = warp_max64(lane < nw ? sh.wmax[lane] : 0ull);
     if (tid == 0) EXP_STAMP(trace, unit, 4);
     const bool compacted = cnt <= kRankList;
     const int nl = compacted ? cnt : 0;
@@ -253,9 +245,7 @@ __device__ __forceinline__ uint64_t kth_largest(const View v, int K, uint32_t km
                 mn = warp_min64(mn);
                 if (lane == 0) sh.wmin[warp] = mn;
                 __syncthreads();
-                T = ~0ull;
-#pragma unroll 1
-                for (int w = 0; w < nw; ++w) T = min(T, sh.wmin[w]);
+                T = warp_min64(lane < nw ? sh.wmin[lane] : ~0ull);
                 __syncthreads();
             }
             break;
@@ -314,7 +304,7 @@ __device__ __forceinline__ int emit_ordered(const View v, uint64_t T, KthShared&
     const int per = ((n + nw - 1) / nw + 31) & ~31;
     const int a = v.lo + warp * per, b = min(v.hi, a + per);
     int c = 0;
-    #pragma unroll 1
+#pragma unroll 4
     for (int i0 = a; i0 < b; i0 += 32) {
         const int i = i0 + lane;
         c += __popc(__ballot_sync(0xffffffffu, i < b && v.rk(i) >= T));
@@ -336,7 +326,7 @@ __device__ __forceinline__ int emit_ordered(const View v, uint64_t T, KthShared&
     int pos = sh.wcnt[warp];
     const int tot = sh.wcnt[32];
     const uint32_t lt = (1u << lane) - 1u;
-    #pragma unroll 1
+#pragma unroll 2
     for (int i0 = a; i0 < b; i0 += 32) {
         const int i = i0 + lane;
         const bool t = i < b && v.rk(i) >= T;
