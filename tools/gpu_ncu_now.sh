@@ -1,5 +1,5 @@
 tag=n1; mkdir -p gpurun_out
-K="regex:score_kernel|select_kernel|attn_kernel|cand_kernel|resolve_kernel|gather_kernel"
+K="regex:score_kernel|rank_kernel|select_kernel|attn_kernel|cand_kernel|resolve_kernel|gather_kernel"
 M="gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,pcie__read_bytes.sum,pcie__write_bytes.sum"
 timeout 900 /usr/local/cuda/bin/ncu --metrics $M --clock-control none -k "$K" -s $((4*768)) -c 768 --csv \
   --log-file gpurun_out/${tag}_launches_c2.csv python bench.py --config c2 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-isolated > gpurun_out/${tag}_ncu_c2.out 2>&1

@@ -1,6 +1,6 @@
 #!/bin/bash
 # Round evidence: GPU parity, smoke, bench lines (default c3, c2, c4, c4k, c5, alpha = 0 for c3 / c5,
-# reference), the ncu launch list of one timed step of the default command and ncu --set full
+# c4h / c3h (hierarchical index), c3q (Quest min/max), c1, reference), the ncu launch list of one timed step of the default command and ncu --set full
 # captures.  usage: tools/gpu_round.sh <tag>
 tag=${1:-r02}; mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > gpurun_out/${tag}_box.txt; nproc >> gpurun_out/${tag}_box.txt
@@ -14,9 +14,13 @@ b c4k --config c4k --no-cpu-baseline
 b c5 --config c5 --no-cpu-baseline
 b c3_alpha0 --config c3 --alpha 0 --no-cpu-baseline
 b c5_alpha0 --config c5 --alpha 0 --no-cpu-baseline
+b c4h --config c4h --no-cpu-baseline
+b c3h --config c3h --no-cpu-baseline
+b c3q --config c3q --no-cpu-baseline
+b c1 --config c1 --no-cpu-baseline
 b reference --impl reference --steps 5 --warmup 3
 M="gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,pcie__read_bytes.sum,pcie__write_bytes.sum"
-K="regex:score_kernel|select_kernel|attn_kernel|cand_kernel|resolve_kernel|gather_kernel"
+K="regex:score_kernel|rank_kernel|select_kernel|attn_kernel|cand_kernel|resolve_kernel|gather_kernel"
 # default command (c3) with 4 fill steps: skip fill (4 x 32 layers x 16 chains x 3) + 3 warm-up graph steps (x 1536),
 # then log one timed step (1536 launches: score, select, attention per layer and chain)
 timeout 1500 /usr/local/cuda/bin/ncu --metrics $M --clock-control none -k "$K" -s $((4*1536 + 3*1536)) -c 1536 --csv \

@@ -3,8 +3,8 @@ DRAM bytes (read + write) and PCIe read bytes per launch and per segment, per AB
 config, for bench.py's roofline "traffic" field.
 usage: python tools/ncu_traffic.py <tag> c2=<rep>:<segments per launch> c3=<rep>:<segs> ...
 
-Per ABI call: select = score_kernel + select_kernel (kvd_select_resolve_fetch: top-k + resolve +
-fetch; + cand_kernel with the hierarchical index), attn = attn_kernel (attention + LSE merge).
+Per ABI call: select = score_kernel + rank_kernel (kvd_select_resolve_fetch: top-k + resolve +
+fetch; select_kernel / cand_kernel on the general and index paths), attn = attn_kernel (attention + LSE merge).
 Averaged over the captured launches."""
 import csv
 import io
@@ -12,7 +12,7 @@ import json
 import subprocess
 import sys
 
-CALLS = {"select": ("select_kernel", "score_kernel", "cand_kernel"), "attn": ("attn_kernel",)}
+CALLS = {"select": ("score_kernel", "rank_kernel", "select_kernel", "cand_kernel"), "attn": ("attn_kernel",)}
 METRICS = ("dram__bytes_read.sum", "dram__bytes_write.sum", "pcie__read_bytes.sum")
 
 
@@ -47,16 +47,18 @@ def main():
         res[cfg] = {}
         for call, names in CALLS.items():
             per = {n: [(b, pc) for k, b, pc in ks if k == n] for n in names}
-            if not per[names[0]]:
+            per = {n: v for n, v in per.items() if v}
+            if not per:
                 continue
+            first = next(iter(per))
             dram = sum(sum(b for b, _ in v) / len(v) for v in per.values() if v)
             pcie = [pc for v in per.values() for _, pc in v]
-            pcie = sum(pcie) / len(per[names[0]]) if pcie and None not in pcie else None
+            pcie = sum(pcie) / len(per[first]) if pcie and None not in pcie else None
             res[cfg][call] = {"dram_bytes_per_launch": dram, "segments_per_launch": segs,
                               "dram_bytes_per_segment": dram / segs,
                               "pcie_read_bytes_per_launch": pcie,
                               "pcie_read_bytes_per_segment": None if pcie is None else pcie / segs,
-                              "launches": len(per[names[0]]),
+                              "launches": len(per[first]),
                               "kernels": " + ".join(n for n in names if per[n]) + f" ({rep.split('/')[-1]})"}
     path = f"profiles/{tag}_ncu_traffic.json"
     json.dump(res, open(path, "w"), indent=1)
