@@ -51,16 +51,16 @@ sys.path.insert(0, ROOT)
 CONFIGS = {
     "c1": dict(chains=1, L=1, B=1, Hq=8, Hkv=2, n=4096, P=16, k=32, C=None, alias=0, shard="weak",
                desc="1 req, 1 layer, 8q/2kv, d128, 4k ctx, block 16, top-k 32, resident"),
-    "c2": dict(chains=8, L=32, B=8, Hq=32, Hkv=8, n=32768, P=16, k=128, C=None, alias=0, shard="weak",
+    "c2": dict(chains=16, L=32, B=8, Hq=32, Hkv=8, n=32768, P=16, k=128, C=None, alias=0, shard="weak",
                desc="Llama-3.1-8B shapes (32 layers, 32q/8kv, d128) bf16, 32k ctx, batch 8, top-k 2048 tokens, resident"),
     "c3": dict(chains=16, L=32, B=16, Hq=32, Hkv=8, n=131072, P=16, k=128, C=2048, alias=4, shard="weak",
                desc="Llama-3.1-8B shapes, 128k ctx, batch 16, GPU cache 25% of KV (2048 slots/segment), misses "
                     "gathered from pinned host DRAM, top-k 2048 tokens"),
-    "c4": dict(chains=4, L=28, B=4, Hq=28, Hkv=4, n=1 << 20, P=16, k=128, C=16384, alias=2, shard="strong",
+    "c4": dict(chains=16, L=28, B=4, Hq=28, Hkv=4, n=1 << 20, P=16, k=128, C=16384, alias=2, shard="strong",
                desc="Qwen2.5-7B-1M shapes (28 layers, 28q/4kv, d128), 1M ctx, batch 4, GPU cache 25%, host-backed"),
-    "c4k": dict(chains=4, L=28, B=4, Hq=28, Hkv=4, n=1 << 20, P=16, k=1024, C=16384, alias=2, shard="strong",
+    "c4k": dict(chains=16, L=28, B=4, Hq=28, Hkv=4, n=1 << 20, P=16, k=1024, C=16384, alias=2, shard="strong",
                 desc="c4 with top-k 1024 blocks (16384 tokens = 1.56% of 1M, SURVEY 8.2)"),
-    "c4h": dict(chains=4, L=28, B=4, Hq=28, Hkv=4, n=1 << 20, P=16, k=128, C=16384, alias=2, shard="strong", index=4,
+    "c4h": dict(chains=16, L=28, B=4, Hq=28, Hkv=4, n=1 << 20, P=16, k=128, C=16384, alias=2, shard="strong", index=4,
                 desc="c4 with the hierarchical centroid index (k-means over block summaries, 4 blocks per centroid; "
                      "PAPER.md:388-391, DESIGN.md R27)"),
     "c3h": dict(chains=16, L=32, B=16, Hq=32, Hkv=8, n=131072, P=16, k=128, C=2048, alias=4, shard="weak", index=4,
@@ -97,7 +97,8 @@ def parse(argv=None):
     ap.add_argument("--no-isolated", action="store_true", help="skip the whole-batch per-kernel roofline pass")
     ap.add_argument("--no-graph", action="store_true", help="launch layer by layer instead of graph replay")
     ap.add_argument("--chains", type=int, default=None,
-                    help="micro-batch chains (SFC overlap): the batch is split into this many request groups, "
+                    help="micro-batch chains (SFC overlap): the batch is split into this many request groups "
+                         "(more chains than requests: one request per chain, its KV heads split into groups), "
                          "each run through all layers on its own stream inside the graph")
     ap.add_argument("--shard", default=None, choices=["weak", "strong"],
                     help="multi-GPU unit assignment (default per config): 'weak' = every rank serves its own B "
@@ -302,9 +303,13 @@ class Runner:
         self.step_dev = torch.zeros(1, dtype=torch.int32, device=dev)
         self.t = 0                     # next step index to run (query row)
         m = args.chains if args.chains else cfg.get("chains", 1)
-        m = max(1, min(m, B))
-        edges = [round(i * B / m) for i in range(m + 1)]
-        self.chains = [(edges[i], edges[i + 1]) for i in range(m) if edges[i + 1] > edges[i]]
+        m = max(1, min(m, B * Hkv))
+        if m <= B:          # request groups, every KV head
+            edges = [round(i * B / m) for i in range(m + 1)]
+            self.chains = [(edges[i], edges[i + 1], 0, Hkv) for i in range(m) if edges[i + 1] > edges[i]]
+        else:               # one request per chain, its KV heads split into hs groups (head-range calls)
+            hs = max(d for d in range(1, Hkv + 1) if Hkv % d == 0 and d <= m // B)
+            self.chains = [(b, b + 1, g * (Hkv // hs), Hkv // hs) for b in range(B) for g in range(hs)]
         self.chain_streams = [torch.cuda.Stream(device=dev) for _ in self.chains]
         self.fused = not args.unfused
         self.launches_per_step = None  # counted by libkvd (kvd_launch_count) over one eager step / the capture
@@ -315,15 +320,18 @@ class Runner:
     # one layer of one chain (requests b0..b1-1) through the ABI calls
     def layer(self, l, s, step=0, chain=None):
         c, k = self.cache, self.cfg["k"]
-        b0, b1 = chain if chain else (0, len(self.reqs))
+        b0, b1, h0, nh = chain if chain else (0, len(self.reqs), 0, self.Hkv)
+        heads = None if nh == self.Hkv else (h0, nh)     # head-range calls (kvd_*_heads)
         reqs = self.reqs[b0:b1]
         q = self.q_cur[l, b0:b1]
-        if self.fused:   # kvd_select_resolve_fetch: score, top-k, resolve and fetch in one kernel
-            c.select_resolve_fetch(l, q, reqs, k, step, self.ids[l, b0:b1], self.attn[l, b0:b1], stream=s)
+        if self.fused:   # kvd_select_resolve_fetch: score, then top-k + resolve + fetch
+            c.select_resolve_fetch(l, q, reqs, k, step, self.ids[l, b0:b1], self.attn[l, b0:b1], stream=s, heads=heads)
         else:
+            assert heads is None, "--unfused runs whole-head chains"
             c.select_topk(l, q, reqs, k, self.ids[l, b0:b1], None, stream=s)
             c.resolve_and_fetch(l, reqs, self.ids[l, b0:b1], k, step, self.attn[l, b0:b1], stream=s)
-        c.sparse_decode(l, q, reqs, self.attn[l, b0:b1], self.W, self.out[l, b0:b1], self.lse[l, b0:b1], stream=s)
+        c.sparse_decode(l, q, reqs, self.attn[l, b0:b1], self.W, self.out[l, b0:b1], self.lse[l, b0:b1], stream=s,
+                        heads=heads)
 
     def eager_step(self, s):
         torch = self.torch
@@ -578,7 +586,7 @@ def run_gpu(args):
     iso = None
     if not args.no_graph and not args.no_isolated:
         saved = (R.chains, R.chain_streams)
-        R.chains, R.chain_streams = [(0, len(R.reqs))], [torch.cuda.Stream(device=dev)]
+        R.chains, R.chain_streams = [(0, len(R.reqs), 0, R.Hkv)], [torch.cuda.Stream(device=dev)]
         R.cache.enable_kernel_timer(True)
         R.prepare_graph(s)
         for _ in range(2):

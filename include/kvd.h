@@ -213,6 +213,16 @@ kvd_status kvd_select_resolve_fetch(kvd_cache* c, int32_t layer, const uint16_t*
                                     uint32_t step, int32_t* out_ids, float* out_scores,
                                     int32_t* out_attn, kvd_stream stream);
 
+/* The fused call for the KV heads [h0, h0 + nh) only (0 <= h0, 1 <= nh, h0 + nh <= Hkv; KVD_EINVAL
+ * otherwise).  Arrays keep their full layouts (q [B][Hq][128], out_ids [B][Hkv][k_blocks], out_attn
+ * [B][Hkv][W][2]); only the range's segments are read and written, with results bit for bit those of
+ * kvd_select_resolve_fetch for those segments.  Segments are independent, so disjoint head ranges
+ * may be issued on different streams (micro-batch chains of fewer heads than a request has). */
+kvd_status kvd_select_resolve_fetch_heads(kvd_cache* c, int32_t layer, const uint16_t* q,
+                                          const int32_t* req_ids, int32_t B, int32_t h0, int32_t nh,
+                                          int32_t k_blocks, uint32_t step, int32_t* out_ids, float* out_scores,
+                                          int32_t* out_attn, kvd_stream stream);
+
 /* Decode-time append ("each step appending new key and value vectors"; DESIGN.md
  * R16): one new token for each listed request of `layer`, at position n_r (the layer's token
  * count), k / v: device bf16 [B][Hkv][128].  The token joins the always-resident local window;
@@ -246,6 +256,14 @@ int32_t kvd_attn_width(const kvd_cache* c, int32_t k_blocks);
 kvd_status kvd_sparse_decode(kvd_cache* c, int32_t layer, const uint16_t* q,
                              const int32_t* req_ids, int32_t B, const int32_t* attn,
                              int32_t W, float* out, float* out_lse, kvd_stream stream);
+
+/* kvd_sparse_decode for the KV heads [h0, h0 + nh) only (their query heads h*G .. h*G+G-1);
+ * arrays keep their full layouts (attn [B][Hkv][W][2], out [B][Hq][128], out_lse [B][Hq]).  Outputs
+ * are bit for bit those of kvd_sparse_decode for those heads (the split plan depends on k only). */
+kvd_status kvd_sparse_decode_heads(kvd_cache* c, int32_t layer, const uint16_t* q,
+                                   const int32_t* req_ids, int32_t B, int32_t h0, int32_t nh,
+                                   const int32_t* attn, int32_t W, float* out, float* out_lse,
+                                   kvd_stream stream);
 
 /* Introspection (synchronous; tests / bench only).  Copy one segment's state
  * to host buffers: table [nb_pad] int32, slot_block/last_use/use_count [C],

@@ -53,6 +53,7 @@ struct StepParams {
     int32_t sel_stride;               // stage 1: output stride per segment (m_max)
     const int32_t* sel_count;         // stage 1: centroids per segment [L][R][Hkv]
     const uint16_t* summ2;            // Quest min/max summaries (sel_mode 2): the maximum matrix
+    int32_t h0, nh;                   // the launch's KV heads [h0, h0 + nh) (arrays keep all Hkv heads)
     int32_t req[KVD_MAX_BATCH];
 };
 

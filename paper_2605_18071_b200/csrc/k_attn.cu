@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, 1) attn_kernel(StepPara
     const int crank = (int)cg::this_cluster().block_rank();
     const int ncl = (int)cg::this_cluster().num_blocks();
     const int cs = blockIdx.y;                                 // segment (request bi, KV head h)
-    const int bi = cs / p.Hkv, h = cs - bi * p.Hkv;
+    const int bi = cs / p.nh, h = p.h0 + (cs - bi * p.nh);
     const int j = crank * WARPS + warp;                         // this warp's piece
     const int ta = (j * wk.TS) / wk.NP, nt = ((j + 1) * wk.TS) / wk.NP - ta;
     uint8_t* my_stage = stage + (size_t)warp * STAGES * kTileBytes;
@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, 1) attn_kernel(StepPara
     const uint64_t pol = l2_evict_first_policy();
     const bool packed = p.G <= 4;
     const uint8_t* seg_slots = ab.slots + (((int64_t)p.layer * p.R + p.req[bi]) * p.Hkv + h) * p.C * (int64_t)rec;
-    const int2* seg_list = reinterpret_cast<const int2*>(attn) + (int64_t)cs * p.W;
+    const int2* seg_list = reinterpret_cast<const int2*>(attn) + ((int64_t)bi * p.Hkv + h) * p.W;
     if (lane == 0) EXP_STAMP(p.exp_trace, cs * 32 + j, 0);
     griddep_wait();                                // lists / slots / q come from earlier kernels
     if (lane == 0) EXP_STAMP(p.exp_trace, cs * 32 + j, 1);
@@ -405,7 +405,7 @@ static cudaError_t launch_attn_s(kvd_cache* c, const StepParams& p, const uint16
 #endif
     AttnBufs ab{c->slots, c->ntok_dev + (int64_t)p.layer * c->R, c->zero_rec};   // token counts of this layer
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(wk.NP / kAttnWarpsPerCta), (unsigned)(p.B * p.Hkv));
+    cfg.gridDim = dim3((unsigned)(wk.NP / kAttnWarpsPerCta), (unsigned)(p.B * p.nh));
     cfg.blockDim = dim3(kAttnWarpsPerCta * 32);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;

@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(kCandThreads, 1) cand_kernel(CandArgs ca, Step
     __shared__ int s_digit, s_above;
     __shared__ ResolveShared rsm;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int h = blockIdx.x, bi = blockIdx.y;
+    const int h = p.h0 + blockIdx.x, bi = blockIdx.y;
     const int r = p.req[bi];
     const int64_t seg = ((int64_t)p.layer * p.R + r) * p.Hkv + h;
     const SegGeom g = seg_geom(ntok[r], p.P, p.sink_tokens, p.local_tokens);
@@ -448,9 +448,9 @@ cudaError_t launch_index_select(kvd_cache* c, const StepParams& p, const uint16_
         smem_set[fused][dev] = smem;
     }
     const int prio = (fused && ca.fa.host_store) ? c->prio_hi : 0;
-    e = fused ? launch_pdl_prio(prio, cand_kernel<true>, dim3(p.Hkv, p.B), dim3(kCandThreads), smem, s, ca, p, q,
+    e = fused ? launch_pdl_prio(prio, cand_kernel<true>, dim3(p.nh, p.B), dim3(kCandThreads), smem, s, ca, p, q,
                                 (const int32_t*)c->ntok_dev + (int64_t)p.layer * c->R, out_ids, out_scores)
-              : launch_pdl(cand_kernel<false>, dim3(p.Hkv, p.B), dim3(kCandThreads), smem, s, ca, p, q,
+              : launch_pdl(cand_kernel<false>, dim3(p.nh, p.B), dim3(kCandThreads), smem, s, ca, p, q,
                            (const int32_t*)c->ntok_dev + (int64_t)p.layer * c->R, out_ids, out_scores);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();

@@ -15,6 +15,8 @@
 // (a4) "block-level sparse fetching ... only the blocks the queries need"
 // (PAPER.md:636-639): each missed 8 KiB record is copied from the pinned,
 // mapped host store into its slot by SM zero-copy 16-byte loads over PCIe.
+#include <cstdlib>
+
 #include "resolve.cuh"
 
 namespace kvd {
@@ -26,7 +28,7 @@ __global__ void __launch_bounds__(kResolveThreads) resolve_kernel(StepParams p, 
                                                                   int32_t* __restrict__ out_attn) {
     extern __shared__ __align__(16) uint8_t smraw[];
     __shared__ ResolveShared rsm;
-    const int bi = blockIdx.y, h = blockIdx.x;
+    const int bi = blockIdx.y, h = p.h0 + blockIdx.x;
     resolve_pre(p, rb, bi, h, rsm);
     griddep_wait();                               // ids / scores come from select
     if (threadIdx.x == 0) kt_begin(p.kt_slots, p.kt_base + kKtResolve);
@@ -47,14 +49,14 @@ __global__ void __launch_bounds__(kGatherThreads) gather_kernel(StepParams p, co
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    const int64_t total = (int64_t)p.B * p.Hkv * p.k;
+    const int64_t total = (int64_t)p.B * p.nh * p.k;
     const int chunks = p.rec_bytes / 16;
     griddep_wait();                               // miss list comes from resolve
     if (threadIdx.x == 0) kt_begin(p.kt_slots, p.kt_base + kKtGather);
     for (int64_t w = warp; w < total; w += nwarps) {
         const int i = (int)(w % p.k);
         const int64_t bh = w / p.k;
-        const int h = (int)(bh % p.Hkv), bi = (int)(bh / p.Hkv);
+        const int h = p.h0 + (int)(bh % p.nh), bi = (int)(bh / p.nh);
         const int r = p.req[bi];
         const int64_t rs = (int64_t)r * p.Hkv + h;
         if (i >= miss_count[rs]) continue;
@@ -164,7 +166,7 @@ cudaError_t launch_resolve(kvd_cache* c, const StepParams& p, const int32_t* ids
         if (e != cudaSuccess) return e;
         smem_set[dev] = smem;
     }
-    cudaError_t e = launch_pdl(resolve_kernel, dim3(p.Hkv, p.B), dim3(kResolveThreads), smem, s, p, rb, ids, out_attn);
+    cudaError_t e = launch_pdl(resolve_kernel, dim3(p.nh, p.B), dim3(kResolveThreads), smem, s, p, rb, ids, out_attn);
     if (e != cudaSuccess) return e;
     if (!c->resident) {
         e = launch_gather(c, p, s);

@@ -43,14 +43,18 @@ __global__ void __launch_bounds__(kScoreThreads, R * V > 32 ? 2 : 4)
                  const uint16_t* __restrict__ mat2, float* __restrict__ scores, const int32_t* __restrict__ ntok) {
     using Vec = typename SVec<V>::T;
     __shared__ float qbar[kHeadDim];
-    const int bi = blockIdx.z, h = blockIdx.y;
+    const int bi = blockIdx.z, h = p.h0 + blockIdx.y;
     const int r = p.req[bi];
     const int64_t seg = ((int64_t)p.layer * p.R + r) * p.Hkv + h;
     // blocks (centroids) of the segment: token counts change only in kvd_load_prefix and
     // kvd_append_token, which complete before a dependent step kernel starts
     const int64_t nb = p.sel_mode == 1 ? (int64_t)p.sel_count[seg] : ((int64_t)ntok[r] + p.P - 1) / p.P;
     const int64_t t0 = (int64_t)blockIdx.x * kScoreThreads * V;
-    if (t0 >= nb) return;                         // whole CTA past this segment's end
+    if (t0 >= nb) {                               // whole CTA past this segment's end
+        if (p.kt_slots && threadIdx.x == 0)
+            kt_end(p.kt_slots, p.kt_acc, p.kt_base + kKtScore, kKtScore, (unsigned long long)gridDim.x * gridDim.y * gridDim.z);
+        return;
+    }
     const int64_t b0 = t0 + (int64_t)threadIdx.x * V;
     const bool ld = b0 < nb;                      // V-groups never straddle the pitch (V | 128)
     const int64_t pitch = p.nb_pad;
@@ -152,9 +156,9 @@ cudaError_t launch_score(kvd_cache* c, const StepParams& p, const uint16_t* q, c
     const unsigned tiles = (unsigned)((p.nb_pad + kScoreThreads * V - 1) / (kScoreThreads * V));
     const int32_t* ntok = c->ntok_dev + (int64_t)p.layer * c->R;
     cudaError_t e = p.sel_mode == 2
-        ? launch_pdl(score_kernel<V, R / 2, true>, dim3(tiles, p.Hkv, p.B), dim3(kScoreThreads), 0, s, p, q, mat, mat2,
+        ? launch_pdl(score_kernel<V, R / 2, true>, dim3(tiles, p.nh, p.B), dim3(kScoreThreads), 0, s, p, q, mat, mat2,
                      scores, ntok)
-        : launch_pdl(score_kernel<V, R, false>, dim3(tiles, p.Hkv, p.B), dim3(kScoreThreads), 0, s, p, q, mat, mat2,
+        : launch_pdl(score_kernel<V, R, false>, dim3(tiles, p.nh, p.B), dim3(kScoreThreads), 0, s, p, q, mat, mat2,
                      scores, ntok);
     return e != cudaSuccess ? e : cudaGetLastError();
 }

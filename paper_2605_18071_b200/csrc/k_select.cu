@@ -103,7 +103,7 @@ static cudaError_t launch_select_any(kvd_cache* c, const StepParams& p, const ui
     int nt, cl, kpt, v;
     select_geometry_pre(c->nb_pad, &nt, &cl, &kpt, &v);
     if (!select_fast_ok(cl, (int64_t)nt * kpt, p.k)) {
-        select_geometry(c->nb_pad, p.B * p.Hkv, c->resident, &nt, &cl, &kpt, &v);
+        select_geometry(c->nb_pad, p.B * p.nh, c->resident, &nt, &cl, &kpt, &v);
         return nt == 512 ? launch_select_nt<512, RESOLVE>(c, p, q, c->summ, c->scores, cl, kpt, v, out_ids, out_scores, fa, s)
                          : launch_select_nt<1024, RESOLVE>(c, p, q, c->summ, c->scores, cl, kpt, v, out_ids, out_scores, fa, s);
     }
@@ -122,7 +122,7 @@ cudaError_t launch_select_centroids(kvd_cache* c, const StepParams& p, const uin
     const FuseArgs fa{};
     cudaError_t e;
     if (!select_fast_ok(cl, (int64_t)nt * kpt, c->m_max)) {
-        select_geometry(c->nc_pad, p.B * p.Hkv, true, &nt, &cl, &kpt, &v);
+        select_geometry(c->nc_pad, p.B * p.nh, true, &nt, &cl, &kpt, &v);
         e = nt == 512 ? launch_select_nt<512, false>(c, p, q, c->cent, c->cscores, cl, kpt, v, c->csel, nullptr, fa, s)
                       : launch_select_nt<1024, false>(c, p, q, c->cent, c->cscores, cl, kpt, v, c->csel, nullptr, fa, s);
     } else {

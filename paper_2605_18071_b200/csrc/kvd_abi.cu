@@ -211,7 +211,9 @@ kvd_status check_step(kvd_cache* c, int32_t layer, const int32_t* req_ids, int32
     p->scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)KVD_HEAD_DIM));
     p->kt_slots = c->kt_on ? c->kt_slots : nullptr;
     p->kt_acc = c->kt_acc;
-    p->kt_base = (layer * c->R + p->req[0]) * kKtKinds;
+    p->h0 = 0;
+    p->nh = c->Hkv;
+    p->kt_base = ((layer * c->R + p->req[0]) * c->Hkv) * kKtKinds;
     p->exp_trace = nullptr;
     p->sel_mode = c->summary_kind == 1 ? 2 : 0;   // Quest min/max scoring (R30) or mean summaries
     p->sel_ratio = 0;
@@ -471,6 +473,41 @@ kvd_status kvd_select_resolve_fetch(kvd_cache* c, int32_t layer, const uint16_t*
     return launched(launch_select_resolve(c, p, q, out_ids, out_scores, out_attn, reinterpret_cast<cudaStream_t>(stream)));
 }
 
+// KV-head range of a step call (the arrays keep their [B][Hkv] layouts; only heads [h0, h0+nh) run)
+static kvd_status set_heads(kvd_cache* c, StepParams* p, int32_t h0, int32_t nh) {
+    if (h0 < 0 || nh < 1 || h0 + nh > c->Hkv) return fail(KVD_EINVAL, "KV heads [%d, %d) outside [0, %d)", h0, h0 + nh, c->Hkv);
+    p->h0 = h0;
+    p->nh = nh;
+    p->kt_base = ((p->layer * c->R + p->req[0]) * c->Hkv + h0) * kKtKinds;   // one timer slot per launch
+    return KVD_OK;
+}
+
+kvd_status kvd_select_resolve_fetch_heads(kvd_cache* c, int32_t layer, const uint16_t* q, const int32_t* req_ids,
+                                          int32_t B, int32_t h0, int32_t nh, int32_t k_blocks, uint32_t step,
+                                          int32_t* out_ids, float* out_scores, int32_t* out_attn, kvd_stream stream) {
+    StepParams p;
+    kvd_status st = check_step(c, layer, req_ids, B, k_blocks, &p);
+    if (st) return st;
+    if ((st = set_heads(c, &p, h0, nh))) return st;
+    if (!q || (!out_ids && k_blocks > 0) || !out_attn) return fail(KVD_EINVAL, "q / out_ids / out_attn is NULL");
+    p.step = step;
+    return launched(launch_select_resolve(c, p, q, out_ids, out_scores, out_attn, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+kvd_status kvd_sparse_decode_heads(kvd_cache* c, int32_t layer, const uint16_t* q, const int32_t* req_ids, int32_t B,
+                                   int32_t h0, int32_t nh, const int32_t* attn, int32_t W, float* out, float* out_lse,
+                                   kvd_stream stream) {
+    if (!c) return fail(KVD_EINVAL, "cache is NULL");
+    const int32_t k = W - c->pmax;
+    if (k < 0) return fail(KVD_EINVAL, "W=%d smaller than max pinned %d", W, c->pmax);
+    StepParams p;
+    kvd_status st = check_step(c, layer, req_ids, B, k, &p);
+    if (st) return st;
+    if ((st = set_heads(c, &p, h0, nh))) return st;
+    if (!q || !attn || !out) return fail(KVD_EINVAL, "q / attn / out is NULL");
+    return launched(launch_attention(c, p, q, attn, out, out_lse, reinterpret_cast<cudaStream_t>(stream)));
+}
+
 kvd_status kvd_append_token(kvd_cache* c, int32_t layer, const int32_t* req_ids, int32_t B, const uint16_t* k,
                             const uint16_t* v, uint32_t step, kvd_stream stream) {
     StepParams p;
@@ -665,7 +702,7 @@ kvd_status kvd_enable_kernel_timer(kvd_cache* c, int32_t enable) {
     if (!c) return fail(KVD_EINVAL, "cache is NULL");
     KVD_CUDA(cudaSetDevice(c->cfg.device));
     KVD_CUDA(cudaDeviceSynchronize());
-    const size_t nslots = (size_t)c->L * c->R * kKtKinds;
+    const size_t nslots = (size_t)c->L * c->R * c->Hkv * kKtKinds;
     if (enable && !c->kt_slots) {
         KVD_CUDA(dalloc(&c->kt_slots, nslots * 16));
         KVD_CUDA(dalloc(&c->kt_acc, (size_t)kKtKinds * 16));

@@ -212,7 +212,7 @@ __device__ __forceinline__ void select_fast(const FuseArgs& fa, const StepParams
         if (sc_out) sc_out[pos] = __ldcg(sc_seg + id);
         if (RESOLVE) sel[pos] = (int32_t)id;
     };
-    const int unit = (bi * gridDim.y + h) * CL + crank;
+    const int unit = (bi * gridDim.y + blockIdx.y) * CL + crank;
     (void)unit;
     if (tid == 0) EXP_STAMP(p.exp_trace, unit, 2);
     const SpanView sv{skey, c_lo, c_hi, (uint32_t)base};
@@ -286,7 +286,7 @@ __device__ __forceinline__ void select_body(const FuseArgs& fa, const StepParams
     __shared__ float qbar[kHeadDim];
     const int crank = CL > 1 ? (int)cg::this_cluster().block_rank() : 0;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int h = blockIdx.y, bi = blockIdx.z;
+    const int h = p.h0 + blockIdx.y, bi = blockIdx.z;
     const int r = p.req[bi];
     const int span = NT * kpt;
     uint2* comp = reinterpret_cast<uint2*>(skey + span);
@@ -348,7 +348,7 @@ __device__ __forceinline__ void select_body(const FuseArgs& fa, const StepParams
         if (gi == 0) {
             griddep_wait();                       // summaries are immutable; q may come from an earlier kernel
             if (tid == 0) kt_begin(p.kt_slots, p.kt_base + kKtSelect);
-            if (tid == 0) EXP_STAMP(p.exp_trace, ((bi * gridDim.y + h) * CL + crank), 1);
+            if (tid == 0) EXP_STAMP(p.exp_trace, ((bi * gridDim.y + blockIdx.y) * CL + crank), 1);
             if (tid < kHeadDim) {
                 // group query: qbar[j] = ((+0 + q_0[j]) + q_1[j]) + ... (fp32, g ascending; R3)
                 const uint16_t* qh = q + ((int64_t)bi * p.Hq + (int64_t)h * p.G) * kHeadDim;
@@ -441,7 +441,7 @@ __device__ __forceinline__ void select_body(const FuseArgs& fa, const StepParams
     }
     // ---- general path (a cluster whose candidates do not fit rank 0's candidate area: K large)
     cta_minmax<CL>(kmn, kmx, sm);
-    if (tid == 0) EXP_STAMP(p.exp_trace, ((bi * gridDim.y + h) * CL + crank), 2);
+    if (tid == 0) EXP_STAMP(p.exp_trace, ((bi * gridDim.y + blockIdx.y) * CL + crank), 2);
     if (K == 0) {
         // nothing to select (the scores are still kept: lookahead victims, kvd_read_scores).  The
         // cluster barrier ends the remote min/max reads and publishes the scores to rank 0.
@@ -492,7 +492,7 @@ __device__ __forceinline__ void select_body(const FuseArgs& fa, const StepParams
         if (warp == 0) pick_digit(sm, 256, kk, lane);
         __syncthreads();
         bstar = sm.digit;
-        if (tid == 0) EXP_STAMP(p.exp_trace, ((bi * gridDim.y + h) * CL + crank), 3);
+        if (tid == 0) EXP_STAMP(p.exp_trace, ((bi * gridDim.y + blockIdx.y) * CL + crank), 3);
         kk -= sm.above;
         cnt = sm.cnt;
     }
@@ -518,7 +518,7 @@ __device__ __forceinline__ void select_body(const FuseArgs& fa, const StepParams
         if (in && slot < kListCap) comp[slot] = make_uint2(key, (uint32_t)i | (b > bstar ? 0x80000000u : 0u));
     }
     cta_minmax<CL>(kmn, kmx, sm);                 // contains the barriers that publish ncomp
-    if (tid == 0) EXP_STAMP(p.exp_trace, ((bi * gridDim.y + h) * CL + crank), 4);
+    if (tid == 0) EXP_STAMP(p.exp_trace, ((bi * gridDim.y + blockIdx.y) * CL + crank), 4);
     bool compacted = sm.ncomp <= kListCap;        // uniform over the CTA
     // ---- clusters: when the cluster's compacted lists fit one list, rank 0 gathers them (ids
     // made cluster-global) and finishes alone, with no further cluster barriers
@@ -615,7 +615,7 @@ __device__ __forceinline__ void select_body(const FuseArgs& fa, const StepParams
         cnt = sm.cnt;
         lo = shift;
     }
-    if (tid == 0) EXP_STAMP(p.exp_trace, ((bi * gridDim.y + h) * CL + crank), 5);
+    if (tid == 0) EXP_STAMP(p.exp_trace, ((bi * gridDim.y + blockIdx.y) * CL + crank), 5);
     // ---- LIST: the <= 32 threshold-bin members of the cluster, ranked by (key desc, id asc)
     if (mode == kModeList) {
         auto add = [&](uint32_t key, int i) {
@@ -803,7 +803,7 @@ __device__ __forceinline__ void select_body(const FuseArgs& fa, const StepParams
         taken_eq_before += __popc(btk);
     }
     }
-    if (tid == 0) EXP_STAMP(p.exp_trace, ((bi * gridDim.y + h) * CL + crank), 6);
+    if (tid == 0) EXP_STAMP(p.exp_trace, ((bi * gridDim.y + blockIdx.y) * CL + crank), 6);
     if constexpr (!RESOLVE) {
         griddep_launch();
         if (CL > 1 && !local) cl_sync<CL>();     // remote readers of this CTA's shared memory are done
@@ -858,7 +858,7 @@ __global__ void __launch_bounds__(NT, 1) rank_kernel(FuseArgs fa, StepParams p, 
     __shared__ ResolveShared rsm;
     const int crank = CL > 1 ? (int)cg::this_cluster().block_rank() : 0;
     const int tid = threadIdx.x;
-    const int h = blockIdx.y, bi = blockIdx.z;
+    const int h = p.h0 + blockIdx.y, bi = blockIdx.z;
     const int r = p.req[bi];
     const int span = NT * kpt;
     const int64_t base = (int64_t)crank * span;
@@ -883,7 +883,7 @@ __global__ void __launch_bounds__(NT, 1) rank_kernel(FuseArgs fa, StepParams p, 
     const int nbv = clampi((int64_t)g.nb - base, 0, span);
     const int c_lo = clampi(g.sink_end - base, 0, nbv);
     const int c_hi = clampi(g.local_begin - base, 0, nbv);
-    const int unit = (bi * gridDim.y + h) * CL + crank;
+    const int unit = (bi * gridDim.y + blockIdx.y) * CL + crank;
     (void)unit;
     if (tid == 0) EXP_STAMP(p.exp_trace, unit, 0);
     if (RESOLVE && crank == 0) resolve_pre(p, fa.rb, bi, h, rsm);
@@ -945,7 +945,7 @@ inline cudaError_t launch_rank_k(kvd_cache* c, const StepParams& p, float* score
         smem_set[dev] = smem;
     }
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(CL, p.Hkv, p.B);
+    cfg.gridDim = dim3(CL, p.nh, p.B);
     cfg.blockDim = dim3(NT);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
@@ -1005,7 +1005,7 @@ inline cudaError_t launch_select_k(kvd_cache* c, const StepParams& p, const uint
         smem_set[dev] = smem;
     }
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(CL, p.Hkv, p.B);
+    cfg.gridDim = dim3(CL, p.nh, p.B);
     cfg.blockDim = dim3(NT);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;

@@ -58,7 +58,8 @@ EXPORTS = ["kvd_required_bytes", "kvd_create_cache", "kvd_destroy_cache", "kvd_g
            "kvd_read_segment", "kvd_read_slot", "kvd_read_host_record", "kvd_read_summaries",
            "kvd_read_scores", "kvd_get_stats", "kvd_reset_stats", "kvd_check", "kvd_last_error",
            "kvd_version", "kvd_set_device_step", "kvd_launch_count",
-           "kvd_select_resolve_fetch", "kvd_enable_kernel_timer", "kvd_read_kernel_timer",
+           "kvd_select_resolve_fetch", "kvd_select_resolve_fetch_heads", "kvd_sparse_decode_heads",
+           "kvd_enable_kernel_timer", "kvd_read_kernel_timer",
            "kvd_probe_zero_copy", "kvd_read_index", "kvd_set_segment_capacity", "kvd_get_segment_stats",
            "kvd_plan_window_scaling", "kvd_read_minmax", "kvd_append_token", "kvd_load_prefix_obs",
            "kvd_read_warm_importance"]
@@ -95,6 +96,8 @@ def lib():
             "kvd_version": ([], ctypes.c_char_p),
             "kvd_launch_count": ([], ctypes.c_uint64),
             "kvd_select_resolve_fetch": ([p, i32, p, p, i32, i32, u32, p, p, p, p], i32),
+            "kvd_select_resolve_fetch_heads": ([p, i32, p, p, i32, i32, i32, i32, u32, p, p, p, p], i32),
+            "kvd_sparse_decode_heads": ([p, i32, p, p, i32, i32, i32, p, i32, p, p, p], i32),
             "kvd_enable_kernel_timer": ([p, i32], i32),
             "kvd_read_kernel_timer": ([p, p, p], i32),
             "kvd_probe_zero_copy": ([p, p, ctypes.c_size_t, i32, p], i32),
@@ -222,21 +225,32 @@ class KVCache:
                                            ptr(out_attn), _stream(stream)))
 
     def select_resolve_fetch(self, layer, q, req_ids, k_blocks, step, out_ids, out_attn, out_scores=None,
-                             stream=None):
-        """select_topk + resolve_and_fetch in one fused launch sequence (identical results)."""
+                             stream=None, heads=None):
+        """select_topk + resolve_and_fetch in one fused launch sequence (identical results).
+        heads=(h0, nh): only KV heads [h0, h0+nh) (kvd_select_resolve_fetch_heads)."""
         r, B = _reqs(req_ids)
-        _check(lib().kvd_select_resolve_fetch(self.h, layer, ptr(q), r.ctypes.data, B, k_blocks, step,
-                                              ptr(out_ids), ptr(out_scores), ptr(out_attn), _stream(stream)))
+        if heads is None:
+            _check(lib().kvd_select_resolve_fetch(self.h, layer, ptr(q), r.ctypes.data, B, k_blocks, step,
+                                                  ptr(out_ids), ptr(out_scores), ptr(out_attn), _stream(stream)))
+        else:
+            _check(lib().kvd_select_resolve_fetch_heads(self.h, layer, ptr(q), r.ctypes.data, B, heads[0], heads[1],
+                                                        k_blocks, step, ptr(out_ids), ptr(out_scores), ptr(out_attn),
+                                                        _stream(stream)))
 
     def append_token(self, layer, req_ids, k, v, step, stream=None):
         """Decode-time append of one token per request (kvd_append_token); k, v [B][Hkv][128]."""
         r, B = _reqs(req_ids)
         _check(lib().kvd_append_token(self.h, layer, r.ctypes.data, B, ptr(k), ptr(v), step, _stream(stream)))
 
-    def sparse_decode(self, layer, q, req_ids, attn, W, out, out_lse=None, stream=None):
+    def sparse_decode(self, layer, q, req_ids, attn, W, out, out_lse=None, stream=None, heads=None):
+        """heads=(h0, nh): only KV heads [h0, h0+nh) (kvd_sparse_decode_heads)."""
         r, B = _reqs(req_ids)
-        _check(lib().kvd_sparse_decode(self.h, layer, ptr(q), r.ctypes.data, B, ptr(attn), W, ptr(out),
-                                       ptr(out_lse), _stream(stream)))
+        if heads is None:
+            _check(lib().kvd_sparse_decode(self.h, layer, ptr(q), r.ctypes.data, B, ptr(attn), W, ptr(out),
+                                           ptr(out_lse), _stream(stream)))
+        else:
+            _check(lib().kvd_sparse_decode_heads(self.h, layer, ptr(q), r.ctypes.data, B, heads[0], heads[1],
+                                                 ptr(attn), W, ptr(out), ptr(out_lse), _stream(stream)))
 
     # ------------------------------------------------------------ introspection
     def read_segment(self, layer, req, head):

@@ -103,6 +103,8 @@ def test_step_calls_validate_before_launch():
     assert L.kvd_resolve_and_fetch(None, 0, reqs, 1, q, 8, 1, q, q) == 1
     assert L.kvd_select_resolve_fetch(None, 0, q, reqs, 1, 8, 1, q, q, q, q) == 1
     assert L.kvd_sparse_decode(None, 0, q, reqs, 1, q, 13, q, q, q) == 1
+    assert L.kvd_select_resolve_fetch_heads(None, 0, q, reqs, 1, 0, 1, 8, 1, q, q, q, q) == 1
+    assert L.kvd_sparse_decode_heads(None, 0, q, reqs, 1, 0, 1, q, 13, q, q, q) == 1
     assert L.kvd_launch_count() == n0
     assert b"NULL" in L.kvd_last_error() or b"null" in L.kvd_last_error()
 

@@ -162,3 +162,36 @@ def test_c4h_fullsize_hierarchical_index():
         gc, gof = R.cache.read_index(0, o.b, o.h, len(o.index[1]))
         assert np.array_equal(gc, o.index[0]) and np.array_equal(gof, o.index[1])
     run_checked(R, samples, n_eager=3, n_graph=2)
+
+
+@pytest.mark.parametrize("config,chains", [("c3", 32), ("c4", 16)])
+def test_head_range_chains_bitwise(config, chains):
+    # kvd_*_heads: chains of one request's KV-head subset (c3: 2 groups of 4 heads, c4: one head per
+    # chain) give the whole-head chains' ids, attention lists, outputs and cache state bit for bit
+    layers = 2 if config == "c3" else 1
+    A, cfg, _ = make_runner(config, layers, ["--fill", "6", "--chains", str(chains)])
+    B, _, _ = make_runner(config, layers, ["--fill", "6", "--chains", str(cfg["B"])])
+    assert any(ch[3] < cfg["Hkv"] for ch in A.chains) and all(ch[3] == cfg["Hkv"] for ch in B.chains)
+    s = torch.cuda.Stream()
+    for _ in range(6):
+        A.eager_step(s)
+        B.eager_step(s)
+    A.prepare_graph(s)
+    B.prepare_graph(s)
+    for _ in range(3):
+        A.graph_step(s)
+        B.graph_step(s)
+        s.synchronize()
+        assert torch.equal(A.ids, B.ids)
+        assert torch.equal(A.attn, B.attn)
+        assert torch.equal(A.out, B.out)
+        assert torch.equal(A.lse, B.lse)
+    assert A.cache.stats() == B.cache.stats()
+
+
+def test_c2_head_range_chains_oracle():
+    # c2 with 16 chains (8 requests x 2 groups of 4 KV heads), graph: sampled segments vs the oracle
+    R, cfg, args = make_runner("c2", 2, ["--chains", "16"])
+    assert len(R.chains) == 16
+    samples = [OracleSegment(R, cfg, args, l, b, h) for (l, b, h) in [(0, 0, 3), (1, 5, 4), (1, 7, 7)]]
+    run_checked(R, samples, n_eager=1, n_graph=2)

@@ -1,7 +1,7 @@
 tag=n1; mkdir -p gpurun_out
 K="regex:score_kernel|rank_kernel|select_kernel|attn_kernel|cand_kernel|resolve_kernel|gather_kernel"
 M="gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,pcie__read_bytes.sum,pcie__write_bytes.sum"
-timeout 900 /usr/local/cuda/bin/ncu --metrics $M --clock-control none -k "$K" -s $((4*768)) -c 768 --csv \
+timeout 900 /usr/local/cuda/bin/ncu --metrics $M --clock-control none -k "$K" -s $((4*1536)) -c 1536 --csv \
   --log-file gpurun_out/${tag}_launches_c2.csv python bench.py --config c2 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-isolated > gpurun_out/${tag}_ncu_c2.out 2>&1
 echo "launch list c2 rc $?"; python tools/ncu_summary.py gpurun_out/${tag}_launches_c2.csv
 for c in c2 c3 c4; do

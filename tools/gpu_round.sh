@@ -26,7 +26,7 @@ K="regex:score_kernel|rank_kernel|select_kernel|attn_kernel|cand_kernel|resolve_
 timeout 1500 /usr/local/cuda/bin/ncu --metrics $M --clock-control none -k "$K" -s $((4*1536 + 3*1536)) -c 1536 --csv \
   --log-file gpurun_out/${tag}_launches_default.csv python bench.py --fill 4 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-isolated > gpurun_out/${tag}_ncu_default.out 2>&1
 echo "launch list rc $?"; python tools/ncu_summary.py gpurun_out/${tag}_launches_default.csv > gpurun_out/${tag}_launches_default_summary.txt; cat gpurun_out/${tag}_launches_default_summary.txt
-timeout 900 /usr/local/cuda/bin/ncu --metrics $M --clock-control none -k "$K" -s $((4*768)) -c 768 --csv \
+timeout 900 /usr/local/cuda/bin/ncu --metrics $M --clock-control none -k "$K" -s $((4*1536)) -c 1536 --csv \
   --log-file gpurun_out/${tag}_launches_c2.csv python bench.py --config c2 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-isolated > gpurun_out/${tag}_ncu_c2.out 2>&1
 echo "launch list c2 rc $?"; python tools/ncu_summary.py gpurun_out/${tag}_launches_c2.csv > gpurun_out/${tag}_launches_c2_summary.txt; cat gpurun_out/${tag}_launches_c2_summary.txt
 # --set full: whole-batch launches (eager, chains = 1, same kernels as the graph) of c2, c3, c4 after

@@ -59,7 +59,7 @@ def main():
                               "pcie_read_bytes_per_launch": pcie,
                               "pcie_read_bytes_per_segment": None if pcie is None else pcie / segs,
                               "launches": len(per[first]),
-                              "kernels": " + ".join(n for n in names if per[n]) + f" ({rep.split('/')[-1]})"}
+                              "kernels": " + ".join(per) + f" ({rep.split('/')[-1]})"}
     path = f"profiles/{tag}_ncu_traffic.json"
     json.dump(res, open(path, "w"), indent=1)
     print(path, json.dumps(res, indent=1))
