@@ -19,12 +19,12 @@ b c3h --config c3h --no-cpu-baseline
 b c3q --config c3q --no-cpu-baseline
 b c1 --config c1 --no-cpu-baseline
 b reference --impl reference --steps 5 --warmup 3
-M="gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,pcie__read_bytes.sum,pcie__write_bytes.sum"
+M="gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,pcie__read_bytes.sum,pcie__write_bytes.sum,syslts__d_sectors_fill_sysmem.sum"
 K="regex:score_kernel|rank_kernel|select_kernel|attn_kernel|cand_kernel|resolve_kernel|gather_kernel"
-# default command (c3) with 4 fill steps: skip fill (4 x 32 layers x 16 chains x 3) + 3 warm-up graph steps (x 1536),
+# default command (c3, 32 fill steps: steady-state misses): skip fill (32 x 32 layers x 16 chains x 3) + 3 warm-up graph steps (x 1536),
 # then log one timed step (1536 launches: score, select, attention per layer and chain)
-timeout 1500 /usr/local/cuda/bin/ncu --metrics $M --clock-control none -k "$K" -s $((4*1536 + 3*1536)) -c 1536 --csv \
-  --log-file gpurun_out/${tag}_launches_default.csv python bench.py --fill 4 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-isolated > gpurun_out/${tag}_ncu_default.out 2>&1
+timeout 1500 /usr/local/cuda/bin/ncu --metrics $M --clock-control none -k "$K" -s $((32*1536 + 3*1536)) -c 1536 --csv \
+  --log-file gpurun_out/${tag}_launches_default.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-isolated > gpurun_out/${tag}_ncu_default.out 2>&1
 echo "launch list rc $?"; python tools/ncu_summary.py gpurun_out/${tag}_launches_default.csv > gpurun_out/${tag}_launches_default_summary.txt; cat gpurun_out/${tag}_launches_default_summary.txt
 timeout 900 /usr/local/cuda/bin/ncu --metrics $M --clock-control none -k "$K" -s $((4*1536)) -c 1536 --csv \
   --log-file gpurun_out/${tag}_launches_c2.csv python bench.py --config c2 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-isolated > gpurun_out/${tag}_ncu_c2.out 2>&1
@@ -37,4 +37,5 @@ for c in c2 c3 c4; do
   echo "full $c rc $?"
   python tools/ncu_details.py gpurun_out/${tag}_full_$c.ncu-rep > gpurun_out/${tag}_full_$c.txt 2>&1
 done
-python tools/ncu_traffic.py ${tag} c2=gpurun_out/${tag}_full_c2.ncu-rep:64 c3=gpurun_out/${tag}_full_c3.ncu-rep:128 c4=gpurun_out/${tag}_full_c4.ncu-rep:16 > gpurun_out/${tag}_traffic.log 2>&1; cp profiles/${tag}_ncu_traffic.json gpurun_out/ 2>/dev/null
+python tools/ncu_traffic.py ${tag} c2=gpurun_out/${tag}_full_c2.ncu-rep:64 c3=gpurun_out/${tag}_full_c3.ncu-rep:128 c4=gpurun_out/${tag}_full_c4.ncu-rep:16 \
+  --link c3=gpurun_out/${tag}_launches_default.csv:8 > gpurun_out/${tag}_traffic.log 2>&1; cp profiles/${tag}_ncu_traffic.json gpurun_out/ 2>/dev/null

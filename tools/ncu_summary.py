@@ -20,11 +20,12 @@ def summarise(path):
         wr = sum(m.get("dram__bytes_write.sum", [0])) / len(t)
         pr = sum(m.get("pcie__read_bytes.sum", [0])) / len(t)
         pw = sum(m.get("pcie__write_bytes.sum", [0])) / len(t)
+        sy = 32 * sum(m.get("syslts__d_sectors_fill_sysmem.sum", [0])) / len(t)   # host-memory reads
         avg = sum(t) / len(t)
-        out.append((n, len(t), avg, sum(t) / tot, rd, wr, pr, pw))
+        out.append((n, len(t), avg, sum(t) / tot, rd, wr, pr, pw, sy))
         print(f"  {n:16s} n={len(t):4d} avg={avg / 1e3:9.2f} us share={sum(t) / tot:.3f} "
               f"dram rd={rd / 1e6:8.2f} MB wr={wr / 1e6:7.2f} MB -> {(rd + wr) / avg:7.1f} GB/s"
-              f"  pcie rd={pr / 1e6:7.2f} MB wr={pw / 1e6:6.2f} MB -> {(pr + pw) / avg:6.1f} GB/s")
+              f"  pcie rd={pr / 1e6:7.2f} MB wr={pw / 1e6:6.2f} MB  sysmem rd={sy / 1e6:7.2f} MB -> {sy / avg:6.1f} GB/s")
     return out
 
 

@@ -36,10 +36,31 @@ def kernels(rep):
     return out
 
 
+def link_bytes(csv_path):
+    """Mean host-memory bytes read (syslts__d_sectors_fill_sysmem x 32 B) per rank_kernel launch
+    of an ncu launch list (the fused miss gather's zero-copy reads over PCIe)."""
+    sys.path.insert(0, "tools")
+    import ncu_summary
+    import contextlib
+    import io as _io
+    with contextlib.redirect_stdout(_io.StringIO()):
+        rows = ncu_summary.summarise(csv_path)
+    for name, n, avg, share, rd, wr, pr, pw, sy in rows:
+        if name.endswith("rank_kernel"):
+            return sy, n
+    return None, 0
+
+
 def main():
     tag = sys.argv[1]
     res = {}
-    for a in sys.argv[2:]:
+    args = sys.argv[2:]
+    links = []
+    if "--link" in args:
+        i = args.index("--link")
+        links = args[i + 1:]
+        args = args[:i]
+    for a in args:
         cfg, spec = a.split("=", 1)
         rep, segs = spec.rsplit(":", 1)
         segs = int(segs)
@@ -60,6 +81,15 @@ def main():
                               "pcie_read_bytes_per_segment": None if pcie is None else pcie / segs,
                               "launches": len(per[first]),
                               "kernels": " + ".join(per) + f" ({rep.split('/')[-1]})"}
+    for a in links:                                # host-link reads of the select call (launch list)
+        cfg, spec = a.split("=", 1)
+        csv_path, segs = spec.rsplit(":", 1)
+        sy, n = link_bytes(csv_path)
+        if sy is not None and cfg in res and "select" in res[cfg]:
+            e = res[cfg]["select"]
+            e["pcie_read_bytes_per_launch_source"] = f"syslts__d_sectors_fill_sysmem x 32 B, {n} rank_kernel launches " \
+                                                     f"of {csv_path.split('/')[-1]} ({segs} segments each)"
+            e["pcie_read_bytes_per_segment"] = sy / int(segs)
     path = f"profiles/{tag}_ncu_traffic.json"
     json.dump(res, open(path, "w"), indent=1)
     print(path, json.dumps(res, indent=1))
