@@ -760,8 +760,13 @@ def run_reference(args):
     L, B, Hkv = cfg["L"], cfg["B"], cfg["Hkv"]
     w1, n1 = OracleSample(args, cfg, 1).run(1)
     per_wall = w1 / n1 / cores                    # ~ seconds per segment-step on all cores
-    budget = min(8.0, 150.0 / max(1, args.steps + args.warmup))   # whole run within a few minutes
-    ntasks = max(cores, int(budget / (3 * per_wall)))
+    seg_steps_per_step = B * Hkv * L
+    # a step = one decode step's worth of segment-steps (B x Hkv x L, in runs of 3 steps), unless
+    # that would not fit the budget (whole run within a few minutes): then a proportional sample
+    budget = min(8.0, 150.0 / max(1, args.steps + args.warmup))
+    ntasks = -(-seg_steps_per_step // 3)
+    if ntasks * 3 * per_wall > budget:
+        ntasks = max(cores, int(budget / (3 * per_wall)))
     sample = OracleSample(args, cfg, ntasks)
     for _ in range(args.warmup):
         sample.run(cores)
@@ -770,7 +775,6 @@ def run_reference(args):
         w, done = sample.run(cores)
         walls.append(w)
     wall = float(np.mean(walls))
-    seg_steps_per_step = B * Hkv * L
     v = B / (wall / done * seg_steps_per_step)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall * 1e3,
@@ -780,8 +784,8 @@ def run_reference(args):
             "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": cores, "kind": "oracle",
                              "sample": f"each step: {done} segment-steps ({ntasks} runs of 3 steps over "
                                        f"{len(sample.segs)} layer-0 segments) on {cores} threads, {wall:.2f} s "
-                                       f"wall (= ms_per_step); value scales it to the {seg_steps_per_step} "
-                                       f"segment-steps of one decode step"},
+                                       f"wall (= ms_per_step); one decode step is {seg_steps_per_step} "
+                                       f"segment-steps (B x Hkv x L), value = B / (wall per decode step)"},
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 

@@ -252,7 +252,9 @@ int32_t kvd_attn_width(const kvd_cache* c, int32_t k_blocks);
  * from resolve, W == kvd_attn_width(c, k) for the k used there.  For every query head: softmax(q K^T / sqrt(128)) V over the
  * tokens of the listed blocks (partial last block masked), split-K over the
  * list with a log-sum-exp merge.  out: device fp32 [B][Hq][128];
- * out_lse: device fp32 [B][Hq] (natural log) or NULL. */
+ * out_lse: device fp32 [B][Hq] (natural log) or NULL.  q is read before the kernel waits on its
+ * stream predecessor (programmatic dependent launch): pass the q of this step's select call, not a
+ * buffer written by the kernel launched immediately before this call. */
 kvd_status kvd_sparse_decode(kvd_cache* c, int32_t layer, const uint16_t* q,
                              const int32_t* req_ids, int32_t B, const int32_t* attn,
                              int32_t W, float* out, float* out_lse, kvd_stream stream);

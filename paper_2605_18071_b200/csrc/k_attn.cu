@@ -68,7 +68,7 @@ struct Work {
 constexpr int kPartFloats = 8 * kHeadDim + 16;
 
 template <int STAGES>
-__global__ void __launch_bounds__(kAttnWarpsPerCta * 32, 1) attn_kernel(StepParams p, AttnBufs ab, Work wk,
+__global__ void __launch_bounds__(kAttnWarpsPerCta * 32, STAGES == 2 ? 3 : 1) attn_kernel(StepParams p, AttnBufs ab, Work wk,
                                                                          const uint16_t* __restrict__ q,
                                                                          const int32_t* __restrict__ attn,
                                                                          float* __restrict__ out,
@@ -95,11 +95,25 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, 1) attn_kernel(StepPara
     const int logP = __ffs(p.P) - 1, logE = 4 - logP, logCT = 7 - logE;
     const int E = 1 << logE, rec = p.rec_bytes, CT = 1 << logCT;
     const uint64_t pol = l2_evict_first_policy();
-    const bool packed = p.G <= 4;
     const uint8_t* seg_slots = ab.slots + (((int64_t)p.layer * p.R + p.req[bi]) * p.Hkv + h) * p.C * (int64_t)rec;
     const int2* seg_list = reinterpret_cast<const int2*>(attn) + ((int64_t)bi * p.Hkv + h) * p.W;
     if (lane == 0) EXP_STAMP(p.exp_trace, cs * 32 + j, 0);
-    griddep_wait();                                // lists / slots / q come from earlier kernels
+    const bool packed = p.G <= 4;
+    const int quad = lane & 3;                              // accumulator columns 2 quad, 2 quad + 1
+    // Q^T B-fragments: column n = lane/4 -> head n (packed: n & 3), dims 16 kk + 2 quad + {0,1} (+8).
+    // q is the query the select call read, two kernels back in the stream (every step kernel waits
+    // on its predecessor before triggering this one), so it is loaded before the wait.
+    uint32_t qf[8][2];
+    {
+        const int hd = packed ? (lane >> 2) & 3 : lane >> 2;
+        const uint16_t* qh = q + ((int64_t)bi * p.Hq + (int64_t)h * p.G + hd) * kHeadDim + 2 * quad;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+            qf[kk][0] = hd < p.G ? *reinterpret_cast<const uint32_t*>(qh + 16 * kk) : 0u;
+            qf[kk][1] = hd < p.G ? *reinterpret_cast<const uint32_t*>(qh + 16 * kk + 8) : 0u;
+        }
+    }
+    griddep_wait();                                // lists / slots come from the select call
     if (lane == 0) EXP_STAMP(p.exp_trace, cs * 32 + j, 1);
     if (threadIdx.x == 0) kt_begin(p.kt_slots, p.kt_base + kKtAttn);
 
@@ -149,22 +163,10 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, 1) attn_kernel(StepPara
     const uint32_t vswz = (uint32_t)((rv & pm) & 7);
     const int kchunk_hi = mi >> 1, vchunk_hi = mi & 1;
     const int row_lo = lane >> 2, row_hi = row_lo + 8;     // token rows of this lane's accumulators
-    const int quad = lane & 3;                              // accumulator columns 2 quad, 2 quad + 1
     const bool lo_lane = packed && quad >= 2;               // packed: this lane's columns carry P_lo
     const float kLn2 = 0.69314718055994531f;
     const int n_cur = ab.ntok[p.req[bi]];
 
-    // Q^T B-fragments: column n = lane/4 -> head n (packed: n & 3), dims 16 kk + 2 quad + {0,1} (+8)
-    uint32_t qf[8][2];
-    {
-        const int hd = packed ? (lane >> 2) & 3 : lane >> 2;
-        const uint16_t* qh = q + ((int64_t)bi * p.Hq + (int64_t)h * p.G + hd) * kHeadDim + 2 * quad;
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-            qf[kk][0] = hd < p.G ? *reinterpret_cast<const uint32_t*>(qh + 16 * kk) : 0u;
-            qf[kk][1] = hd < p.G ? *reinterpret_cast<const uint32_t*>(qh + 16 * kk + 8) : 0u;
-        }
-    }
     float oacc[8][4];
 #pragma unroll
     for (int mt = 0; mt < 8; ++mt) oacc[mt][0] = oacc[mt][1] = oacc[mt][2] = oacc[mt][3] = 0.f;
@@ -427,7 +429,12 @@ static cudaError_t launch_attn_s(kvd_cache* c, const StepParams& p, const uint16
 cudaError_t launch_attention(kvd_cache* c, const StepParams& p, const uint16_t* q, const int32_t* attn, float* out,
                              float* out_lse, cudaStream_t s) {
     // 4 warps x 3 stages of 8 KiB per CTA, 2 CTAs per SM (the per-warp dependent chain of MMA +
-    // softmax needs >= 2 warps per scheduler; measured round 1)
+    // softmax needs >= 2 warps per scheduler; measured round 1).  KVD_ATTN_STAGES=2 (experiment
+    // builds): 2 stages, 3 CTAs per SM (167 registers, no spills).
+#ifdef KVD_EXPERIMENTS
+    if (const char* e = getenv("KVD_ATTN_STAGES"))
+        if (atoi(e) == 2) return launch_attn_s<2>(c, p, q, attn, out, out_lse, s);
+#endif
     return launch_attn_s<3>(c, p, q, attn, out, out_lse, s);
 }
 
