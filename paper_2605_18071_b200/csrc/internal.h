@@ -54,6 +54,10 @@ struct StepParams {
     const int32_t* sel_count;         // stage 1: centroids per segment [L][R][Hkv]
     const uint16_t* summ2;            // Quest min/max summaries (sel_mode 2): the maximum matrix
     int32_t h0, nh;                   // the launch's KV heads [h0, h0 + nh) (arrays keep all Hkv heads)
+    // 1: every step kernel triggers its dependent launch right after its own griddepcontrol.wait
+    // (the dependent's CTAs become resident and run their prologue while this kernel works; they
+    // still wait for its completion).  c2 +3 %, c4 +7 %, c3 unchanged.  2: score / attention only.
+    int32_t early_trigger;
     int32_t req[KVD_MAX_BATCH];
 };
 

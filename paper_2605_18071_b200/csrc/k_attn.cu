@@ -114,6 +114,7 @@ __global__ void __launch_bounds__(kAttnWarpsPerCta * 32, STAGES == 2 ? 3 : 1) at
         }
     }
     griddep_wait();                                // lists / slots come from the select call
+    if (p.early_trigger) griddep_launch();
     if (lane == 0) EXP_STAMP(p.exp_trace, cs * 32 + j, 1);
     if (threadIdx.x == 0) kt_begin(p.kt_slots, p.kt_base + kKtAttn);
 

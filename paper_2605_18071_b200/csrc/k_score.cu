@@ -69,6 +69,7 @@ __global__ void __launch_bounds__(kScoreThreads, R * V > 32 ? 2 : 4)
     for (int u = 0; u < R; ++u)
         if (ld) bufB[u] = QUEST ? __ldcs(src2 + u * rstride) : __ldcs(src + (R + u) * rstride);
     griddep_wait();                               // q may come from an earlier kernel of the step
+    if (p.early_trigger) griddep_launch();
     if (threadIdx.x == 0) kt_begin(p.kt_slots, p.kt_base + kKtScore);
     if (threadIdx.x < kHeadDim) {
         // group query: qbar[j] = ((+0 + q_0[j]) + q_1[j]) + ... (fp32, g ascending; R3)

@@ -213,6 +213,10 @@ kvd_status check_step(kvd_cache* c, int32_t layer, const int32_t* req_ids, int32
     p->kt_acc = c->kt_acc;
     p->h0 = 0;
     p->nh = c->Hkv;
+    p->early_trigger = 1;
+#ifdef KVD_EXPERIMENTS
+    if (const char* e = getenv("KVD_EARLY_TRIGGER")) p->early_trigger = atoi(e);
+#endif
     p->kt_base = ((layer * c->R + p->req[0]) * c->Hkv) * kKtKinds;
     p->exp_trace = nullptr;
     p->sel_mode = c->summary_kind == 1 ? 2 : 0;   // Quest min/max scoring (R30) or mean summaries

@@ -888,6 +888,7 @@ __global__ void __launch_bounds__(NT, 1) rank_kernel(FuseArgs fa, StepParams p, 
     if (tid == 0) EXP_STAMP(p.exp_trace, unit, 0);
     if (RESOLVE && crank == 0) resolve_pre(p, fa.rb, bi, h, rsm);
     griddep_wait();                                // the scores come from score_kernel
+    if (p.early_trigger == 1) griddep_launch();
     if (tid == 0) kt_begin(p.kt_slots, p.kt_base + kKtSelect);
     if (tid == 0) EXP_STAMP(p.exp_trace, unit, 1);
     // ---- this CTA's scores -> monotone keys in shared memory (16-byte loads; base and the row
