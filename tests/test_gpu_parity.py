@@ -230,6 +230,15 @@ def test_topk_cluster_mixed_list_overflow(monkeypatch, fused):
     c.run(steps=2)
 
 
+# ---- the general top-k path (self-scoring select_kernel): a cluster whose candidates would not
+# fit rank 0's candidate area (k x cluster size > 8192) -- P = 1, 40,000 blocks in a cluster of 8,
+# k = 2000 -- resident and host-backed, both call paths
+@pytest.mark.parametrize("fused,C", [(False, None), (True, None), (True, 3000), (False, 3000)])
+def test_general_select_path_large_k(fused, C):
+    c = Case(L=1, B=2, Hq=8, Hkv=2, n=40000, P=1, k=2000, C=C, policy="la", seed=24, ragged=True, fused=fused)
+    c.run(steps=2)
+
+
 # ---- the split-K plan is a function of the segment (its k) only: a request attended alone and
 # the same request inside a 16-request call give bit-identical outputs
 @pytest.mark.parametrize("fused", [False, True])
