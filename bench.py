@@ -76,7 +76,7 @@ METRIC = "decode tokens/s at 128k ctx; sparse-attn HBM GB/s % peak; fetch GB/s, 
 RECORD = 8192           # bytes of one 16-token K||V block record (bf16)
 SUMMARY = 256           # bytes of one block summary (128 bf16)
 KINDS = ("score", "select", "resolve", "gather", "attn")
-KIND_NAMES = {"score": "score_kernel (a1)", "select": "select_kernel (a2; fused: +a3+a4)",
+KIND_NAMES = {"score": "score_kernel (a1)", "select": "rank_kernel (a2; fused: +a3+a4)",
               "resolve": "resolve_kernel (a3)", "gather": "gather_kernel (a4)", "attn": "attn_kernel (a5+a6)"}
 
 
@@ -150,7 +150,7 @@ def per_segment_bytes(cfg, misses_per_seg=0.0, victims=True):
     return dict(
         select=SUMMARY * sel_blocks + 2 * G * 128 + 8 * k,  # summaries (or centroids + members) + q + ids
         # the kernels of the select call: score_kernel streams the summaries and writes fp32 scores;
-        # select_kernel ranks them from L2 and writes the ids
+        # rank_kernel ranks them from L2 and writes the ids
         score=SUMMARY * sel_blocks + 2 * G * 128 + 4 * nb,
         topk=8 * k,
         resolve=4 * k + (0 if resident or not victims else 13 * C + 4 * C),   # table probes + victim scan (LA)
